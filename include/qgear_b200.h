@@ -1,0 +1,153 @@
+/*
+ * qgear_b200.h — C ABI of libqgear_b200.so, the B200-native executor for the
+ * Q-Gear state-vector hot path (arXiv 2504.03967).
+ *
+ * The reference has no FFI: its executor is pure Python/numpy
+ * (/root/reference/pkg/src/qgear/statevec.py, partition.py).  Each entry
+ * point below names the reference function/loop it replaces; the Python
+ * package paper_2504_03967_b200 binds them with ctypes and keeps the
+ * reference's Python signatures on top.
+ *
+ * Conventions (Appendix A of SURVEY.md):
+ *   - qubit k is bit k of the basis index (statevec.py:5-8);
+ *   - a state (or one rank's shard) is a contiguous device array of 2^n_local
+ *     complex amplitudes, interleaved (re, im): float pairs for
+ *     QG_DTYPE_C64 ("fp32", statevec.py:34) or double pairs for QG_DTYPE_C128
+ *     ("fp64");
+ *   - gate_type rows are (kind, control or -1, target) int32, gate_param is
+ *     float64 (ir.py:281-303); kinds H=0 RX=1 RY=2 RZ=3 CX=4 CR1=5
+ *     MEASURE=6 (ir.py:31-40);
+ *   - all device pointers are plain CUDA device pointers, `stream` is a
+ *     cudaStream_t (NULL = legacy default stream);
+ *   - every function returns QG_OK (0) or a negative QG_E_* code; the message
+ *     of the last failure on the calling thread is qg_last_error().
+ */
+#ifndef QGEAR_B200_H
+#define QGEAR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QG_ABI_VERSION 1
+
+/* status codes -> Python exceptions (paper_2504_03967_b200/errors.py) */
+#define QG_OK 0
+#define QG_E_INVALID_ARG -1          /* ValueError */
+#define QG_E_INDEX_OUT_OF_RANGE -2   /* IndexOutOfRangeError   statevec.py:149-160 */
+#define QG_E_SELF_PAIR -3            /* SelfPairError          statevec.py:159-160 */
+#define QG_E_MEASURE_MID_CIRCUIT -4  /* MeasureMidCircuitError statevec.py:187-197 */
+#define QG_E_TOO_MANY_QUBITS -5      /* TooManyQubitsError     statevec.py:89-91 */
+#define QG_E_UNNORMALIZED -6         /* UnnormalizedStateError statevec.py:226-228 */
+#define QG_E_BAD_WORKER_COUNT -7     /* BadWorkerCountError    partition.py:82-86 */
+#define QG_E_CORRUPT_TENSOR -8       /* CorruptTensorError     ir.py:264-273, 339-345 */
+#define QG_E_PROTOCOL -9             /* ProtocolViolationError partition.py:168-173 */
+#define QG_E_CUDA -10                /* CUDA runtime / launch failure */
+#define QG_E_NONFINITE_PARAM -11     /* NonFiniteParamError */
+#define QG_E_INVALID_GATE -12        /* InvalidGateError */
+#define QG_E_OUT_OF_MEMORY -13
+
+#define QG_DTYPE_C64 0
+#define QG_DTYPE_C128 1
+
+typedef struct qg_plan qg_plan;
+
+typedef struct {
+    int32_t dtype;            /* QG_DTYPE_C64 / QG_DTYPE_C128 */
+    int32_t log2_ranks;       /* number of global (sharded) qubits; 0 = one device */
+    int32_t fuse;             /* 1 = fused multi-gate passes (default); 0 = one kernel per gate */
+    int32_t tile_qubits;      /* 0 = auto; else force the tile width k of fused passes */
+    int32_t max_stages;       /* 0 = auto; register stages per pass (SMEM transposes + 1) */
+    int32_t max_cost;         /* 0 = auto; per-amplitude instruction budget of one pass */
+    int32_t reserved[6];
+} qg_plan_opts;
+
+typedef struct {
+    int64_t n_body_gates;     /* live gates before the trailing MEASURE block */
+    int64_t n_passes;         /* fused-pass (or single-gate) kernel launches per execute */
+    int64_t n_segments;       /* passes between two remaps = n_remaps + 1 */
+    int64_t n_remaps;         /* qubit-remap all-to-alls (multi-rank only) */
+    int64_t n_ops;            /* register-level ops after fusion */
+    int64_t n_stages;         /* total register stages over all passes */
+    int32_t tile_qubits;      /* k of the fused kernel chosen */
+    int32_t n_local;          /* qubits per shard */
+    int32_t n_qubits;
+    int32_t dtype;
+} qg_plan_info;
+
+/* one qubit-remap between segment `seg` and `seg + 1`: physical local
+ * positions n_local-s .. n_local-1 swap with the global positions in
+ * `global_pos[0..s-1]` (same order). */
+typedef struct {
+    int32_t s;
+    int32_t global_pos[8];
+    int32_t local_pos[8];
+} qg_remap;
+
+typedef struct {
+    double pass_ms;           /* summed CUDA-event time of fused-pass launches (0 if not timed) */
+    int64_t pass_launches;    /* kernels launched by qg_plan_execute*, this call */
+    int64_t bytes_moved;      /* algorithmic HBM bytes of those launches (2 x shard bytes each) */
+} qg_exec_stats;
+
+/* ---- planner: replaces the per-gate dispatch loop statevec.py:207-208 and the
+ *      per-gate LOCAL/EXCHANGE tagging partition.py:100-109 ---------------- */
+int qg_plan_create(const int32_t* gate_type, const double* gate_param, int64_t n_gates,
+                   int32_t n_qubits, const qg_plan_opts* opts, qg_plan** out);
+int qg_plan_destroy(qg_plan* plan);
+int qg_plan_get_info(const qg_plan* plan, qg_plan_info* out);
+int qg_plan_get_remap(const qg_plan* plan, int64_t remap_index, qg_remap* out);
+/* logical qubit q sits at physical position phys_of_logical[q] after the last
+ * segment (identity unless remaps ran); n_qubits entries */
+int qg_plan_get_final_map(const qg_plan* plan, int32_t* phys_of_logical);
+/* debug/test export of the fused program at op granularity (physical qubits):
+ *   rec[i*8 + ...] = {pass, stage, kind, target, control, cmask, qmask, mat}
+ *   mats[m*8 + ...] = 2x2 (or diagonal / phase) coefficients in float64
+ * Call with NULL buffers to get the counts. */
+int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* mats, int64_t* n_mats);
+
+/* ---- execution ------------------------------------------------------------ */
+/* init_zero_state (statevec.py:81-94) for one shard: amplitude 0 = 1 on rank 0 */
+int qg_state_init_zero(void* state, int32_t n_local, int32_t dtype, int32_t rank, void* stream);
+/* run one segment of the plan (all passes on one device): replaces statevec.py:207-208
+ * (and the per-worker loop partition.py:265-274 for the LOCAL part) */
+int qg_plan_execute_segment(const qg_plan* plan, int64_t segment, void* state, int32_t rank,
+                            void* stream, int32_t timed, qg_exec_stats* stats);
+/* all segments back to back (single device, log2_ranks == 0) */
+int qg_plan_execute(const qg_plan* plan, void* state, void* stream, int32_t timed, qg_exec_stats* stats);
+
+/* ---- the reference's array kernels (statevec.py:115-144), one launch each ----- */
+/* u = 2x2 complex row-major as 8 doubles (re00, im00, re01, im01, re10, im10, re11, im11) */
+int qg_apply_matrix(void* state, int32_t n_local, int32_t dtype, int32_t target, const double* u, void* stream);
+int qg_apply_cx(void* state, int32_t n_local, int32_t dtype, int32_t control, int32_t target, void* stream);
+int qg_apply_cr1(void* state, int32_t n_local, int32_t dtype, int32_t control, int32_t target, double lam,
+                 void* stream);
+
+/* ---- reductions and sampling (statevec.py:47-50, 215-234) ----------------- */
+/* sum |a|^2 in float64; result written to *out_host (synchronises `stream`) */
+int qg_norm_sq(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
+               double* out_host, void* stream);
+/* probs_dev[i] = |a_i|^2 in float64 */
+int qg_probabilities(const void* state, int64_t n_amps, int32_t dtype, double* probs_dev, void* stream);
+
+/* Multinomial sampler.  `uniforms_dev` = NULL: counter-based Philox4x32-10
+ * uniforms from `seed`; otherwise `shots` caller-supplied uniforms in [0,1)
+ * (e.g. numpy default_rng(seed).random(shots), which reproduces the
+ * reference's Generator.choice draws).  The norm is checked against
+ * `norm_tol` first (QG_E_UNNORMALIZED).  Output: unique outcome indices in
+ * increasing order and their counts, n_unique written to *n_unique_host. */
+int64_t qg_sample_workspace_bytes(int64_t n_amps, int64_t shots);
+int qg_sample(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, uint64_t seed,
+              const double* uniforms_dev, double norm_tol, void* workspace, int64_t workspace_bytes,
+              int64_t* out_index_dev, int64_t* out_count_dev, int64_t* n_unique_host,
+              double* norm_sq_host, void* stream);
+
+const char* qg_last_error(void);
+int qg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QGEAR_B200_H */

@@ -1,0 +1,312 @@
+// capi.cu — the extern "C" boundary of libqgear_b200.so (include/qgear_b200.h).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/qgear_b200.h"
+#include "kernels.h"
+#include "plan.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(QG_E_CUDA, std::string(where) + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e));
+}
+
+#define QG_CUDA(call, where)                         \
+    do {                                             \
+        cudaError_t e_ = (call);                     \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+int check_dtype(int32_t dtype) {
+    return (dtype == QG_DTYPE_C64 || dtype == QG_DTYPE_C128) ? QG_OK : fail(QG_E_INVALID_ARG, "dtype must be 0 (c64) or 1 (c128)");
+}
+
+int run_segment(const qg_plan* plan, int64_t seg, void* state, int32_t rank, cudaStream_t st, qg_exec_stats* stats) {
+    const uint64_t rank_bits = (uint64_t)rank << plan->n_local;
+    const auto& passes = plan->segs[seg];
+    const auto& idx = plan->desc_index[seg];
+    const int64_t shard_bytes = ((int64_t)1 << plan->n_local) * (plan->dtype == QG_DTYPE_C64 ? 8 : 16);
+    for (size_t p = 0; p < passes.size(); ++p) {
+        cudaError_t e;
+        if (idx[p] >= 0) {
+            const void* d = plan->dtype == QG_DTYPE_C64 ? (const void*)&plan->d32[idx[p]] : (const void*)&plan->d64[idx[p]];
+            e = qg::launch_fused(plan->dtype, plan->cfg.id, d, state, rank_bits, st);
+        } else {
+            e = qg::launch_gate(plan->dtype, passes[p].gop, state, plan->n_local, rank_bits, st);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "pass launch");
+        if (stats) {
+            stats->pass_launches += 1;
+            stats->bytes_moved += 2 * shard_bytes;
+        }
+    }
+    return QG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qg_last_error(void) { return g_err.c_str(); }
+int qg_abi_version(void) { return QG_ABI_VERSION; }
+
+int qg_plan_create(const int32_t* gate_type, const double* gate_param, int64_t n_gates, int32_t n_qubits,
+                   const qg_plan_opts* opts, qg_plan** out) {
+    if (!out) return fail(QG_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    qg_plan_opts o{};
+    o.fuse = 1;
+    if (opts) o = *opts;
+    qg_plan* p = new (std::nothrow) qg_plan();
+    if (!p) return fail(QG_E_OUT_OF_MEMORY, "plan allocation failed");
+    std::string err;
+    int rc;
+    try {
+        rc = qg::build_plan(gate_type, gate_param, n_gates, n_qubits, o, *p, err);
+    } catch (const std::bad_alloc&) {
+        rc = QG_E_OUT_OF_MEMORY;
+        err = "out of host memory while planning";
+    }
+    if (rc != QG_OK) {
+        delete p;
+        return fail(rc, err);
+    }
+    *out = p;
+    return QG_OK;
+}
+
+int qg_plan_destroy(qg_plan* plan) {
+    delete plan;
+    return QG_OK;
+}
+
+int qg_plan_get_info(const qg_plan* plan, qg_plan_info* out) {
+    if (!plan || !out) return fail(QG_E_INVALID_ARG, "NULL argument");
+    std::memset(out, 0, sizeof(*out));
+    out->n_body_gates = plan->n_body;
+    for (const auto& s : plan->segs) out->n_passes += (int64_t)s.size();
+    out->n_segments = (int64_t)plan->segs.size();
+    out->n_remaps = (int64_t)plan->remaps.size();
+    out->n_ops = plan->stats.n_ops;
+    out->n_stages = plan->stats.n_stages;
+    out->tile_qubits = plan->cfg.k();
+    out->n_local = plan->n_local;
+    out->n_qubits = plan->n;
+    out->dtype = plan->dtype;
+    return QG_OK;
+}
+
+int qg_plan_get_remap(const qg_plan* plan, int64_t i, qg_remap* out) {
+    if (!plan || !out) return fail(QG_E_INVALID_ARG, "NULL argument");
+    if (i < 0 || i >= (int64_t)plan->remaps.size()) return fail(QG_E_INVALID_ARG, "remap index out of range");
+    *out = plan->remaps[i];
+    return QG_OK;
+}
+
+int qg_plan_get_final_map(const qg_plan* plan, int32_t* phys_of_logical) {
+    if (!plan || !phys_of_logical) return fail(QG_E_INVALID_ARG, "NULL argument");
+    for (int q = 0; q < plan->n; ++q) phys_of_logical[q] = plan->final_phys[q];
+    return QG_OK;
+}
+
+int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* mats, int64_t* n_mats) {
+    if (!plan || !n_rec || !n_mats) return fail(QG_E_INVALID_ARG, "NULL argument");
+    int64_t nr = 0, nm = 0, pass_id = 0;
+    for (const auto& seg : plan->segs) {
+        for (const auto& hp : seg) {
+            if (hp.fused) {
+                for (size_t s = 0; s < hp.stages.size(); ++s) {
+                    for (const auto& o : hp.stages[s].ops) {
+                        if (rec) {
+                            int64_t* r = rec + 8 * nr;
+                            r[0] = pass_id; r[1] = (int64_t)s; r[2] = o.kind; r[3] = o.tq; r[4] = o.cq;
+                            r[5] = (int64_t)o.cmask; r[6] = (int64_t)o.qmask; r[7] = nm;
+                        }
+                        if (mats) std::memcpy(mats + 8 * nm, o.m, 8 * sizeof(double));
+                        ++nr; ++nm;
+                    }
+                }
+            } else {
+                if (rec) {
+                    int64_t* r = rec + 8 * nr;
+                    r[0] = pass_id; r[1] = -1; r[2] = 100 + hp.gop.kind; r[3] = hp.gop.t; r[4] = -1;
+                    r[5] = (int64_t)hp.gop.cmask; r[6] = (int64_t)hp.gop.qmask; r[7] = nm;
+                }
+                if (mats) std::memcpy(mats + 8 * nm, hp.gop.m, 8 * sizeof(double));
+                ++nr; ++nm;
+            }
+            ++pass_id;
+        }
+        ++pass_id;  // a segment boundary (remap) consumes one id
+    }
+    *n_rec = nr;
+    *n_mats = nm;
+    return QG_OK;
+}
+
+int qg_state_init_zero(void* state, int32_t n_local, int32_t dtype, int32_t rank, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (!state || n_local < 0 || n_local > 40) return fail(QG_E_INVALID_ARG, "bad state / n_local");
+    QG_CUDA(qg::launch_init_zero(state, n_local, dtype, rank, (cudaStream_t)stream), "init_zero");
+    return QG_OK;
+}
+
+int qg_plan_execute_segment(const qg_plan* plan, int64_t segment, void* state, int32_t rank, void* stream,
+                            int32_t timed, qg_exec_stats* stats) {
+    if (!plan || !state) return fail(QG_E_INVALID_ARG, "NULL argument");
+    if (segment < 0 || segment >= (int64_t)plan->segs.size()) return fail(QG_E_INVALID_ARG, "segment out of range");
+    if (rank < 0 || rank >= (1 << plan->g)) return fail(QG_E_BAD_WORKER_COUNT, "rank out of range");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (timed) {
+        QG_CUDA(cudaEventCreate(&e0), "event");
+        QG_CUDA(cudaEventCreate(&e1), "event");
+        QG_CUDA(cudaEventRecord(e0, st), "event record");
+    }
+    int rc = run_segment(plan, segment, state, rank, st, stats);
+    if (timed) {
+        if (rc == QG_OK) {
+            cudaEventRecord(e1, st);
+            cudaError_t e = cudaEventSynchronize(e1);
+            float ms = 0;
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+            if (e != cudaSuccess) rc = cuda_fail(e, "timed execute");
+            else if (stats) stats->pass_ms = ms;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    return rc;
+}
+
+int qg_plan_execute(const qg_plan* plan, void* state, void* stream, int32_t timed, qg_exec_stats* stats) {
+    if (!plan || !state) return fail(QG_E_INVALID_ARG, "NULL argument");
+    if (plan->g != 0) return fail(QG_E_BAD_WORKER_COUNT, "multi-rank plan: use qg_plan_execute_segment + remaps");
+    return qg_plan_execute_segment(plan, 0, state, 0, stream, timed, stats);
+}
+
+static int single_gate(void* state, int32_t n_local, int32_t dtype, const qg::GateOp& op, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (!state || n_local < 1 || n_local > 40) return fail(QG_E_INVALID_ARG, "bad state / n_local");
+    QG_CUDA(qg::launch_gate(dtype, op, state, n_local, 0, (cudaStream_t)stream), "gate launch");
+    return QG_OK;
+}
+
+int qg_apply_matrix(void* state, int32_t n_local, int32_t dtype, int32_t target, const double* u, void* stream) {
+    if (target < 0 || target >= n_local)
+        return fail(QG_E_INDEX_OUT_OF_RANGE, "target " + std::to_string(target) + " out of range for " +
+                                                 std::to_string(n_local) + " qubits");
+    if (!u) return fail(QG_E_INVALID_ARG, "u is NULL");
+    qg::GateOp op{};
+    op.kind = 0;
+    op.t = target;
+    std::memcpy(op.m, u, sizeof(op.m));
+    return single_gate(state, n_local, dtype, op, stream);
+}
+
+static int check_pair(int32_t n, int32_t c, int32_t t) {
+    for (int q : {c, t})
+        if (q < 0 || q >= n)
+            return fail(QG_E_INDEX_OUT_OF_RANGE, "qubit " + std::to_string(q) + " out of range for " +
+                                                     std::to_string(n) + " qubits");
+    if (c == t) return fail(QG_E_SELF_PAIR, "control == target == " + std::to_string(c));
+    return QG_OK;
+}
+
+int qg_apply_cx(void* state, int32_t n_local, int32_t dtype, int32_t control, int32_t target, void* stream) {
+    if (int rc = check_pair(n_local, control, target)) return rc;
+    qg::GateOp op{};
+    op.kind = 0;
+    op.t = target;
+    op.cmask = 1ull << control;
+    op.m[2] = 1.0;  // [[0,1],[1,0]]
+    op.m[4] = 1.0;
+    return single_gate(state, n_local, dtype, op, stream);
+}
+
+int qg_apply_cr1(void* state, int32_t n_local, int32_t dtype, int32_t control, int32_t target, double lam,
+                 void* stream) {
+    if (int rc = check_pair(n_local, control, target)) return rc;
+    qg::GateOp op{};
+    op.kind = 0;
+    op.t = target;
+    op.cmask = 1ull << control;
+    op.m[0] = 1.0;
+    op.m[6] = std::cos(lam);
+    op.m[7] = std::sin(lam);
+    return single_gate(state, n_local, dtype, op, stream);
+}
+
+int qg_norm_sq(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
+               double* out_host, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    const int parts = qg::norm_parts();
+    if (!state || !workspace || !out_host || n_amps < 1) return fail(QG_E_INVALID_ARG, "NULL argument");
+    if (workspace_bytes < (int64_t)(parts + 1) * 8) return fail(QG_E_INVALID_ARG, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    double* part = static_cast<double*>(workspace);
+    QG_CUDA(qg::launch_norm(state, n_amps, dtype, part, parts, st), "norm");
+    QG_CUDA(cudaMemcpyAsync(out_host, part + parts, sizeof(double), cudaMemcpyDeviceToHost, st), "norm copy");
+    QG_CUDA(cudaStreamSynchronize(st), "norm sync");
+    return QG_OK;
+}
+
+int qg_probabilities(const void* state, int64_t n_amps, int32_t dtype, double* probs_dev, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (!state || !probs_dev || n_amps < 1) return fail(QG_E_INVALID_ARG, "NULL argument");
+    QG_CUDA(qg::launch_probs(state, n_amps, dtype, probs_dev, (cudaStream_t)stream), "probabilities");
+    return QG_OK;
+}
+
+int64_t qg_sample_workspace_bytes(int64_t n_amps, int64_t shots) {
+    if (n_amps < 1 || shots < 0) return -1;
+    return qg::sample_workspace_bytes(n_amps, shots);
+}
+
+int qg_sample(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, uint64_t seed,
+              const double* uniforms_dev, double norm_tol, void* workspace, int64_t workspace_bytes,
+              int64_t* out_index_dev, int64_t* out_count_dev, int64_t* n_unique_host, double* norm_sq_host,
+              void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (shots < 1) return fail(QG_E_INVALID_ARG, "shots must be >= 1, got " + std::to_string(shots));
+    if (shots > (int64_t)INT32_MAX) return fail(QG_E_INVALID_ARG, "shots > 2^31-1 not supported by this sampler");
+    if (!state || !workspace || !out_index_dev || !out_count_dev || !n_unique_host || n_amps < 1 ||
+        (n_amps & (n_amps - 1)))
+        return fail(QG_E_INVALID_ARG, "bad sampler arguments");
+    if (workspace_bytes < qg::sample_workspace_bytes(n_amps, shots)) return fail(QG_E_INVALID_ARG, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    QG_CUDA(qg::sample_prefix(state, n_amps, dtype, workspace, st, nullptr), "sample prefix");
+    double total = 0;
+    QG_CUDA(cudaMemcpyAsync(&total, qg::sample_total_ptr(workspace, n_amps), sizeof(double), cudaMemcpyDeviceToHost, st),
+            "norm copy");
+    QG_CUDA(cudaStreamSynchronize(st), "sample sync");
+    if (norm_sq_host) *norm_sq_host = total;
+    if (!(std::fabs(total - 1.0) <= norm_tol)) {  // statevec.py:226-228 (NaN fails too)
+        char buf[96];
+        std::snprintf(buf, sizeof(buf), "norm^2 = %.17g outside tolerance", total);
+        return fail(QG_E_UNNORMALIZED, buf);
+    }
+    int64_t* nu = const_cast<int64_t*>(qg::sample_nunique_ptr(workspace, n_amps, shots));
+    QG_CUDA(qg::sample_draw(state, n_amps, dtype, shots, seed, uniforms_dev, workspace, out_index_dev, out_count_dev, st,
+                            nu),
+            "sample draw");
+    QG_CUDA(cudaMemcpyAsync(n_unique_host, nu, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "nunique copy");
+    QG_CUDA(cudaStreamSynchronize(st), "sample sync");
+    return QG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,391 @@
+// fused.cu — the fused multi-gate pass kernel (sm_100a) and the single-gate kernel.
+//
+// Replaces the reference's three array kernels (statevec.py:115-144), which
+// each stream the whole state through numpy once per gate, with ONE HBM pass
+// per group of gates:
+//
+//   tile   = 2^k amplitudes sharing all index bits outside the pass's tile
+//            qubits (desc.tile_q); the 5 lowest tile bits are the lane bits of
+//            the io mapping, so global loads/stores are >= 256 B contiguous.
+//   thread = 2^RB amplitudes in registers; a register stage applies every op
+//            whose target is a register bit with straight-line FMA code
+//            (switch over the runtime bit -> compile-time-unrolled body).
+//   stage switch = one SMEM round trip with a linear XOR swizzle
+//            (conflict-free lanes chosen by the planner).
+//   controls / diagonal phases on non-register qubits = per-thread predicates
+//            and a per-thread phase accumulator, no data movement.
+//
+// Memory traffic per pass = read + write of the state once (2 x S bytes),
+// the roofline quantity reported by bench.py.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "desc.h"
+#include "kernels.h"
+
+namespace qg {
+
+template <typename Real>
+struct V2;
+template <>
+struct V2<float> {
+    using T = float2;
+};
+template <>
+struct V2<double> {
+    using T = double2;
+};
+
+template <typename T2>
+__device__ __forceinline__ T2 cmul(T2 a, T2 b) {
+    T2 r;
+    r.x = a.x * b.x - a.y * b.y;
+    r.y = a.x * b.y + a.y * b.x;
+    return r;
+}
+
+__host__ __device__ constexpr int ctz_c(int x) { return (x & 1) ? 0 : 1 + ctz_c(x >> 1); }
+__host__ __device__ constexpr int gray_c(int x) { return x ^ (x >> 1); }
+
+// ----------------------------------------------------------------- register ops
+template <int RB, int TB, typename T2, typename Real>
+__device__ __forceinline__ void r_dense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
+    if constexpr (TB < RB) {
+        const Real m00r = m[0], m00i = m[1], m01r = m[2], m01i = m[3];
+        const Real m10r = m[4], m10i = m[5], m11r = m[6], m11i = m[7];
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            if (i & (1 << TB)) continue;
+            const int j = i | (1 << TB);
+            const T2 x = a[i], y = a[j];
+            a[i].x = m00r * x.x - m00i * x.y + m01r * y.x - m01i * y.y;
+            a[i].y = m00r * x.y + m00i * x.x + m01r * y.y + m01i * y.x;
+            a[j].x = m10r * x.x - m10i * x.y + m11r * y.x - m11i * y.y;
+            a[j].y = m10r * x.y + m10i * x.x + m11r * y.y + m11i * y.x;
+        }
+    }
+}
+
+// diag(d0, d1) on reg bit TB; lo_id = 1 -> d0 == 1 (only the |1> half changes)
+template <int RB, int TB, typename T2, typename Real>
+__device__ __forceinline__ void r_diag(T2 (&a)[1 << RB], int lo_id, const Real* __restrict__ m) {
+    if constexpr (TB < RB) {
+        T2 d0, d1;
+        d0.x = m[0]; d0.y = m[1];
+        d1.x = m[2]; d1.y = m[3];
+        if (lo_id) {
+#pragma unroll
+            for (int i = 0; i < (1 << RB); ++i)
+                if (i & (1 << TB)) a[i] = cmul(a[i], d1);
+        } else {
+#pragma unroll
+            for (int i = 0; i < (1 << RB); ++i) a[i] = cmul(a[i], (i & (1 << TB)) ? d1 : d0);
+        }
+    }
+}
+
+template <int RB, int TB, typename T2>
+__device__ __forceinline__ void r_x(T2 (&a)[1 << RB]) {
+    if constexpr (TB < RB) {
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            if (i & (1 << TB)) continue;
+            const T2 x = a[i];
+            a[i] = a[i | (1 << TB)];
+            a[i | (1 << TB)] = x;
+        }
+    }
+}
+
+template <int RB, int TB, int CB, typename T2>
+__device__ __forceinline__ void r_cx(T2 (&a)[1 << RB]) {
+    if constexpr (TB < RB && CB < RB && TB != CB) {
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            if ((i & (1 << TB)) || !(i & (1 << CB))) continue;
+            const T2 x = a[i];
+            a[i] = a[i | (1 << TB)];
+            a[i | (1 << TB)] = x;
+        }
+    }
+}
+
+template <int RB, int TB, int CB, typename T2, typename Real>
+__device__ __forceinline__ void r_cphase(T2 (&a)[1 << RB], const Real* __restrict__ m) {
+    if constexpr (TB < RB && CB < RB && TB != CB) {
+        T2 e;
+        e.x = m[0]; e.y = m[1];
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i)
+            if ((i & (1 << TB)) && (i & (1 << CB))) a[i] = cmul(a[i], e);
+    }
+}
+
+// runtime bit -> compile-time body
+#define QG_CASES5(BODY) \
+    case 0: BODY(0); break; case 1: BODY(1); break; case 2: BODY(2); break; case 3: BODY(3); break; \
+    case 4: BODY(4); break;
+
+template <int RB, int TB, typename T2>
+__device__ __forceinline__ void cx_on_c(T2 (&a)[1 << RB], int c) {
+#define B_(C) r_cx<RB, TB, C>(a)
+    switch (c) { QG_CASES5(B_) }
+#undef B_
+}
+
+template <int RB, int TB, typename T2, typename Real>
+__device__ __forceinline__ void cphase_on_c(T2 (&a)[1 << RB], int c, const Real* __restrict__ m) {
+#define B_(C) r_cphase<RB, TB, C>(a, m)
+    switch (c) { QG_CASES5(B_) }
+#undef B_
+}
+
+template <int RB, typename T2, typename Real>
+__device__ __forceinline__ void apply_op(T2 (&a)[1 << RB], const OpDesc& op, const Real* __restrict__ m) {
+    const int t = op.t, c = op.c;
+    switch (op.kind) {
+        case OP_DENSE:
+#define B_(T) r_dense<RB, T>(a, m)
+            switch (t) { QG_CASES5(B_) }
+#undef B_
+            break;
+        case OP_DIAG:
+#define B_(T) r_diag<RB, T>(a, c, m)
+            switch (t) { QG_CASES5(B_) }
+#undef B_
+            break;
+        case OP_X:
+#define B_(T) r_x<RB, T>(a)
+            switch (t) { QG_CASES5(B_) }
+#undef B_
+            break;
+        case OP_CX:
+#define B_(T) cx_on_c<RB, T>(a, c)
+            switch (t) { QG_CASES5(B_) }
+#undef B_
+            break;
+        case OP_CPHASE:
+#define B_(T) cphase_on_c<RB, T>(a, c, m)
+            switch (t) { QG_CASES5(B_) }
+#undef B_
+            break;
+        default:
+            break;
+    }
+}
+
+// ----------------------------------------------------------------- mappings
+template <int WB>
+__device__ __forceinline__ uint64_t thread_gbits(const StageDesc& S, int lane, int warp) {
+    uint64_t g = 0;
+#pragma unroll
+    for (int l = 0; l < kLaneBits; ++l) g |= (uint64_t)((lane >> l) & 1) << S.lane_q[l];
+#pragma unroll
+    for (int w = 0; w < WB; ++w) g |= (uint64_t)((warp >> w) & 1) << S.warp_q[w];
+    return g;
+}
+
+template <int WB>
+__device__ __forceinline__ uint32_t thread_soff(const StageDesc& S, int lane, int warp) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int l = 0; l < kLaneBits; ++l) s ^= ((lane >> l) & 1) ? (uint32_t)S.lane_s[l] : 0u;
+#pragma unroll
+    for (int w = 0; w < WB; ++w) s ^= ((warp >> w) & 1) ? (uint32_t)S.warp_s[w] : 0u;
+    return s;
+}
+
+template <int RB, int WB, typename T2>
+__device__ __forceinline__ void smem_put(T2* sm, const StageDesc& S, int lane, int warp, const T2 (&a)[1 << RB]) {
+    uint32_t so = thread_soff<WB>(S, lane, warp);
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if (j) so ^= S.reg_s[ctz_c(j)];
+        sm[so] = a[gray_c(j)];
+    }
+}
+
+template <int RB, int WB, typename T2>
+__device__ __forceinline__ void smem_get(const T2* sm, const StageDesc& S, int lane, int warp, T2 (&a)[1 << RB]) {
+    uint32_t so = thread_soff<WB>(S, lane, warp);
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if (j) so ^= S.reg_s[ctz_c(j)];
+        a[gray_c(j)] = sm[so];
+    }
+}
+
+// ----------------------------------------------------------------- the kernel
+template <typename Real, int RB, int WB>
+__global__ void __launch_bounds__(32 << WB)
+    fused_pass_kernel(const __grid_constant__ PassDesc<Real> P, typename V2<Real>::T* __restrict__ psi,
+                      uint64_t rank_bits) {
+    using T2 = typename V2<Real>::T;
+    constexpr int R = 1 << RB;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T2* sm = reinterpret_cast<T2*>(smem_raw);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int ns = P.n_stages;
+    const int li = P.load_direct ? 1 : 0;   // mapping used for the global load
+    const int si = P.store_direct ? ns : 0; // mapping used for the global store
+    T2 a[R];
+
+    for (uint64_t tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+        // tile id -> index bits outside the tile (insert a zero at every tile qubit)
+        uint64_t base = tile;
+        for (int j = 0; j < P.k; ++j) {
+            const int p = P.tile_q[j];
+            base = ((base >> p) << (p + 1)) | (base & ((1ull << p) - 1ull));
+        }
+        {  // global load, Gray-code order over the register index
+            const StageDesc& S = P.stg[li];
+            uint64_t g = base | thread_gbits<WB>(S, lane, warp);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                if (j) g ^= 1ull << S.reg_q[ctz_c(j)];
+                a[gray_c(j)] = __ldcs(psi + g);
+            }
+        }
+        int cur = li;
+        for (int s = 1; s <= ns; ++s) {
+            const StageDesc& S = P.stg[s];
+            if (cur != s) {  // SMEM transpose into this stage's mapping
+                __syncthreads();
+                smem_put<RB, WB>(sm, P.stg[cur], lane, warp, a);
+                __syncthreads();
+                smem_get<RB, WB>(sm, S, lane, warp, a);
+                cur = s;
+            }
+            const uint64_t tb = base | rank_bits | thread_gbits<WB>(S, lane, warp);
+            T2 ph;
+            ph.x = Real(1);
+            ph.y = Real(0);
+            for (int o = S.op_begin; o < S.op_end; ++o) {
+                const OpDesc& op = P.ops[o];
+                const uint64_t cm = op.cmask;
+                if ((tb & cm) != cm) continue;
+                const Real* m = P.mats[op.mat];
+                if (op.kind == OP_TPHASE) {
+                    T2 v;
+                    const bool hi = (tb & op.qmask) != 0;
+                    v.x = hi ? m[2] : m[0];
+                    v.y = hi ? m[3] : m[1];
+                    ph = cmul(ph, v);
+                } else {
+                    apply_op<RB>(a, op, m);
+                }
+            }
+            if (S.has_tphase) {
+#pragma unroll
+                for (int i = 0; i < R; ++i) a[i] = cmul(a[i], ph);
+            }
+        }
+        if (cur != si) {
+            __syncthreads();
+            smem_put<RB, WB>(sm, P.stg[cur], lane, warp, a);
+            __syncthreads();
+            smem_get<RB, WB>(sm, P.stg[si], lane, warp, a);
+        }
+        {
+            const StageDesc& S = P.stg[si];
+            uint64_t g = base | thread_gbits<WB>(S, lane, warp);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                if (j) g ^= 1ull << S.reg_q[ctz_c(j)];
+                __stcs(psi + g, a[gray_c(j)]);
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------- single-gate kernel
+template <typename Real>
+__global__ void gate_kernel(typename V2<Real>::T* __restrict__ psi, int n_local, GateOp op, uint64_t rank_bits) {
+    using T2 = typename V2<Real>::T;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (op.kind == 0) {
+        const int t = op.t;
+        const uint64_t npairs = 1ull << (n_local - 1);
+        const Real m00r = (Real)op.m[0], m00i = (Real)op.m[1], m01r = (Real)op.m[2], m01i = (Real)op.m[3];
+        const Real m10r = (Real)op.m[4], m10i = (Real)op.m[5], m11r = (Real)op.m[6], m11i = (Real)op.m[7];
+        for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += stride) {
+            const uint64_t i0 = ((p >> t) << (t + 1)) | (p & ((1ull << t) - 1ull));
+            const uint64_t i1 = i0 | (1ull << t);
+            if (((rank_bits | i0) & op.cmask) != op.cmask) continue;
+            const T2 x = psi[i0], y = psi[i1];
+            T2 u, v;
+            u.x = m00r * x.x - m00i * x.y + m01r * y.x - m01i * y.y;
+            u.y = m00r * x.y + m00i * x.x + m01r * y.y + m01i * y.x;
+            v.x = m10r * x.x - m10i * x.y + m11r * y.x - m11i * y.y;
+            v.y = m10r * x.y + m10i * x.x + m11r * y.y + m11i * y.x;
+            psi[i0] = u;
+            psi[i1] = v;
+        }
+    } else {
+        const uint64_t namps = 1ull << n_local;
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < namps; i += stride) {
+            const uint64_t g = rank_bits | i;
+            if ((g & op.cmask) != op.cmask) continue;
+            const bool hi = (g & op.qmask) != 0;
+            T2 v;
+            v.x = (Real)(hi ? op.m[2] : op.m[0]);
+            v.y = (Real)(hi ? op.m[3] : op.m[1]);
+            psi[i] = cmul(psi[i], v);
+        }
+    }
+}
+
+// ----------------------------------------------------------------- launchers
+template <typename Real, int RB, int WB>
+static cudaError_t launch_fused_t(const PassDesc<Real>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
+    constexpr int threads = 32 << WB;
+    const int k = RB + kLaneBits + WB;
+    const size_t smem = ((size_t)1 << k) * sizeof(typename V2<Real>::T);
+    auto kern = fused_pass_kernel<Real, RB, WB>;
+    static int max_blocks = -1;  // per instantiation: resident CTAs per SM x SMs
+    if (max_blocks < 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (e != cudaSuccess) return e;
+        max_blocks = sms * (occ > 0 ? occ : 1);
+    }
+    const uint64_t grid = P.n_tiles < (uint64_t)max_blocks ? P.n_tiles : (uint64_t)max_blocks;
+    kern<<<(unsigned)grid, threads, smem, st>>>(P, reinterpret_cast<typename V2<Real>::T*>(psi), rank_bits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uint64_t rank_bits, cudaStream_t st) {
+    if (dtype == 0) {
+        const auto& P = *static_cast<const PassDesc<float>*>(desc);
+        switch (cfg_id) {
+            case 0: return launch_fused_t<float, 5, 3>(P, psi, rank_bits, st);
+            case 1: return launch_fused_t<float, 4, 2>(P, psi, rank_bits, st);
+            default: return launch_fused_t<float, 3, 0>(P, psi, rank_bits, st);
+        }
+    }
+    const auto& P = *static_cast<const PassDesc<double>*>(desc);
+    switch (cfg_id) {
+        case 0: return launch_fused_t<double, 4, 3>(P, psi, rank_bits, st);
+        case 1: return launch_fused_t<double, 3, 2>(P, psi, rank_bits, st);
+        default: return launch_fused_t<double, 3, 0>(P, psi, rank_bits, st);
+    }
+}
+
+cudaError_t launch_gate(int dtype, const GateOp& op, void* psi, int n_local, uint64_t rank_bits, cudaStream_t st) {
+    const uint64_t work = op.kind == 0 ? (1ull << (n_local - 1)) : (1ull << n_local);
+    const int threads = 256;
+    uint64_t blocks = (work + threads - 1) / threads;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    if (dtype == 0)
+        gate_kernel<float><<<(unsigned)blocks, threads, 0, st>>>(static_cast<float2*>(psi), n_local, op, rank_bits);
+    else
+        gate_kernel<double><<<(unsigned)blocks, threads, 0, st>>>(static_cast<double2*>(psi), n_local, op, rank_bits);
+    return cudaGetLastError();
+}
+
+}  // namespace qg

@@ -1,0 +1,29 @@
+// kernels.h — launch entry points of the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "desc.h"
+
+namespace qg {
+
+cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uint64_t rank_bits, cudaStream_t st);
+cudaError_t launch_gate(int dtype, const GateOp& op, void* psi, int n_local, uint64_t rank_bits, cudaStream_t st);
+
+cudaError_t launch_init_zero(void* psi, int n_local, int dtype, int rank, cudaStream_t st);
+// partial fp64 sums of |a|^2: grid-stride, one double per CTA into `partial`, then
+// a single-CTA finish into partial[n_parts]
+cudaError_t launch_norm(const void* psi, int64_t n_amps, int dtype, double* partial, int n_parts, cudaStream_t st);
+int norm_parts();
+cudaError_t launch_probs(const void* psi, int64_t n_amps, int dtype, double* out, cudaStream_t st);
+
+// sampler (see reduce.cu for the layout of the workspace)
+int64_t sample_workspace_bytes(int64_t n_amps, int64_t shots);
+cudaError_t sample_prefix(const void* psi, int64_t n_amps, int dtype, void* ws, cudaStream_t st, double* total_dev);
+cudaError_t sample_draw(const void* psi, int64_t n_amps, int dtype, int64_t shots, uint64_t seed,
+                        const double* uniforms, void* ws, int64_t* out_idx, int64_t* out_cnt, cudaStream_t st,
+                        int64_t* n_unique_dev);
+const double* sample_total_ptr(const void* ws, int64_t n_amps);
+const int64_t* sample_nunique_ptr(const void* ws, int64_t n_amps, int64_t shots);
+
+}  // namespace qg

@@ -1,0 +1,337 @@
+// reduce.cu — state init, fp64 norm / probabilities, and the shot sampler.
+//
+// Reference: init_zero_state statevec.py:81-94; StateVector.norm_sq
+// statevec.py:47-50; exact_probabilities statevec.py:215-218; sample_counts
+// statevec.py:221-234 (fp64 |a|^2, norm check, cdf = cumsum / last,
+// searchsorted(side='right') of uniforms, unique counts).
+//
+// Sampler (two-level inverse-CDF, no full-length prefix array):
+//   1. chunk_sums:  one HBM read of the state; fp64 sums per 256-amp sub-block
+//                   and per 16384-amp chunk (sub-block sums kept in workspace).
+//   2. chunk_scan:  exclusive prefix of the chunk sums (single CTA) -> total.
+//   3. draw:        per shot, u*total -> binary search over chunk prefixes ->
+//                   linear walk over <= 64 sub-block sums -> <= 256 amplitudes.
+//   4. CUB radix sort of the outcome indices + run-length encode -> (index, count).
+// Uniforms come from a counter-based Philox4x32-10 stream (seed, shot) or from
+// the caller (numpy's default_rng(seed).random(shots) reproduces the reference's
+// Generator.choice draws exactly up to fp64 rounding of the cdf).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cub/cub.cuh>
+
+#include "kernels.h"
+
+namespace qg {
+
+template <typename Real>
+struct A2;
+template <>
+struct A2<float> {
+    using T = float2;
+};
+template <>
+struct A2<double> {
+    using T = double2;
+};
+
+template <typename T2>
+__device__ __forceinline__ double prob(T2 a) {
+    const double x = (double)a.x, y = (double)a.y;
+    return x * x + y * y;
+}
+
+// ----------------------------------------------------------------- init
+template <typename T2>
+__global__ void set_one(T2* psi) {
+    T2 v;
+    v.x = 1;
+    v.y = 0;
+    psi[0] = v;
+}
+
+cudaError_t launch_init_zero(void* psi, int n_local, int dtype, int rank, cudaStream_t st) {
+    const size_t bytes = ((size_t)1 << n_local) * (dtype == 0 ? 8 : 16);
+    cudaError_t e = cudaMemsetAsync(psi, 0, bytes, st);
+    if (e != cudaSuccess) return e;
+    if (rank == 0) {
+        if (dtype == 0) set_one<<<1, 1, 0, st>>>(static_cast<float2*>(psi));
+        else set_one<<<1, 1, 0, st>>>(static_cast<double2*>(psi));
+    }
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- norm / probs
+constexpr int kNormParts = 148 * 4;
+int norm_parts() { return kNormParts; }
+
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    if (w == 0) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;  // valid in thread 0
+}
+
+template <typename T2>
+__global__ void norm_partial(const T2* __restrict__ psi, int64_t n, double* __restrict__ part) {
+    double acc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += prob(psi[i]);
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void norm_finish(double* part, int n_parts) {
+    double acc = 0;
+    for (int i = threadIdx.x; i < n_parts; i += blockDim.x) acc += part[i];
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) part[n_parts] = acc;
+}
+
+cudaError_t launch_norm(const void* psi, int64_t n_amps, int dtype, double* partial, int n_parts, cudaStream_t st) {
+    if (dtype == 0) norm_partial<<<n_parts, 256, 0, st>>>(static_cast<const float2*>(psi), n_amps, partial);
+    else norm_partial<<<n_parts, 256, 0, st>>>(static_cast<const double2*>(psi), n_amps, partial);
+    norm_finish<<<1, 1024, 0, st>>>(partial, n_parts);
+    return cudaGetLastError();
+}
+
+template <typename T2>
+__global__ void probs_kernel(const T2* __restrict__ psi, int64_t n, double* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = prob(psi[i]);
+}
+
+cudaError_t launch_probs(const void* psi, int64_t n_amps, int dtype, double* out, cudaStream_t st) {
+    int64_t blocks = (n_amps + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (dtype == 0) probs_kernel<<<(int)blocks, 256, 0, st>>>(static_cast<const float2*>(psi), n_amps, out);
+    else probs_kernel<<<(int)blocks, 256, 0, st>>>(static_cast<const double2*>(psi), n_amps, out);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- sampler layout
+constexpr int64_t kSub = 256;      // amplitudes per sub-block
+constexpr int64_t kChunk = 16384;  // amplitudes per chunk (64 sub-blocks)
+
+struct SLayout {
+    int64_t sb, ch, n_sub, n_ch;
+    size_t off_sub, off_bsum, off_bpre, off_draw, off_sorted, off_runs, off_cub, total;
+    size_t cub_bytes;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int bits_for(int64_t n) {
+    int b = 0;
+    while ((1ll << b) < n) ++b;
+    return b < 1 ? 1 : b;
+}
+
+static SLayout layout(int64_t n_amps, int64_t shots) {
+    SLayout L{};
+    L.sb = n_amps < kSub ? n_amps : kSub;
+    L.ch = n_amps < kChunk ? n_amps : kChunk;
+    L.n_sub = n_amps / L.sb;
+    L.n_ch = n_amps / L.ch;
+    size_t sort_b = 0, rle_b = 0;
+    const int64_t ns = shots > 0 ? shots : 1;
+    cub::DeviceRadixSort::SortKeys(nullptr, sort_b, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                   (int)ns, 0, bits_for(n_amps));
+    cub::DeviceRunLengthEncode::Encode(nullptr, rle_b, (const int64_t*)nullptr, (int64_t*)nullptr, (int64_t*)nullptr,
+                                       (int64_t*)nullptr, (int)ns);
+    L.cub_bytes = sort_b > rle_b ? sort_b : rle_b;
+    size_t o = 0;
+    L.off_sub = o; o += align256(L.n_sub * 8);
+    L.off_bsum = o; o += align256(L.n_ch * 8);
+    L.off_bpre = o; o += align256((L.n_ch + 1) * 8);
+    L.off_draw = o; o += align256(ns * 8);
+    L.off_sorted = o; o += align256(ns * 8);
+    L.off_runs = o; o += align256(8);
+    L.off_cub = o; o += align256(L.cub_bytes);
+    L.total = o;
+    return L;
+}
+
+int64_t sample_workspace_bytes(int64_t n_amps, int64_t shots) { return (int64_t)layout(n_amps, shots).total; }
+
+const double* sample_total_ptr(const void* ws, int64_t n_amps) {
+    const SLayout L = layout(n_amps, 1);
+    return reinterpret_cast<const double*>(static_cast<const char*>(ws) + L.off_bpre) + L.n_ch;
+}
+
+const int64_t* sample_nunique_ptr(const void* ws, int64_t n_amps, int64_t shots) {
+    const SLayout L = layout(n_amps, shots);
+    return reinterpret_cast<const int64_t*>(static_cast<const char*>(ws) + L.off_runs);
+}
+
+// ----------------------------------------------------------------- sampler kernels
+// one CTA (256 threads = 8 warps) per chunk; warp w sums sub-blocks w, w+8, ...
+template <typename T2>
+__global__ void chunk_sums(const T2* __restrict__ psi, int64_t sb, int64_t ch, double* __restrict__ sub,
+                           double* __restrict__ bsum) {
+    const int64_t c = blockIdx.x;
+    const int64_t nsb = ch / sb;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    double wacc = 0;
+    for (int64_t j = w; j < nsb; j += 8) {
+        const T2* p = psi + c * ch + j * sb;
+        double acc = 0;
+        for (int64_t i = l; i < sb; i += 32) acc += prob(p[i]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (l == 0) sub[c * nsb + j] = acc;
+        wacc += acc;
+    }
+    __shared__ double ws[8];
+    if (l == 0) ws[w] = wacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int i = 0; i < 8; ++i) t += ws[i];
+        bsum[c] = t;
+    }
+}
+
+// exclusive prefix of n doubles with one CTA of 1024 threads; out[n] = total
+__global__ void chunk_scan(const double* __restrict__ in, int64_t n, double* __restrict__ out) {
+    __shared__ double part[1024];
+    const int t = threadIdx.x;
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t b = t * per, e = (b + per < n) ? b + per : n;
+    double s = 0;
+    for (int64_t i = b; i < e; ++i) s += in[i];
+    part[t] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan
+        const double v = t >= off ? part[t - off] : 0.0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    double run = t ? part[t - 1] : 0.0;
+    for (int64_t i = b; i < e; ++i) {
+        out[i] = run;
+        run += in[i];
+    }
+    if (t == 1023) out[n] = part[1023];
+}
+
+__device__ __forceinline__ uint32_t mulhilo(uint32_t a, uint32_t b, uint32_t& hi) {
+    const uint64_t p = (uint64_t)a * b;
+    hi = (uint32_t)(p >> 32);
+    return (uint32_t)p;
+}
+
+// Philox4x32-10 (Salmon et al., SC'11) -> one double in [0, 1) with 53 random bits
+__device__ __forceinline__ double philox_uniform(uint64_t seed, uint64_t ctr) {
+    uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32), c2 = 0x51ea1e5u, c3 = 0u;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0, hi1;
+        const uint32_t lo0 = mulhilo(0xD2511F53u, c0, hi0);
+        const uint32_t lo1 = mulhilo(0xCD9E8D57u, c2, hi1);
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    const uint64_t x = ((uint64_t)c0 << 32) | c1;
+    return (double)(x >> 11) * (1.0 / 9007199254740992.0);
+}
+
+template <typename T2>
+__global__ void draw_kernel(const T2* __restrict__ psi, int64_t shots, uint64_t seed, const double* __restrict__ uni,
+                            const double* __restrict__ sub, const double* __restrict__ bpre, int64_t n_ch, int64_t sb,
+                            int64_t ch, unsigned long long* __restrict__ out) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= shots) return;
+    const double u = uni ? uni[s] : philox_uniform(seed, (uint64_t)s);
+    const double tot = bpre[n_ch];
+    const double target = u * tot;
+    // first chunk c with bpre[c+1] > target  (searchsorted side='right')
+    int64_t lo = 0, hi = n_ch - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (bpre[mid + 1] > target) hi = mid;
+        else lo = mid + 1;
+    }
+    int64_t c = lo;
+    while (c > 0 && bpre[c + 1] - bpre[c] <= 0.0) --c;  // rounding clamp onto a chunk with mass
+    double r = target - bpre[c];
+    const int64_t nsb = ch / sb;
+    int64_t j = 0, last = -1;
+    double acc = 0;
+    for (; j < nsb; ++j) {
+        const double v = sub[c * nsb + j];
+        if (v > 0) last = j;
+        if (acc + v > r) break;
+        acc += v;
+    }
+    if (j == nsb) { j = last < 0 ? nsb - 1 : last; acc -= sub[c * nsb + j]; }
+    r -= acc;
+    const T2* p = psi + c * ch + j * sb;
+    int64_t i = 0, lasti = -1;
+    double acc2 = 0;
+    for (; i < sb; ++i) {
+        const double v = prob(p[i]);
+        if (v > 0) lasti = i;
+        if (acc2 + v > r) break;
+        acc2 += v;
+    }
+    if (i == sb) i = lasti < 0 ? sb - 1 : lasti;
+    out[s] = (unsigned long long)(c * ch + j * sb + i);
+}
+
+cudaError_t sample_prefix(const void* psi, int64_t n_amps, int dtype, void* ws, cudaStream_t st, double* total_dev) {
+    const SLayout L = layout(n_amps, 1);
+    char* w = static_cast<char*>(ws);
+    double* sub = reinterpret_cast<double*>(w + L.off_sub);
+    double* bsum = reinterpret_cast<double*>(w + L.off_bsum);
+    double* bpre = reinterpret_cast<double*>(w + L.off_bpre);
+    if (dtype == 0) chunk_sums<<<(unsigned)L.n_ch, 256, 0, st>>>(static_cast<const float2*>(psi), L.sb, L.ch, sub, bsum);
+    else chunk_sums<<<(unsigned)L.n_ch, 256, 0, st>>>(static_cast<const double2*>(psi), L.sb, L.ch, sub, bsum);
+    chunk_scan<<<1, 1024, 0, st>>>(bsum, L.n_ch, bpre);
+    (void)total_dev;
+    return cudaGetLastError();
+}
+
+cudaError_t sample_draw(const void* psi, int64_t n_amps, int dtype, int64_t shots, uint64_t seed,
+                        const double* uniforms, void* ws, int64_t* out_idx, int64_t* out_cnt, cudaStream_t st,
+                        int64_t* n_unique_dev) {
+    const SLayout L = layout(n_amps, shots);
+    char* w = static_cast<char*>(ws);
+    const double* sub = reinterpret_cast<const double*>(w + L.off_sub);
+    const double* bpre = reinterpret_cast<const double*>(w + L.off_bpre);
+    auto* draws = reinterpret_cast<unsigned long long*>(w + L.off_draw);
+    auto* sorted = reinterpret_cast<unsigned long long*>(w + L.off_sorted);
+    const unsigned blocks = (unsigned)((shots + 255) / 256);
+    if (dtype == 0)
+        draw_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(psi), shots, seed, uniforms, sub, bpre, L.n_ch,
+                                            L.sb, L.ch, draws);
+    else
+        draw_kernel<<<blocks, 256, 0, st>>>(static_cast<const double2*>(psi), shots, seed, uniforms, sub, bpre,
+                                            L.n_ch, L.sb, L.ch, draws);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    size_t tb = L.cub_bytes;
+    e = cub::DeviceRadixSort::SortKeys(w + L.off_cub, tb, draws, sorted, (int)shots, 0, bits_for(n_amps), st);
+    if (e != cudaSuccess) return e;
+    tb = L.cub_bytes;
+    e = cub::DeviceRunLengthEncode::Encode(w + L.off_cub, tb, reinterpret_cast<const int64_t*>(sorted), out_idx,
+                                           out_cnt, n_unique_dev, (int)shots, st);
+    return e;
+}
+
+}  // namespace qg
