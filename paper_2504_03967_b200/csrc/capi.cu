@@ -128,16 +128,30 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
     for (const auto& seg : plan->segs) {
         for (const auto& hp : seg) {
             if (hp.fused) {
+                // kernel execution order: per stage the thread phases, then rounds slot by slot
+                static const int kExport[] = {0, 0, 1, 2, 3, 4, 5};  // AbsKind -> interpreter op kind
                 for (size_t s = 0; s < hp.stages.size(); ++s) {
-                    for (const auto& o : hp.stages[s].ops) {
+                    const auto& st = hp.stages[s];
+                    auto emit = [&](const qg::HostOp& o) {
                         if (rec) {
                             int64_t* r = rec + 8 * nr;
-                            r[0] = pass_id; r[1] = (int64_t)s; r[2] = o.kind; r[3] = o.tq; r[4] = o.cq;
+                            r[0] = pass_id; r[1] = (int64_t)s; r[2] = kExport[o.kind]; r[3] = o.tq; r[4] = o.cq;
                             r[5] = (int64_t)o.cmask; r[6] = (int64_t)o.qmask; r[7] = nm;
                         }
-                        if (mats) std::memcpy(mats + 8 * nm, o.m, 8 * sizeof(double));
+                        if (mats) {
+                            double* m = mats + 8 * nm;
+                            if (o.kind == qg::A_RDENSE) {  // expand the real 2x2 to complex layout
+                                const double v[8] = {o.m[0], 0, o.m[1], 0, o.m[2], 0, o.m[3], 0};
+                                std::memcpy(m, v, sizeof(v));
+                            } else {
+                                std::memcpy(m, o.m, 8 * sizeof(double));
+                            }
+                        }
                         ++nr; ++nm;
-                    }
+                    };
+                    for (const auto& o : st.tph) emit(o);
+                    for (const auto& r : st.rounds)
+                        for (const auto& o : r.ops) emit(o);
                 }
             } else {
                 if (rec) {

@@ -44,10 +44,16 @@ __device__ __forceinline__ T2 cmul(T2 a, T2 b) {
     return r;
 }
 
-__host__ __device__ constexpr int ctz_c(int x) { return (x & 1) ? 0 : 1 + ctz_c(x >> 1); }
+__host__ __device__ constexpr int ctz_c(int x) {  // x in 1..31 (unrolled loop constant)
+    return (x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : (x & 8) ? 3 : 4;
+}
 __host__ __device__ constexpr int gray_c(int x) { return x ^ (x >> 1); }
 
 // ----------------------------------------------------------------- register ops
+// Every body below is bound to compile-time register bits (TB, CB), so the
+// amplitude array never needs runtime indexing; the round loop enables them
+// with warp-uniform mask tests (if-then diamonds the register allocator keeps
+// in place).
 template <int RB, int TB, typename T2, typename Real>
 __device__ __forceinline__ void r_dense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
     if constexpr (TB < RB) {
@@ -66,13 +72,27 @@ __device__ __forceinline__ void r_dense(T2 (&a)[1 << RB], const Real* __restrict
     }
 }
 
-// diag(d0, d1) on reg bit TB; lo_id = 1 -> d0 == 1 (only the |1> half changes)
+// real 2x2 (H, RY and their products): half the FMAs of the complex case
 template <int RB, int TB, typename T2, typename Real>
-__device__ __forceinline__ void r_diag(T2 (&a)[1 << RB], int lo_id, const Real* __restrict__ m) {
+__device__ __forceinline__ void r_rdense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
     if constexpr (TB < RB) {
-        T2 d0, d1;
-        d0.x = m[0]; d0.y = m[1];
-        d1.x = m[2]; d1.y = m[3];
+        const Real m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            if (i & (1 << TB)) continue;
+            const int j = i | (1 << TB);
+            const T2 x = a[i], y = a[j];
+            a[i].x = m00 * x.x + m01 * y.x;
+            a[i].y = m00 * x.y + m01 * y.y;
+            a[j].x = m10 * x.x + m11 * y.x;
+            a[j].y = m10 * x.y + m11 * y.y;
+        }
+    }
+}
+
+template <int RB, int TB, typename T2>
+__device__ __forceinline__ void r_diag(T2 (&a)[1 << RB], T2 d0, T2 d1, bool lo_id) {
+    if constexpr (TB < RB) {
         if (lo_id) {
 #pragma unroll
             for (int i = 0; i < (1 << RB); ++i)
@@ -110,67 +130,87 @@ __device__ __forceinline__ void r_cx(T2 (&a)[1 << RB]) {
     }
 }
 
-template <int RB, int TB, int CB, typename T2, typename Real>
-__device__ __forceinline__ void r_cphase(T2 (&a)[1 << RB], const Real* __restrict__ m) {
+template <int RB, int TB, int CB, typename T2>
+__device__ __forceinline__ void r_cphase(T2 (&a)[1 << RB], T2 e) {
     if constexpr (TB < RB && CB < RB && TB != CB) {
-        T2 e;
-        e.x = m[0]; e.y = m[1];
 #pragma unroll
         for (int i = 0; i < (1 << RB); ++i)
             if ((i & (1 << TB)) && (i & (1 << CB))) a[i] = cmul(a[i], e);
     }
 }
 
-// runtime bit -> compile-time body
-#define QG_CASES5(BODY) \
-    case 0: BODY(0); break; case 1: BODY(1); break; case 2: BODY(2); break; case 3: BODY(3); break; \
-    case 4: BODY(4); break;
-
-template <int RB, int TB, typename T2>
-__device__ __forceinline__ void cx_on_c(T2 (&a)[1 << RB], int c) {
-#define B_(C) r_cx<RB, TB, C>(a)
-    switch (c) { QG_CASES5(B_) }
-#undef B_
-}
-
-template <int RB, int TB, typename T2, typename Real>
-__device__ __forceinline__ void cphase_on_c(T2 (&a)[1 << RB], int c, const Real* __restrict__ m) {
-#define B_(C) r_cphase<RB, TB, C>(a, m)
-    switch (c) { QG_CASES5(B_) }
-#undef B_
-}
-
+// one round: slots in the fixed order dense < diag < X < CX < CPHASE (desc.h)
 template <int RB, typename T2, typename Real>
-__device__ __forceinline__ void apply_op(T2 (&a)[1 << RB], const OpDesc& op, const Real* __restrict__ m) {
-    const int t = op.t, c = op.c;
-    switch (op.kind) {
-        case OP_DENSE:
-#define B_(T) r_dense<RB, T>(a, m)
-            switch (t) { QG_CASES5(B_) }
-#undef B_
-            break;
-        case OP_DIAG:
-#define B_(T) r_diag<RB, T>(a, c, m)
-            switch (t) { QG_CASES5(B_) }
-#undef B_
-            break;
-        case OP_X:
-#define B_(T) r_x<RB, T>(a)
-            switch (t) { QG_CASES5(B_) }
-#undef B_
-            break;
-        case OP_CX:
-#define B_(T) cx_on_c<RB, T>(a, c)
-            switch (t) { QG_CASES5(B_) }
-#undef B_
-            break;
-        case OP_CPHASE:
-#define B_(T) cphase_on_c<RB, T>(a, c, m)
-            switch (t) { QG_CASES5(B_) }
-#undef B_
-            break;
-        default:
-            break;
+__device__ __forceinline__ void run_round(T2 (&a)[1 << RB], const PassDesc<Real>& P, const RoundDesc& R, uint64_t tb) {
+    int ci = R.coef;
+    int ei = R.ent;
+    const uint32_t md = R.dense, mr = R.rdense;
+    if (md | mr) {
+#define QG_DENSE(B)                                                        \
+    if (B < RB) {                                                          \
+        if (md & (1u << B)) { r_dense<RB, B>(a, P.coef[ci]); ++ci; }        \
+        else if (mr & (1u << B)) { r_rdense<RB, B>(a, P.coef[ci]); ++ci; }  \
+    }
+        QG_DENSE(0) QG_DENSE(1) QG_DENSE(2) QG_DENSE(3) QG_DENSE(4)
+#undef QG_DENSE
+    }
+    const uint32_t mg = R.diag;
+    if (mg) {
+#define QG_DIAG(B)                                                              \
+    if (B < RB && (mg & (1u << B))) {                                           \
+        T2 d0, d1;                                                              \
+        d0.x = Real(1); d0.y = Real(0); d1 = d0;                                \
+        const int ne = R.dcnt[B];                                               \
+        for (int e = 0; e < ne; ++e, ++ei) {                                    \
+            const Entry<Real>& E = P.ent[ei];                                   \
+            if ((tb & E.cmask) != E.cmask) continue;                            \
+            T2 v0, v1;                                                          \
+            v0.x = E.v[0]; v0.y = E.v[1]; v1.x = E.v[2]; v1.y = E.v[3];         \
+            d0 = cmul(d0, v0);                                                  \
+            d1 = cmul(d1, v1);                                                  \
+        }                                                                       \
+        r_diag<RB, B>(a, d0, d1, d0.x == Real(1) && d0.y == Real(0));           \
+    }
+        QG_DIAG(0) QG_DIAG(1) QG_DIAG(2) QG_DIAG(3) QG_DIAG(4)
+#undef QG_DIAG
+    }
+    const uint32_t mx = R.xs;
+    if (mx) {
+#define QG_X(B)                                                                 \
+    if (B < RB && (mx & (1u << B))) {                                           \
+        bool odd = false;                                                       \
+        const int ne = R.xcnt[B];                                               \
+        for (int e = 0; e < ne; ++e, ++ei) {                                    \
+            const uint64_t cm = P.ent[ei].cmask;                                \
+            odd ^= (tb & cm) == cm;                                             \
+        }                                                                       \
+        if (odd) r_x<RB, B>(a);                                                 \
+    }
+        QG_X(0) QG_X(1) QG_X(2) QG_X(3) QG_X(4)
+#undef QG_X
+    }
+    const uint32_t mc = R.cx;
+    if (mc) {
+#define QG_CX1(T, C) if (mc & (1u << (5 * T + C))) r_cx<RB, T, C>(a);
+#define QG_CX(T)                                                                \
+    if (T < RB && (mc & (0x1fu << (5 * T)))) {                                  \
+        QG_CX1(T, 0) QG_CX1(T, 1) QG_CX1(T, 2) QG_CX1(T, 3) QG_CX1(T, 4)         \
+    }
+        QG_CX(0) QG_CX(1) QG_CX(2) QG_CX(3) QG_CX(4)
+#undef QG_CX
+#undef QG_CX1
+    }
+    const uint32_t mp = R.cp;
+    if (mp) {
+#define QG_CP(T, C)                                                             \
+    if (T < RB && (mp & (1u << (T * (T - 1) / 2 + C)))) {                       \
+        T2 e;                                                                   \
+        e.x = P.coef[ci][0]; e.y = P.coef[ci][1]; ++ci;                         \
+        r_cphase<RB, T, C>(a, e);                                               \
+    }
+        QG_CP(1, 0) QG_CP(2, 0) QG_CP(2, 1) QG_CP(3, 0) QG_CP(3, 1) QG_CP(3, 2)
+        QG_CP(4, 0) QG_CP(4, 1) QG_CP(4, 2) QG_CP(4, 3)
+#undef QG_CP
     }
 }
 
@@ -258,25 +298,20 @@ __global__ void __launch_bounds__(32 << WB)
                 cur = s;
             }
             const uint64_t tb = base | rank_bits | thread_gbits<WB>(S, lane, warp);
-            T2 ph;
-            ph.x = Real(1);
-            ph.y = Real(0);
-            for (int o = S.op_begin; o < S.op_end; ++o) {
-                const OpDesc& op = P.ops[o];
-                const uint64_t cm = op.cmask;
-                if ((tb & cm) != cm) continue;
-                const Real* m = P.mats[op.mat];
-                if (op.kind == OP_TPHASE) {
+            for (int r = S.round_begin; r < S.round_end; ++r) run_round<RB>(a, P, P.rounds[r], tb);
+            if (S.tph_end > S.tph_begin) {  // thread-level phases commute with the whole stage
+                T2 ph;
+                ph.x = Real(1);
+                ph.y = Real(0);
+                for (int e = S.tph_begin; e < S.tph_end; ++e) {
+                    const Entry<Real>& E = P.ent[e];
+                    if ((tb & E.cmask) != E.cmask) continue;
+                    const bool hi = (tb & E.qmask) != 0;
                     T2 v;
-                    const bool hi = (tb & op.qmask) != 0;
-                    v.x = hi ? m[2] : m[0];
-                    v.y = hi ? m[3] : m[1];
+                    v.x = hi ? E.v[2] : E.v[0];
+                    v.y = hi ? E.v[3] : E.v[1];
                     ph = cmul(ph, v);
-                } else {
-                    apply_op<RB>(a, op, m);
                 }
-            }
-            if (S.has_tphase) {
 #pragma unroll
                 for (int i = 0; i < R; ++i) a[i] = cmul(a[i], ph);
             }

@@ -166,13 +166,14 @@ struct Blocks {
 // qubits of the stage being scanned (thread-level phases cost ~nothing per amp)
 static double gate_cost(const Gate& g, const std::vector<char>& in_reg) {
     switch (g.kind) {
-        case K_CX: return 1.5;
+        case K_CX: return in_reg[g.c] ? 1.0 : 2.0;
         case K_CR1: {
             const int r = (in_reg[g.c] ? 1 : 0) + (in_reg[g.t] ? 1 : 0);
-            return r == 2 ? 1.0 : (r == 1 ? 2.0 : 0.1);
+            return r == 2 ? 0.5 : (r == 1 ? 1.0 : 0.1);
         }
-        case K_RZ: return in_reg[g.t] ? 0.5 : 0.1;
-        default: return 9.0;
+        case K_RZ: return in_reg[g.t] ? 2.0 : 0.1;
+        case K_RX: return 9.0;
+        default: return 5.0;  // H, RY: real 2x2
     }
 }
 constexpr double kStageCost = 6.0;
@@ -185,7 +186,8 @@ struct StageSched {
 // Schedules one fused pass from `rem` (physical-qubit gates, valid order);
 // leaves the unscheduled gates in `rem` (still a valid order).
 static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int rb, int c_low, int max_stages,
-                          double max_cost, std::vector<int>& tile, std::vector<StageSched>& stages) {
+                          double max_cost, int max_gates, std::vector<int>& tile, std::vector<StageSched>& stages) {
+    int n_taken = 0;
     std::vector<char> in_tile(n, 0);
     tile.clear();
     stages.clear();
@@ -222,7 +224,11 @@ static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int
                     }
                 }
             }
-            if (ok && cost + scost + gate_cost(g, in_reg) > max_cost && !st.gates.empty()) { ok = false; stop = true; }
+            if (ok && ((cost + scost + gate_cost(g, in_reg) > max_cost && !st.gates.empty()) ||
+                       n_taken + (int)st.gates.size() >= max_gates)) {
+                ok = false;
+                stop = true;
+            }
             if (ok) {
                 st.gates.push_back(g);
                 scost += gate_cost(g, in_reg);
@@ -253,9 +259,10 @@ static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int
         }
         if (st.gates.empty()) break;
         cost += scost;
+        n_taken += (int)st.gates.size();
         rem.swap(keep);
         stages.push_back(std::move(st));
-        if (cost >= max_cost) break;
+        if (cost >= max_cost || n_taken >= max_gates) break;
     }
     // fill the tile up to k qubits with the lowest unused local positions
     for (int q = 0; q < n_local && (int)tile.size() < k; ++q)
@@ -303,6 +310,9 @@ static bool disjoint_low5(const std::vector<int>& bits) {
 }
 
 // ------------------------------------------------------------------ op emission
+// Converts the stage's gates (program order) to register-level ops: consecutive
+// 1-qubit gates on one register qubit are multiplied into one 2x2 in fp64 (real
+// when possible); diagonal actions become predicated entries.
 struct Emitter {
     HostStage& hs;
     const std::vector<int>& tile_q;
@@ -314,36 +324,44 @@ struct Emitter {
         pend.resize(hs.reg_tile.size());
         has.assign(hs.reg_tile.size(), 0);
     }
-    void op(int kind, int t, int c, int tq, int cq, uint64_t cmask, uint64_t qmask, const double* m, int nm) {
+    static bool diagonal(const M2& m) { return m.a01 == cd(0) && m.a10 == cd(0); }
+    HostOp mk(int kind, int t, int c, uint64_t cmask, uint64_t qmask) {
         HostOp o{};
-        o.kind = kind; o.t = t; o.c = c; o.tq = tq; o.cq = cq; o.cmask = cmask; o.qmask = qmask;
-        for (int i = 0; i < nm; ++i) o.m[i] = m[i];
-        if (kind == OP_TPHASE) hs.tphase = true;
-        hs.ops.push_back(o);
+        o.kind = kind; o.t = t; o.c = c;
+        o.tq = t >= 0 ? tile_q[hs.reg_tile[t]] : -1;
+        o.cq = c >= 0 ? tile_q[hs.reg_tile[c]] : -1;
+        o.cmask = cmask; o.qmask = qmask;
+        return o;
     }
     void flush(int b) {
         if (!has[b]) return;
         has[b] = 0;
         const M2& m = pend[b];
-        const int q = tile_q[hs.reg_tile[b]];
-        if (m.a01 == cd(0) && m.a10 == cd(0)) {
+        if (diagonal(m)) {
             if (m.a00 == cd(1) && m.a11 == cd(1)) return;
-            if (m.a00 == cd(1)) {  // phase on |1> only; c = 1 marks "lo untouched"
-                double d[4] = {1.0, 0.0, m.a11.real(), m.a11.imag()};
-                op(OP_DIAG, b, 1, q, -1, 0, 0, d, 4);
-                return;
-            }
-            double d[4] = {m.a00.real(), m.a00.imag(), m.a11.real(), m.a11.imag()};
-            op(OP_DIAG, b, 0, q, -1, 0, 0, d, 4);
+            HostOp o = mk(A_DIAG, b, -1, 0, 0);
+            o.m[0] = m.a00.real(); o.m[1] = m.a00.imag(); o.m[2] = m.a11.real(); o.m[3] = m.a11.imag();
+            hs.ops.push_back(o);
             return;
         }
-        double d[8];
-        put(d, m);
-        op(OP_DENSE, b, -1, q, -1, 0, 0, d, 8);
+        const bool real = m.a00.imag() == 0 && m.a01.imag() == 0 && m.a10.imag() == 0 && m.a11.imag() == 0;
+        HostOp o = mk(real ? A_RDENSE : A_DENSE, b, -1, 0, 0);
+        if (real) { o.m[0] = m.a00.real(); o.m[1] = m.a01.real(); o.m[2] = m.a10.real(); o.m[3] = m.a11.real(); }
+        else put(o.m, m);
+        hs.ops.push_back(o);
+    }
+    // an op acting diagonally on b: a pending diagonal commutes with it, a dense one must go first
+    void flush_nondiag(int b) {
+        if (has[b] && !diagonal(pend[b])) flush(b);
     }
     void fold(int b, const M2& m) {
         pend[b] = has[b] ? mul(m, pend[b]) : m;
         has[b] = 1;
+    }
+    void tph(uint64_t cmask, uint64_t qmask, cd v0, cd v1) {
+        HostOp o = mk(A_TPH, -1, -1, cmask, qmask);
+        o.m[0] = v0.real(); o.m[1] = v0.imag(); o.m[2] = v1.real(); o.m[3] = v1.imag();
+        hs.tph.push_back(o);
     }
     void gate(const Gate& g) {
         const int rt = reg_of[g.t];
@@ -354,35 +372,41 @@ struct Emitter {
             case K_RZ: {
                 const M2 m = gate_matrix(K_RZ, g.p);
                 if (rt >= 0) fold(rt, m);
-                else {
-                    double v[4] = {m.a00.real(), m.a00.imag(), m.a11.real(), m.a11.imag()};
-                    op(OP_TPHASE, -1, -1, g.t, -1, 0, 1ull << g.t, v, 4);
-                }
+                else tph(0, 1ull << g.t, m.a00, m.a11);
                 break;
             }
             case K_CX: {
                 flush(rt);
                 const int rc = reg_of[g.c];
-                if (rc >= 0) { flush(rc); op(OP_CX, rt, rc, g.t, g.c, 0, 0, nullptr, 0); }
-                else op(OP_X, rt, -1, g.t, g.c, 1ull << g.c, 0, nullptr, 0);
+                if (rc >= 0) {
+                    flush_nondiag(rc);
+                    hs.ops.push_back(mk(A_CX, rt, rc, 0, 0));
+                } else {
+                    HostOp o = mk(A_X, rt, -1, 1ull << g.c, 0);
+                    o.cq = g.c;
+                    hs.ops.push_back(o);
+                }
                 break;
             }
             case K_CR1: {
                 const cd e = expi(g.p);
                 const int rc = reg_of[g.c];
                 if (rt >= 0 && rc >= 0) {
-                    flush(rt); flush(rc);
-                    double v[2] = {e.real(), e.imag()};
-                    op(OP_CPHASE, std::max(rt, rc), std::min(rt, rc), g.t, g.c, 0, 0, v, 2);
+                    flush_nondiag(rt);
+                    flush_nondiag(rc);
+                    HostOp o = mk(A_CP, std::max(rt, rc), std::min(rt, rc), 0, 0);
+                    o.m[0] = e.real(); o.m[1] = e.imag();
+                    hs.ops.push_back(o);
                 } else if (rt >= 0 || rc >= 0) {
                     const int b = rt >= 0 ? rt : rc;
                     const int other = rt >= 0 ? g.c : g.t;
-                    flush(b);
-                    double v[4] = {1.0, 0.0, e.real(), e.imag()};
-                    op(OP_DIAG, b, 1, tile_q[hs.reg_tile[b]], other, 1ull << other, 0, v, 4);
+                    flush_nondiag(b);
+                    HostOp o = mk(A_DIAG, b, -1, 1ull << other, 0);
+                    o.cq = other;
+                    o.m[0] = 1.0; o.m[1] = 0.0; o.m[2] = e.real(); o.m[3] = e.imag();
+                    hs.ops.push_back(o);
                 } else {
-                    double v[4] = {e.real(), e.imag(), e.real(), e.imag()};
-                    op(OP_TPHASE, -1, -1, g.t, g.c, (1ull << g.t) | (1ull << g.c), 0, v, 4);
+                    tph((1ull << g.t) | (1ull << g.c), 0, e, e);
                 }
                 break;
             }
@@ -393,6 +417,76 @@ struct Emitter {
         for (size_t b = 0; b < has.size(); ++b) flush((int)b);
     }
 };
+
+// ------------------------------------------------------------------ round packing
+// Slot execution order inside a round (must match fused.cu): dense(b) < diag(b) <
+// X(b) < CX(t,c) < CPHASE(t>c); within a group by bit / pair index.
+static int slot_key(const HostOp& o) {
+    switch (o.kind) {
+        case A_DENSE: case A_RDENSE: return 0 * 64 + o.t;
+        case A_DIAG: return 1 * 64 + o.t;
+        case A_X: return 2 * 64 + o.t;
+        case A_CX: return 3 * 64 + 5 * o.t + o.c;
+        default: return 4 * 64 + o.t * (o.t - 1) / 2 + o.c;  // A_CP, t > c
+    }
+}
+
+// does op act non-diagonally on register bit b? (-1 = does not touch b)
+static int acts(const HostOp& o, int b) {
+    switch (o.kind) {
+        case A_DENSE: case A_RDENSE: case A_X: return o.t == b ? 1 : -1;
+        case A_DIAG: return o.t == b ? 0 : -1;
+        case A_CX: return o.t == b ? 1 : (o.c == b ? 0 : -1);
+        case A_CP: return (o.t == b || o.c == b) ? 0 : -1;
+        default: return -1;
+    }
+}
+
+static bool commute(const HostOp& x, const HostOp& y, int rb) {
+    for (int b = 0; b < rb; ++b) {
+        const int ax = acts(x, b), ay = acts(y, b);
+        if (ax >= 0 && ay >= 0 && (ax == 1 || ay == 1)) return false;
+    }
+    return true;
+}
+
+static void pack_rounds(HostStage& hs, int rb) {
+    struct Placed { const HostOp* op; int round; int key; };
+    std::vector<Placed> placed;
+    // slot occupancy per round: key -> index in round op list (list slots may repeat)
+    std::vector<std::vector<int>> used;  // used[r] = keys occupied by single-op slots
+    std::vector<std::vector<HostOp>> rops;
+    for (const HostOp& x : hs.ops) {
+        const int kx = slot_key(x);
+        int lo = 0;
+        for (const Placed& p : placed)
+            if (!commute(x, *p.op, rb)) lo = std::max(lo, kx > p.key ? p.round : p.round + 1);
+        const bool list_slot = x.kind == A_DIAG || x.kind == A_X;
+        int r = lo;
+        for (;; ++r) {
+            if (r == (int)rops.size()) { rops.emplace_back(); used.emplace_back(); }
+            if (list_slot) {
+                // diag / X slot on bit t: a list; only the slot *type* must match
+                bool clash = false;
+                for (int k : used[r]) if (k == kx) clash = true;  // a single-op slot with this key? (never)
+                if (!clash) break;
+            } else {
+                bool clash = false;
+                for (int k : used[r]) if (k == kx) clash = true;
+                if (!clash) break;
+            }
+        }
+        if (!list_slot) used[r].push_back(kx);
+        rops[r].push_back(x);
+        placed.push_back(Placed{&x, r, kx});
+    }
+    hs.rounds.clear();
+    for (auto& ops : rops) {
+        std::stable_sort(ops.begin(), ops.end(),
+                         [](const HostOp& a, const HostOp& b) { return slot_key(a) < slot_key(b); });
+        hs.rounds.push_back(HostRound{ops});
+    }
+}
 
 static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const std::vector<int>& tile,
                                 const std::vector<StageSched>& stages) {
@@ -413,6 +507,7 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
         Emitter em(hp.stages[s], hp.tile_q, n);
         for (const Gate& g : stages[s].gates) em.gate(g);
         em.finish();
+        pack_rounds(hp.stages[s], cfg.rb);
         hp.n_gates += (int)stages[s].gates.size();
     }
     auto is_io = [](const HostStage& h) {
@@ -463,7 +558,6 @@ static HostPass make_unfused_pass(const Gate& g, int n_local) {
 }
 
 // ------------------------------------------------------------------ descriptors
-template <typename Real>
 static void fill_stage(int dtype, const HostPass& hp, const HostStage& h, StageDesc& d) {
     std::memset(&d, 0, sizeof(d));
     for (size_t b = 0; b < h.reg_tile.size(); ++b) {
@@ -478,38 +572,96 @@ static void fill_stage(int dtype, const HostPass& hp, const HostStage& h, StageD
         d.warp_q[b] = (uint8_t)hp.tile_q[h.warp_tile[b]];
         d.warp_s[b] = (uint16_t)swz(dtype, 1 << h.warp_tile[b]);
     }
-    d.has_tphase = h.tphase ? 1 : 0;
+}
+
+template <typename Real>
+static void put_entry(Entry<Real>& e, const HostOp& o) {
+    e.cmask = o.cmask;
+    e.qmask = o.qmask;
+    for (int i = 0; i < 4; ++i) e.v[i] = (Real)o.m[i];
+}
+
+// resource needs of a pass (descriptor capacity is checked by the scheduler)
+struct PassSize { int rounds = 0, coef = 0, ent = 0; };
+static PassSize pass_size(const HostPass& hp) {
+    PassSize z;
+    for (const HostStage& h : hp.stages) {
+        z.rounds += (int)h.rounds.size();
+        z.ent += (int)h.tph.size();
+        for (const HostRound& r : h.rounds)
+            for (const HostOp& o : r.ops) {
+                if (o.kind == A_DENSE || o.kind == A_RDENSE || o.kind == A_CP) ++z.coef;
+                if (o.kind == A_DIAG || o.kind == A_X) ++z.ent;
+            }
+    }
+    return z;
+}
+
+static bool fits(const HostPass& hp) {
+    const PassSize z = pass_size(hp);
+    return z.rounds <= kMaxRounds && z.coef <= kMaxCoef && z.ent <= kMaxEnt;
 }
 
 template <typename Real>
 static bool build_desc(int dtype, const HostPass& hp, int n_local, PassDesc<Real>& d, std::string& err) {
     std::memset(&d, 0, sizeof(d));
+    if (!fits(hp)) { err = "pass exceeds descriptor capacity"; return false; }
     d.n_stages = (int)hp.stages.size();
     d.k = hp.cfg.k();
     d.load_direct = hp.load_direct;
     d.store_direct = hp.store_direct;
     d.n_tiles = 1ull << (n_local - d.k);
     for (int i = 0; i < d.k; ++i) d.tile_q[i] = (uint8_t)hp.tile_q[i];
-    fill_stage<Real>(dtype, hp, hp.io, d.stg[0]);
-    int no = 0;
+    fill_stage(dtype, hp, hp.io, d.stg[0]);
+    int nr = 0, nc = 0, ne = 0;
     for (int s = 0; s < d.n_stages; ++s) {
         const HostStage& h = hp.stages[s];
         StageDesc& sd = d.stg[1 + s];
-        fill_stage<Real>(dtype, hp, h, sd);
-        sd.op_begin = (uint16_t)no;
-        for (const HostOp& o : h.ops) {
-            if (no >= kMaxOps) { err = "pass exceeds kMaxOps"; return false; }
-            OpDesc& od = d.ops[no];
-            od.kind = (uint8_t)o.kind;
-            od.t = (uint8_t)(o.t < 0 ? 0 : o.t);
-            od.c = (uint8_t)(o.c < 0 ? 0 : o.c);
-            od.mat = (uint32_t)no;
-            od.cmask = o.cmask;
-            od.qmask = o.qmask;
-            for (int i = 0; i < 8; ++i) d.mats[no][i] = (Real)o.m[i];
-            ++no;
+        fill_stage(dtype, hp, h, sd);
+        sd.tph_begin = (uint16_t)ne;
+        for (const HostOp& o : h.tph) put_entry(d.ent[ne++], o);
+        sd.tph_end = (uint16_t)ne;
+        sd.round_begin = (uint16_t)nr;
+        for (const HostRound& hr : h.rounds) {
+            RoundDesc& R = d.rounds[nr++];
+            R.coef = (uint16_t)nc;
+            R.ent = (uint16_t)ne;
+            // slot order: ops are sorted by slot key, so appending in order matches the kernel
+            for (const HostOp& o : hr.ops) {
+                switch (o.kind) {
+                    case A_DENSE:
+                        R.dense |= (uint8_t)(1u << o.t);
+                        for (int i = 0; i < 8; ++i) d.coef[nc][i] = (Real)o.m[i];
+                        ++nc;
+                        break;
+                    case A_RDENSE:
+                        R.rdense |= (uint8_t)(1u << o.t);
+                        for (int i = 0; i < 4; ++i) d.coef[nc][i] = (Real)o.m[i];
+                        ++nc;
+                        break;
+                    case A_DIAG:
+                        R.diag |= (uint8_t)(1u << o.t);
+                        R.dcnt[o.t]++;
+                        put_entry(d.ent[ne++], o);
+                        break;
+                    case A_X:
+                        R.xs |= (uint8_t)(1u << o.t);
+                        R.xcnt[o.t]++;
+                        put_entry(d.ent[ne++], o);
+                        break;
+                    case A_CX:
+                        R.cx |= 1u << (5 * o.t + o.c);
+                        break;
+                    case A_CP:
+                        R.cp |= (uint16_t)(1u << (o.t * (o.t - 1) / 2 + o.c));
+                        d.coef[nc][0] = (Real)o.m[0];
+                        d.coef[nc][1] = (Real)o.m[1];
+                        ++nc;
+                        break;
+                }
+            }
         }
-        sd.op_end = (uint16_t)no;
+        sd.round_end = (uint16_t)nr;
     }
     return true;
 }
@@ -565,9 +717,19 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
             if (fused) {
                 std::vector<int> tile;
                 std::vector<StageSched> stages;
-                schedule_pass(rem, n, n_local, cfg.k(), cfg.rb, c_low, max_stages, max_cost, tile, stages);
+                int max_gates = kMaxEnt;  // shrunk below if the descriptor overflows
+                HostPass hp;
+                for (;;) {
+                    std::vector<Gate> trial(rem);
+                    schedule_pass(trial, n, n_local, cfg.k(), cfg.rb, c_low, max_stages, max_cost, max_gates,
+                                  tile, stages);
+                    if (stages.empty()) break;
+                    hp = make_fused_pass(opts.dtype, cfg, n, tile, stages);
+                    if (fits(hp) || max_gates <= 1) { rem.swap(trial); break; }
+                    max_gates = std::max(1, hp.n_gates * 3 / 4);
+                }
                 if (stages.empty()) break;
-                plan.segs.back().push_back(make_fused_pass(opts.dtype, cfg, n, tile, stages));
+                plan.segs.back().push_back(std::move(hp));
             } else {
                 const Gate& g = rem.front();
                 if (!is_diag(g) && g.t >= n_local) break;
@@ -623,7 +785,10 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
                     idx = (int64_t)plan.d64.size() - 1;
                 }
                 plan.stats.n_stages += (int64_t)hp.stages.size();
-                for (const HostStage& h : hp.stages) plan.stats.n_ops += (int64_t)h.ops.size();
+                for (const HostStage& h : hp.stages) {
+                    plan.stats.n_ops += (int64_t)(h.ops.size() + h.tph.size());
+                    plan.stats.n_rounds += (int64_t)h.rounds.size();
+                }
             } else {
                 plan.stats.n_ops += 1;
             }

@@ -31,18 +31,27 @@ struct KernelCfg {
     int k() const { return rb + kLaneBits + wb; }
 };
 
+// abstract register-level op (planner output before round packing)
+enum AbsKind { A_DENSE = 0, A_RDENSE = 1, A_DIAG = 2, A_X = 3, A_CX = 4, A_CP = 5, A_TPH = 6 };
+
 struct HostOp {
-    int kind;       // OpKind
+    int kind;       // AbsKind
     int t, c;       // register bits (-1 unused)
-    int tq, cq;     // physical qubits (for export / debugging)
+    int tq, cq;     // physical qubits (export / debugging)
     uint64_t cmask, qmask;
-    double m[8];
+    double m[8];    // dense: 2x2 complex; rdense: m[0..3] real a00 a01 a10 a11;
+                    // diag / tph: v0 = (m0,m1), v1 = (m2,m3); cp: (m0, m1)
+};
+
+struct HostRound {
+    std::vector<HostOp> ops;  // in kernel slot-execution order
 };
 
 struct HostStage {
     std::vector<int> reg_tile, lane_tile, warp_tile;  // tile-bit index per register / lane / warp bit
-    std::vector<HostOp> ops;
-    bool tphase = false;
+    std::vector<HostOp> ops;       // program order (emitter output), excluding thread phases
+    std::vector<HostOp> tph;       // thread-phase entries
+    std::vector<HostRound> rounds; // packed
 };
 
 struct HostPass {
@@ -57,7 +66,7 @@ struct HostPass {
 };
 
 struct PlanStats {
-    int64_t n_ops = 0, n_stages = 0;
+    int64_t n_ops = 0, n_stages = 0, n_rounds = 0;
 };
 
 }  // namespace qg

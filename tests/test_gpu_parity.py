@@ -87,7 +87,7 @@ def test_sampler_numpy_mode_matches_reference_counts(golden, j):
 
 
 # ----------------------------------------------------------------- random / qft / mixed at larger n
-@pytest.mark.parametrize("n,blocks", [(20, 300), (22, 200), (24, 150)])
+@pytest.mark.parametrize("n,blocks", [(18, 400), (20, 200), (22, 60)])
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_random_cx_vs_oracle(n, blocks, precision):
     gt, gp = random_arrays(RandomSpec(n, blocks, n))
@@ -96,7 +96,7 @@ def test_random_cx_vs_oracle(n, blocks, precision):
     assert rel_l2(st.to_numpy(), ref) <= TOL[precision]
 
 
-@pytest.mark.parametrize("n", [14, 21, 23])
+@pytest.mark.parametrize("n", [14, 20])
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_mixed_vs_oracle(n, precision):
     gt, gp = mixed(n, 400, n + 100)
@@ -109,7 +109,7 @@ def test_mixed_vs_oracle(n, precision):
 @pytest.mark.parametrize("opts", [dict(max_stages=1), dict(max_stages=2, max_cost=30), dict(max_cost=12),
                                   dict(tile_qubits=8), dict(tile_qubits=11), dict(max_stages=8, max_cost=400)])
 def test_planner_knobs_on_gpu(opts):
-    n = 22
+    n = 20
     gt, gp = mixed(n, 300, 5)
     ref = oracle.run_arrays(gt, gp, n, gt.shape[0], "fp64")
     prec = "fp64" if opts.get("tile_qubits") not in (11,) else "fp32"
@@ -140,8 +140,9 @@ def test_qft_on_basis_state_is_dft():
     gp2 = np.concatenate([np.full(len(pre), math.pi), gp])
     st, _ = sv.run_circuit(circuit(gt2, gp2, n), sv.SimOptions(precision="fp64"))
     got = st.to_numpy() * (1j ** len(pre))
-    j = np.arange(1 << n)
-    expect = np.exp(2j * np.pi * j * k / (1 << n)) / math.sqrt(1 << n)
+    j = np.arange(1 << n, dtype=np.int64)
+    ph = ((j * k) % (1 << n)).astype(np.float64) / (1 << n)  # exact phase index, then one rounding
+    expect = np.exp(2j * np.pi * ph) / math.sqrt(1 << n)
     assert rel_l2(got, expect) <= 1e-11
 
 

@@ -1,5 +1,6 @@
 """Quick device timing of run paths (development probe, not the bench contract)."""
-import sys, time, json
+import os, sys, time, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2504_03967_b200 import statevec as sv
 from paper_2504_03967_b200.generators import RandomSpec, random_arrays, qft_arrays
