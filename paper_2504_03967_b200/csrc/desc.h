@@ -38,13 +38,17 @@ struct RoundDesc {
     uint8_t dense;       // complex 2x2 on reg bit b       (coef: 8 reals)
     uint8_t rdense;      // real 2x2 on reg bit b          (coef: 4 reals)
     uint8_t diag;        // diag slot on reg bit b         (dcnt[b] entries)
-    uint8_t xs;          // X slot on reg bit b            (xcnt[b] entries)
+    uint8_t xs;          // X slot on reg bit b            (xcnt[b] entries): folded into the
+                         // thread's register flip mask, no data movement
     uint32_t cx;         // bit 5*t + c: swap pairs of reg bit t where reg bit c = 1
     uint16_t cp;         // bit t*(t-1)/2 + c (t > c): amps with both bits *= coef
+    uint8_t dhi;         // diag slots whose d0 == 1 for every entry (only the |1> half changes)
+    uint8_t pad;
     uint8_t dcnt[kMaxRegBits];
     uint8_t xcnt[kMaxRegBits];
     uint16_t coef;       // first coef row: dense/rdense in bit order, then cp in order
     uint16_t ent;        // first entry: diag entries (bit order), then X entries (bit order)
+    uint16_t pad2;
 };
 
 template <typename Real>

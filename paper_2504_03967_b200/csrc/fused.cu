@@ -139,62 +139,118 @@ __device__ __forceinline__ void r_cphase(T2 (&a)[1 << RB], T2 e) {
     }
 }
 
-// one round: slots in the fixed order dense < diag < X < CX < CPHASE (desc.h)
+// CPHASE when the thread's register flips move the |11> quadrant to (1^ft, 1^fc)
+template <int RB, int TB, int CB, typename T2>
+__device__ __forceinline__ void r_cphase_flip(T2 (&a)[1 << RB], T2 e, uint32_t ft, uint32_t fc) {
+    if constexpr (TB < RB && CB < RB && TB != CB) {
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            const uint32_t bt = ((i >> TB) & 1) ^ ft, bc = ((i >> CB) & 1) ^ fc;
+            T2 v;
+            v.x = (bt & bc) ? e.x : decltype(e.x)(1);
+            v.y = (bt & bc) ? e.y : decltype(e.y)(0);
+            a[i] = cmul(a[i], v);
+        }
+    }
+}
+
+// select between a and b without branching (per-thread condition)
+template <typename Real>
+__device__ __forceinline__ Real sel(bool c, Real a, Real b) { return c ? a : b; }
+
+// One round: slots in the fixed order dense < diag < X < CX < CPHASE (desc.h).
+// F is the thread's register flip mask: register slot i holds the amplitude of
+// logical register index i ^ F (X ops under thread-level controls only toggle
+// F; the next transpose / store writes through the flipped addresses).
 template <int RB, typename T2, typename Real>
-__device__ __forceinline__ void run_round(T2 (&a)[1 << RB], const PassDesc<Real>& P, const RoundDesc& R, uint64_t tb) {
+__device__ __forceinline__ void run_round(T2 (&a)[1 << RB], const PassDesc<Real>& P, const RoundDesc& R, uint64_t tb,
+                                          uint32_t& F) {
     int ci = R.coef;
     int ei = R.ent;
     const uint32_t md = R.dense, mr = R.rdense;
     if (md | mr) {
-#define QG_DENSE(B)                                                        \
-    if (B < RB) {                                                          \
-        if (md & (1u << B)) { r_dense<RB, B>(a, P.coef[ci]); ++ci; }        \
-        else if (mr & (1u << B)) { r_rdense<RB, B>(a, P.coef[ci]); ++ci; }  \
+        // flipped bit: X U X = U with rows and columns swapped
+#define QG_DENSE(B)                                                                      \
+    if (B < RB) {                                                                        \
+        if (md & (1u << B)) {                                                            \
+            const Real* m = P.coef[ci];                                                  \
+            const bool f = (F >> B) & 1u;                                                \
+            Real c[8];                                                                   \
+            c[0] = sel(f, m[6], m[0]); c[1] = sel(f, m[7], m[1]);                        \
+            c[2] = sel(f, m[4], m[2]); c[3] = sel(f, m[5], m[3]);                        \
+            c[4] = sel(f, m[2], m[4]); c[5] = sel(f, m[3], m[5]);                        \
+            c[6] = sel(f, m[0], m[6]); c[7] = sel(f, m[1], m[7]);                        \
+            r_dense<RB, B>(a, c);                                                        \
+            ++ci;                                                                        \
+        }                                                                                \
+        if (mr & (1u << B)) {                                                            \
+            const Real* m = P.coef[ci];                                                  \
+            const bool f = (F >> B) & 1u;                                                \
+            Real c[4];                                                                   \
+            c[0] = sel(f, m[3], m[0]); c[1] = sel(f, m[2], m[1]);                        \
+            c[2] = sel(f, m[1], m[2]); c[3] = sel(f, m[0], m[3]);                        \
+            r_rdense<RB, B>(a, c);                                                       \
+            ++ci;                                                                        \
+        }                                                                                \
     }
         QG_DENSE(0) QG_DENSE(1) QG_DENSE(2) QG_DENSE(3) QG_DENSE(4)
 #undef QG_DENSE
     }
     const uint32_t mg = R.diag;
     if (mg) {
-#define QG_DIAG(B)                                                              \
-    if (B < RB && (mg & (1u << B))) {                                           \
-        T2 d0, d1;                                                              \
-        d0.x = Real(1); d0.y = Real(0); d1 = d0;                                \
-        const int ne = R.dcnt[B];                                               \
-        for (int e = 0; e < ne; ++e, ++ei) {                                    \
-            const Entry<Real>& E = P.ent[ei];                                   \
-            if ((tb & E.cmask) != E.cmask) continue;                            \
-            T2 v0, v1;                                                          \
-            v0.x = E.v[0]; v0.y = E.v[1]; v1.x = E.v[2]; v1.y = E.v[3];         \
-            d0 = cmul(d0, v0);                                                  \
-            d1 = cmul(d1, v1);                                                  \
-        }                                                                       \
-        r_diag<RB, B>(a, d0, d1, d0.x == Real(1) && d0.y == Real(0));           \
+        const uint32_t mh = R.dhi;
+#define QG_DIAG(B)                                                                       \
+    if (B < RB && (mg & (1u << B))) {                                                    \
+        T2 d0, d1;                                                                       \
+        d0.x = Real(1); d0.y = Real(0); d1 = d0;                                         \
+        const int ne = R.dcnt[B];                                                        \
+        for (int e = 0; e < ne; ++e, ++ei) {                                             \
+            const Entry<Real>& E = P.ent[ei];                                            \
+            if ((tb & E.cmask) != E.cmask) continue;                                     \
+            T2 v0, v1;                                                                   \
+            v0.x = E.v[0]; v0.y = E.v[1]; v1.x = E.v[2]; v1.y = E.v[3];                  \
+            d0 = cmul(d0, v0);                                                           \
+            d1 = cmul(d1, v1);                                                           \
+        }                                                                                \
+        const bool f = (F >> B) & 1u;                                                    \
+        if ((mh & (1u << B)) && !f) {                                                    \
+            r_diag<RB, B>(a, d0, d1, true);                                              \
+        } else {                                                                         \
+            T2 e0, e1;                                                                   \
+            e0.x = sel(f, d1.x, d0.x); e0.y = sel(f, d1.y, d0.y);                        \
+            e1.x = sel(f, d0.x, d1.x); e1.y = sel(f, d0.y, d1.y);                        \
+            r_diag<RB, B>(a, e0, e1, false);                                             \
+        }                                                                                \
     }
         QG_DIAG(0) QG_DIAG(1) QG_DIAG(2) QG_DIAG(3) QG_DIAG(4)
 #undef QG_DIAG
     }
     const uint32_t mx = R.xs;
     if (mx) {
-#define QG_X(B)                                                                 \
-    if (B < RB && (mx & (1u << B))) {                                           \
-        bool odd = false;                                                       \
-        const int ne = R.xcnt[B];                                               \
-        for (int e = 0; e < ne; ++e, ++ei) {                                    \
-            const uint64_t cm = P.ent[ei].cmask;                                \
-            odd ^= (tb & cm) == cm;                                             \
-        }                                                                       \
-        if (odd) r_x<RB, B>(a);                                                 \
+#define QG_X(B)                                                                          \
+    if (B < RB && (mx & (1u << B))) {                                                    \
+        uint32_t odd = 0;                                                                \
+        const int ne = R.xcnt[B];                                                        \
+        for (int e = 0; e < ne; ++e, ++ei) {                                             \
+            const uint64_t cm = P.ent[ei].cmask;                                         \
+            odd ^= (tb & cm) == cm ? 1u : 0u;                                            \
+        }                                                                                \
+        F ^= odd << B;                                                                   \
     }
         QG_X(0) QG_X(1) QG_X(2) QG_X(3) QG_X(4)
 #undef QG_X
     }
     const uint32_t mc = R.cx;
     if (mc) {
-#define QG_CX1(T, C) if (mc & (1u << (5 * T + C))) r_cx<RB, T, C>(a);
-#define QG_CX(T)                                                                \
-    if (T < RB && (mc & (0x1fu << (5 * T)))) {                                  \
-        QG_CX1(T, 0) QG_CX1(T, 1) QG_CX1(T, 2) QG_CX1(T, 3) QG_CX1(T, 4)         \
+        // a flipped control bit inverts the control: CX_inv = CX * X_t  ->  F_t ^= F_c
+#define QG_CX1(T, C)                                                                     \
+    if (mc & (1u << (5 * T + C))) {                                                      \
+        r_cx<RB, T, C>(a);                                                               \
+        F ^= ((F >> C) & 1u) << T;                                                       \
+    }
+#define QG_CX(T)                                                                         \
+    if (T < RB && (mc & (0x1fu << (5 * T)))) {                                           \
+        QG_CX1(T, 0) QG_CX1(T, 1) QG_CX1(T, 2) QG_CX1(T, 3) QG_CX1(T, 4)                  \
     }
         QG_CX(0) QG_CX(1) QG_CX(2) QG_CX(3) QG_CX(4)
 #undef QG_CX
@@ -202,11 +258,13 @@ __device__ __forceinline__ void run_round(T2 (&a)[1 << RB], const PassDesc<Real>
     }
     const uint32_t mp = R.cp;
     if (mp) {
-#define QG_CP(T, C)                                                             \
-    if (T < RB && (mp & (1u << (T * (T - 1) / 2 + C)))) {                       \
-        T2 e;                                                                   \
-        e.x = P.coef[ci][0]; e.y = P.coef[ci][1]; ++ci;                         \
-        r_cphase<RB, T, C>(a, e);                                               \
+        // flipped bits move the phased quadrant: use the general 4-quadrant form then
+#define QG_CP(T, C)                                                                      \
+    if (T < RB && (mp & (1u << (T * (T - 1) / 2 + C)))) {                                \
+        T2 e;                                                                            \
+        e.x = P.coef[ci][0]; e.y = P.coef[ci][1]; ++ci;                                  \
+        if (((F >> T) | (F >> C)) & 1u) r_cphase_flip<RB, T, C>(a, e, (F >> T) & 1u, (F >> C) & 1u); \
+        else r_cphase<RB, T, C>(a, e);                                                   \
     }
         QG_CP(1, 0) QG_CP(2, 0) QG_CP(2, 1) QG_CP(3, 0) QG_CP(3, 1) QG_CP(3, 2)
         QG_CP(4, 0) QG_CP(4, 1) QG_CP(4, 2) QG_CP(4, 3)
@@ -236,8 +294,12 @@ __device__ __forceinline__ uint32_t thread_soff(const StageDesc& S, int lane, in
 }
 
 template <int RB, int WB, typename T2>
-__device__ __forceinline__ void smem_put(T2* sm, const StageDesc& S, int lane, int warp, const T2 (&a)[1 << RB]) {
+__device__ __forceinline__ void smem_put(T2* sm, const StageDesc& S, int lane, int warp, const T2 (&a)[1 << RB],
+                                         uint32_t F) {
     uint32_t so = thread_soff<WB>(S, lane, warp);
+#pragma unroll
+    for (int b = 0; b < RB; ++b)
+        if ((F >> b) & 1u) so ^= S.reg_s[b];
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) {
         if (j) so ^= S.reg_s[ctz_c(j)];
@@ -288,17 +350,19 @@ __global__ void __launch_bounds__(32 << WB)
             }
         }
         int cur = li;
+        uint32_t F = 0;  // register flip mask (see run_round)
         for (int s = 1; s <= ns; ++s) {
             const StageDesc& S = P.stg[s];
             if (cur != s) {  // SMEM transpose into this stage's mapping
                 __syncthreads();
-                smem_put<RB, WB>(sm, P.stg[cur], lane, warp, a);
+                smem_put<RB, WB>(sm, P.stg[cur], lane, warp, a, F);
                 __syncthreads();
                 smem_get<RB, WB>(sm, S, lane, warp, a);
                 cur = s;
+                F = 0;
             }
             const uint64_t tb = base | rank_bits | thread_gbits<WB>(S, lane, warp);
-            for (int r = S.round_begin; r < S.round_end; ++r) run_round<RB>(a, P, P.rounds[r], tb);
+            for (int r = S.round_begin; r < S.round_end; ++r) run_round<RB>(a, P, P.rounds[r], tb, F);
             if (S.tph_end > S.tph_begin) {  // thread-level phases commute with the whole stage
                 T2 ph;
                 ph.x = Real(1);
@@ -318,13 +382,17 @@ __global__ void __launch_bounds__(32 << WB)
         }
         if (cur != si) {
             __syncthreads();
-            smem_put<RB, WB>(sm, P.stg[cur], lane, warp, a);
+            smem_put<RB, WB>(sm, P.stg[cur], lane, warp, a, F);
             __syncthreads();
             smem_get<RB, WB>(sm, P.stg[si], lane, warp, a);
+            F = 0;
         }
         {
             const StageDesc& S = P.stg[si];
             uint64_t g = base | thread_gbits<WB>(S, lane, warp);
+#pragma unroll
+            for (int b = 0; b < RB; ++b)
+                if ((F >> b) & 1u) g ^= 1ull << S.reg_q[b];
 #pragma unroll
             for (int j = 0; j < R; ++j) {
                 if (j) g ^= 1ull << S.reg_q[ctz_c(j)];

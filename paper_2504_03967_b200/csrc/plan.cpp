@@ -640,6 +640,8 @@ static bool build_desc(int dtype, const HostPass& hp, int n_local, PassDesc<Real
                         ++nc;
                         break;
                     case A_DIAG:
+                        if (!(R.diag & (1u << o.t))) R.dhi |= (uint8_t)(1u << o.t);
+                        if (!(o.m[0] == 1.0 && o.m[1] == 0.0)) R.dhi &= (uint8_t)~(1u << o.t);
                         R.diag |= (uint8_t)(1u << o.t);
                         R.dcnt[o.t]++;
                         put_entry(d.ent[ne++], o);
