@@ -36,12 +36,71 @@ struct V2<double> {
     using T = double2;
 };
 
+// ----------------------------------------------------------------- complex math
+// complex64 amplitudes use Blackwell's packed f32x2 FMA/MUL (FFMA2/FMUL2): a
+// complex multiply-add by a scalar complex coefficient is two instructions,
+// the (im, re) swap and the sign folded into operand modifiers by ptxas.
+// complex128 uses scalar DFMA.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float a, float b) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 upk(u64 r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// m * x, m = (mr, mi)
+__device__ __forceinline__ float2 c_mul(float2 x, float mr, float mi) {
+    return upk(fma2(pk(-mi, mi), pk(x.y, x.x), mul2(pk(mr, mr), pk(x.x, x.y))));
+}
+// acc + m * x
+__device__ __forceinline__ float2 c_fma(float2 acc, float2 x, float mr, float mi) {
+    return upk(fma2(pk(-mi, mi), pk(x.y, x.x), fma2(pk(mr, mr), pk(x.x, x.y), pk(acc.x, acc.y))));
+}
+__device__ __forceinline__ float2 r_mul(float2 x, float r) { return upk(mul2(pk(r, r), pk(x.x, x.y))); }
+__device__ __forceinline__ float2 r_fma(float2 acc, float2 x, float r) {
+    return upk(fma2(pk(r, r), pk(x.x, x.y), pk(acc.x, acc.y)));
+}
+
+__device__ __forceinline__ double2 c_mul(double2 x, double mr, double mi) {
+    double2 r;
+    r.x = mr * x.x - mi * x.y;
+    r.y = mr * x.y + mi * x.x;
+    return r;
+}
+__device__ __forceinline__ double2 c_fma(double2 acc, double2 x, double mr, double mi) {
+    acc.x += mr * x.x - mi * x.y;
+    acc.y += mr * x.y + mi * x.x;
+    return acc;
+}
+__device__ __forceinline__ double2 r_mul(double2 x, double r) {
+    x.x *= r;
+    x.y *= r;
+    return x;
+}
+__device__ __forceinline__ double2 r_fma(double2 acc, double2 x, double r) {
+    acc.x += r * x.x;
+    acc.y += r * x.y;
+    return acc;
+}
+
 template <typename T2>
 __device__ __forceinline__ T2 cmul(T2 a, T2 b) {
-    T2 r;
-    r.x = a.x * b.x - a.y * b.y;
-    r.y = a.x * b.y + a.y * b.x;
-    return r;
+    return c_mul(a, b.x, b.y);
 }
 
 __host__ __device__ constexpr int ctz_c(int x) {  // x in 1..31 (unrolled loop constant)
@@ -64,15 +123,13 @@ __device__ __forceinline__ void r_dense(T2 (&a)[1 << RB], const Real* __restrict
             if (i & (1 << TB)) continue;
             const int j = i | (1 << TB);
             const T2 x = a[i], y = a[j];
-            a[i].x = m00r * x.x - m00i * x.y + m01r * y.x - m01i * y.y;
-            a[i].y = m00r * x.y + m00i * x.x + m01r * y.y + m01i * y.x;
-            a[j].x = m10r * x.x - m10i * x.y + m11r * y.x - m11i * y.y;
-            a[j].y = m10r * x.y + m10i * x.x + m11r * y.y + m11i * y.x;
+            a[i] = c_fma(c_mul(x, m00r, m00i), y, m01r, m01i);
+            a[j] = c_fma(c_mul(x, m10r, m10i), y, m11r, m11i);
         }
     }
 }
 
-// real 2x2 (H, RY and their products): half the FMAs of the complex case
+// real 2x2 (H, RY and their products): half the work of the complex case
 template <int RB, int TB, typename T2, typename Real>
 __device__ __forceinline__ void r_rdense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
     if constexpr (TB < RB) {
@@ -82,10 +139,8 @@ __device__ __forceinline__ void r_rdense(T2 (&a)[1 << RB], const Real* __restric
             if (i & (1 << TB)) continue;
             const int j = i | (1 << TB);
             const T2 x = a[i], y = a[j];
-            a[i].x = m00 * x.x + m01 * y.x;
-            a[i].y = m00 * x.y + m01 * y.y;
-            a[j].x = m10 * x.x + m11 * y.x;
-            a[j].y = m10 * x.y + m11 * y.y;
+            a[i] = r_fma(r_mul(x, m00), y, m01);
+            a[j] = r_fma(r_mul(x, m10), y, m11);
         }
     }
 }
@@ -319,7 +374,7 @@ __device__ __forceinline__ void smem_get(const T2* sm, const StageDesc& S, int l
 
 // ----------------------------------------------------------------- the kernel
 template <typename Real, int RB, int WB>
-__global__ void __launch_bounds__(32 << WB)
+__global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 : 2)
     fused_pass_kernel(const __grid_constant__ PassDesc<Real> P, typename V2<Real>::T* __restrict__ psi,
                       uint64_t rank_bits) {
     using T2 = typename V2<Real>::T;
@@ -463,11 +518,13 @@ static cudaError_t launch_fused_t(const PassDesc<Real>& P, void* psi, uint64_t r
 }
 
 cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uint64_t rank_bits, cudaStream_t st) {
+    // must match kCfgC64 / kCfgC128 in plan.cpp
     if (dtype == 0) {
         const auto& P = *static_cast<const PassDesc<float>*>(desc);
         switch (cfg_id) {
-            case 0: return launch_fused_t<float, 5, 3>(P, psi, rank_bits, st);
-            case 1: return launch_fused_t<float, 4, 2>(P, psi, rank_bits, st);
+            case 0: return launch_fused_t<float, 4, 4>(P, psi, rank_bits, st);
+            case 1: return launch_fused_t<float, 4, 3>(P, psi, rank_bits, st);
+            case 2: return launch_fused_t<float, 4, 2>(P, psi, rank_bits, st);
             default: return launch_fused_t<float, 3, 0>(P, psi, rank_bits, st);
         }
     }

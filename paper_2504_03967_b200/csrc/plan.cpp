@@ -120,19 +120,22 @@ static int validate(const int32_t* gt, const double* gp, int64_t n_gates, int n,
 }
 
 // ------------------------------------------------------------------ kernel configs
-static const KernelCfg kCfgC64[] = {{0, 5, 3}, {1, 4, 2}, {2, 3, 0}};
+// must match launch_fused in fused.cu
+static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}};
 static const KernelCfg kCfgC128[] = {{0, 4, 3}, {1, 3, 2}, {2, 3, 0}};
+static int n_cfgs(int dtype) { return dtype == QG_DTYPE_C64 ? 4 : 3; }
 
 static bool pick_cfg(int dtype, int n_local, int force_k, KernelCfg& out) {
     const KernelCfg* cfgs = dtype == QG_DTYPE_C64 ? kCfgC64 : kCfgC128;
+    const int nc = n_cfgs(dtype);
     if (force_k > 0) {
-        for (int i = 0; i < 3; ++i)
+        for (int i = 0; i < nc; ++i)
             if (cfgs[i].k() == force_k && force_k <= n_local) { out = cfgs[i]; return true; }
         return false;
     }
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < nc; ++i)
         if (n_local - cfgs[i].k() >= 8) { out = cfgs[i]; return true; }
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < nc; ++i)
         if (cfgs[i].k() <= n_local) { out = cfgs[i]; return true; }
     return false;
 }

@@ -30,6 +30,6 @@ for n in n_list:
     gt, gp = qft_arrays(n)
     time_plan("qft", gt, gp, n, "fp32")
 gt, gp = random_arrays(RandomSpec(28, 1000, 0))
-for kw in [dict(max_stages=1), dict(max_stages=2), dict(max_cost=60), dict(max_cost=150), dict(max_stages=6, max_cost=200), dict(tile_qubits=11)]:
+for kw in [dict(max_stages=1), dict(max_stages=2), dict(max_cost=60), dict(max_cost=150), dict(max_stages=6, max_cost=200), dict(tile_qubits=12), dict(tile_qubits=11)]:
     time_plan("random", gt, gp, 28, "fp32", **kw)
 time_plan("random-unfused", gt[:300], gp[:300], 28, "fp32", fuse=False)
