@@ -63,17 +63,19 @@ __device__ __forceinline__ u64 mul2(u64 a, u64 b) {
     return d;
 }
 
+// Operand order matters: data first (ptxas folds the (im, re) swap and the
+// partial negate into operand A), coefficient second (scalar broadcast .F32).
 // m * x, m = (mr, mi)
 __device__ __forceinline__ float2 c_mul(float2 x, float mr, float mi) {
-    return upk(fma2(pk(-mi, mi), pk(x.y, x.x), mul2(pk(mr, mr), pk(x.x, x.y))));
+    return upk(fma2(pk(-x.y, x.x), pk(mi, mi), mul2(pk(x.x, x.y), pk(mr, mr))));
 }
 // acc + m * x
 __device__ __forceinline__ float2 c_fma(float2 acc, float2 x, float mr, float mi) {
-    return upk(fma2(pk(-mi, mi), pk(x.y, x.x), fma2(pk(mr, mr), pk(x.x, x.y), pk(acc.x, acc.y))));
+    return upk(fma2(pk(-x.y, x.x), pk(mi, mi), fma2(pk(x.x, x.y), pk(mr, mr), pk(acc.x, acc.y))));
 }
-__device__ __forceinline__ float2 r_mul(float2 x, float r) { return upk(mul2(pk(r, r), pk(x.x, x.y))); }
+__device__ __forceinline__ float2 r_mul(float2 x, float r) { return upk(mul2(pk(x.x, x.y), pk(r, r))); }
 __device__ __forceinline__ float2 r_fma(float2 acc, float2 x, float r) {
-    return upk(fma2(pk(r, r), pk(x.x, x.y), pk(acc.x, acc.y)));
+    return upk(fma2(pk(x.x, x.y), pk(r, r), pk(acc.x, acc.y)));
 }
 
 __device__ __forceinline__ double2 c_mul(double2 x, double mr, double mi) {
@@ -348,27 +350,38 @@ __device__ __forceinline__ uint32_t thread_soff(const StageDesc& S, int lane, in
     return s;
 }
 
+// SMEM offsets are kept in BYTES (swizzled amplitude index * sizeof(T2)) so an
+// access is one LOP3 (xor) + STS/LDS [reg + smem_base] with no scaling.
 template <int RB, int WB, typename T2>
-__device__ __forceinline__ void smem_put(T2* sm, const StageDesc& S, int lane, int warp, const T2 (&a)[1 << RB],
+__device__ __forceinline__ void smem_put(char* sm, const StageDesc& S, int lane, int warp, const T2 (&a)[1 << RB],
                                          uint32_t F) {
+    constexpr int sh = sizeof(T2) == 8 ? 3 : 4;
     uint32_t so = thread_soff<WB>(S, lane, warp);
 #pragma unroll
     for (int b = 0; b < RB; ++b)
         if ((F >> b) & 1u) so ^= S.reg_s[b];
+    so <<= sh;
+    uint32_t rs[RB];
+#pragma unroll
+    for (int b = 0; b < RB; ++b) rs[b] = (uint32_t)S.reg_s[b] << sh;
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) {
-        if (j) so ^= S.reg_s[ctz_c(j)];
-        sm[so] = a[gray_c(j)];
+        if (j) so ^= rs[ctz_c(j)];
+        *reinterpret_cast<T2*>(sm + so) = a[gray_c(j)];
     }
 }
 
 template <int RB, int WB, typename T2>
-__device__ __forceinline__ void smem_get(const T2* sm, const StageDesc& S, int lane, int warp, T2 (&a)[1 << RB]) {
-    uint32_t so = thread_soff<WB>(S, lane, warp);
+__device__ __forceinline__ void smem_get(const char* sm, const StageDesc& S, int lane, int warp, T2 (&a)[1 << RB]) {
+    constexpr int sh = sizeof(T2) == 8 ? 3 : 4;
+    uint32_t so = thread_soff<WB>(S, lane, warp) << sh;
+    uint32_t rs[RB];
+#pragma unroll
+    for (int b = 0; b < RB; ++b) rs[b] = (uint32_t)S.reg_s[b] << sh;
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) {
-        if (j) so ^= S.reg_s[ctz_c(j)];
-        a[gray_c(j)] = sm[so];
+        if (j) so ^= rs[ctz_c(j)];
+        a[gray_c(j)] = *reinterpret_cast<const T2*>(sm + so);
     }
 }
 
@@ -380,7 +393,7 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
     using T2 = typename V2<Real>::T;
     constexpr int R = 1 << RB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T2* sm = reinterpret_cast<T2*>(smem_raw);
+    char* sm = reinterpret_cast<char*>(smem_raw);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int ns = P.n_stages;
