@@ -297,21 +297,26 @@ __device__ __forceinline__ void run_round(T2 (&a)[1 << RB], const PassDesc<Real>
         QG_X(0) QG_X(1) QG_X(2) QG_X(3) QG_X(4)
 #undef QG_X
     }
-    const uint32_t mc = R.cx;
-    if (mc) {
-        // a flipped control bit inverts the control: CX_inv = CX * X_t  ->  F_t ^= F_c
-#define QG_CX1(T, C)                                                                     \
-    if (mc & (1u << (5 * T + C))) {                                                      \
-        r_cx<RB, T, C>(a);                                                               \
-        F ^= ((F >> C) & 1u) << T;                                                       \
-    }
-#define QG_CX(T)                                                                         \
-    if (T < RB && (mc & (0x1fu << (5 * T)))) {                                           \
-        QG_CX1(T, 0) QG_CX1(T, 1) QG_CX1(T, 2) QG_CX1(T, 3) QG_CX1(T, 4)                  \
-    }
-        QG_CX(0) QG_CX(1) QG_CX(2) QG_CX(3) QG_CX(4)
-#undef QG_CX
-#undef QG_CX1
+    uint32_t mc = R.cx;
+    // iterate over the set CX slots in (t, c) order; one switch case per slot keeps
+    // every body a real branch (if-converted bodies would all be issued predicated)
+    while (mc) {
+        const int k = __ffs(mc) - 1;
+        mc &= mc - 1;
+        switch (k) {
+#define QG_CXK(T, C)                                                                     \
+    case 5 * T + C:                                                                      \
+        if constexpr (T < RB && C < RB && T != C) {                                      \
+            r_cx<RB, T, C>(a);                                                           \
+            F ^= ((F >> C) & 1u) << T;                                                   \
+        }                                                                                \
+        break;
+#define QG_CXT(T) QG_CXK(T, 0) QG_CXK(T, 1) QG_CXK(T, 2) QG_CXK(T, 3) QG_CXK(T, 4)
+            QG_CXT(0) QG_CXT(1) QG_CXT(2) QG_CXT(3) QG_CXT(4)
+#undef QG_CXT
+#undef QG_CXK
+            default: break;
+        }
     }
     const uint32_t mp = R.cp;
     if (mp) {
