@@ -129,7 +129,7 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
         for (const auto& hp : seg) {
             if (hp.fused) {
                 // kernel execution order: per stage the thread phases, then rounds slot by slot
-                static const int kExport[] = {0, 0, 1, 2, 3, 4, 5};  // AbsKind -> interpreter op kind
+                static const int kExport[] = {0, 0, 1, 2, 3, 4, 5, 1};  // AbsKind -> interpreter op kind
                 for (size_t s = 0; s < hp.stages.size(); ++s) {
                     const auto& st = hp.stages[s];
                     auto emit = [&](const qg::HostOp& o) {
@@ -152,6 +152,7 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
                     for (const auto& o : st.tph) emit(o);
                     for (const auto& r : st.rounds)
                         for (const auto& o : r.ops) emit(o);
+                    for (const auto& o : st.deferred) emit(o);  // absorbed into the out map
                 }
             } else {
                 if (rec) {

@@ -37,16 +37,16 @@ constexpr int kMaxTile = 16;
 struct RoundDesc {
     uint8_t dense;       // complex 2x2 on reg bit b       (coef: 8 reals)
     uint8_t rdense;      // real 2x2 on reg bit b          (coef: 4 reals)
-    uint8_t diag;        // diag slot on reg bit b         (dcnt[b] entries)
+    uint8_t cdiag;       // constant diag(d0, d1) on reg bit b (coef: 4 reals)
+    uint8_t diag;        // predicated diag slot on reg bit b (dcnt[b] entries)
     uint8_t xs;          // X slot on reg bit b            (xcnt[b] entries): folded into the
                          // thread's register flip mask, no data movement
     uint32_t cx;         // bit 5*t + c: swap pairs of reg bit t where reg bit c = 1
     uint16_t cp;         // bit t*(t-1)/2 + c (t > c): amps with both bits *= coef
     uint8_t dhi;         // diag slots whose d0 == 1 for every entry (only the |1> half changes)
-    uint8_t pad;
     uint8_t dcnt[kMaxRegBits];
     uint8_t xcnt[kMaxRegBits];
-    uint16_t coef;       // first coef row: dense/rdense in bit order, then cp in order
+    uint16_t coef;       // first coef row: dense/rdense in bit order, cdiag in bit order, then cp
     uint16_t ent;        // first entry: diag entries (bit order), then X entries (bit order)
     uint16_t pad2;
 };
@@ -65,9 +65,14 @@ struct StageDesc {
     uint8_t lane_q[kLaneBits];
     uint8_t warp_q[kMaxWarpBits];
     uint8_t pad[2];
-    uint16_t reg_s[kMaxRegBits];
+    uint16_t reg_s[kMaxRegBits];   // input mapping: SMEM offset of each register bit
     uint16_t lane_s[kLaneBits];
     uint16_t warp_s[kMaxWarpBits];
+    // output mapping (transpose out / global store): the register bits' tile-index
+    // vectors after the stage's deferred register CX gates (a GF(2)-linear map),
+    // as SMEM offsets and as global index masks
+    uint16_t out_s[kMaxRegBits];
+    uint64_t out_g[kMaxRegBits];
 };
 
 template <typename Real>
@@ -78,6 +83,7 @@ struct PassDesc {
     int32_t store_direct;  // 1: store from the last stage; 0: transpose to io then store
     uint64_t n_tiles;      // 2^(n_local - k)
     uint8_t tile_q[kMaxTile];  // sorted physical positions of the tile bits
+    uint8_t comp_q[48];        // local positions outside the tile, ascending (tile id bits)
     // stg[0] = coalesced io mapping (lanes = tile bits 0..4); stg[1 + s] = compute stage s
     StageDesc stg[kMaxStages + 1];
     RoundDesc rounds[kMaxRounds];

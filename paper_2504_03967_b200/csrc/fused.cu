@@ -25,6 +25,9 @@
 
 namespace qg {
 
+static_assert(sizeof(PassDesc<double>) <= 32764, "pass descriptor exceeds the kernel-parameter limit");
+static_assert(sizeof(PassDesc<float>) <= 32764, "pass descriptor exceeds the kernel-parameter limit");
+
 template <typename Real>
 struct V2;
 template <>
@@ -215,7 +218,7 @@ __device__ __forceinline__ void r_cphase_flip(T2 (&a)[1 << RB], T2 e, uint32_t f
 template <typename Real>
 __device__ __forceinline__ Real sel(bool c, Real a, Real b) { return c ? a : b; }
 
-// One round: slots in the fixed order dense < diag < X < CX < CPHASE (desc.h).
+// One round: slots in the fixed order dense < cdiag < diag < X < CX < CPHASE (desc.h).
 // F is the thread's register flip mask: register slot i holds the amplitude of
 // logical register index i ^ F (X ops under thread-level controls only toggle
 // F; the next transpose / store writes through the flipped addresses).
@@ -252,6 +255,21 @@ __device__ __forceinline__ void run_round(T2 (&a)[1 << RB], const PassDesc<Real>
     }
         QG_DENSE(0) QG_DENSE(1) QG_DENSE(2) QG_DENSE(3) QG_DENSE(4)
 #undef QG_DENSE
+    }
+    const uint32_t mk = R.cdiag;
+    if (mk) {
+#define QG_CDIAG(B)                                                                      \
+    if (B < RB && (mk & (1u << B))) {                                                    \
+        const Real* m = P.coef[ci];                                                      \
+        ++ci;                                                                            \
+        const bool f = (F >> B) & 1u;                                                    \
+        T2 d0, d1;                                                                       \
+        d0.x = sel(f, m[2], m[0]); d0.y = sel(f, m[3], m[1]);                            \
+        d1.x = sel(f, m[0], m[2]); d1.y = sel(f, m[1], m[3]);                            \
+        r_diag<RB, B>(a, d0, d1, false);                                                 \
+    }
+        QG_CDIAG(0) QG_CDIAG(1) QG_CDIAG(2) QG_CDIAG(3) QG_CDIAG(4)
+#undef QG_CDIAG
     }
     const uint32_t mg = R.diag;
     if (mg) {
@@ -357,18 +375,16 @@ __device__ __forceinline__ uint32_t thread_soff(const StageDesc& S, int lane, in
 
 // SMEM offsets are kept in BYTES (swizzled amplitude index * sizeof(T2)) so an
 // access is one LOP3 (xor) + STS/LDS [reg + smem_base] with no scaling.
-template <int RB, int WB, typename T2>
-__device__ __forceinline__ void smem_put(char* sm, const StageDesc& S, int lane, int warp, const T2 (&a)[1 << RB],
+template <int RB, typename T2>
+__device__ __forceinline__ void smem_put(char* sm, const StageDesc& S, uint32_t so, const T2 (&a)[1 << RB],
                                          uint32_t F) {
     constexpr int sh = sizeof(T2) == 8 ? 3 : 4;
-    uint32_t so = thread_soff<WB>(S, lane, warp);
-#pragma unroll
-    for (int b = 0; b < RB; ++b)
-        if ((F >> b) & 1u) so ^= S.reg_s[b];
-    so <<= sh;
     uint32_t rs[RB];
 #pragma unroll
-    for (int b = 0; b < RB; ++b) rs[b] = (uint32_t)S.reg_s[b] << sh;
+    for (int b = 0; b < RB; ++b) rs[b] = (uint32_t)S.out_s[b] << sh;
+#pragma unroll
+    for (int b = 0; b < RB; ++b)
+        if ((F >> b) & 1u) so ^= rs[b];
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) {
         if (j) so ^= rs[ctz_c(j)];
@@ -376,10 +392,9 @@ __device__ __forceinline__ void smem_put(char* sm, const StageDesc& S, int lane,
     }
 }
 
-template <int RB, int WB, typename T2>
-__device__ __forceinline__ void smem_get(const char* sm, const StageDesc& S, int lane, int warp, T2 (&a)[1 << RB]) {
+template <int RB, typename T2>
+__device__ __forceinline__ void smem_get(const char* sm, const StageDesc& S, uint32_t so, T2 (&a)[1 << RB]) {
     constexpr int sh = sizeof(T2) == 8 ? 3 : 4;
-    uint32_t so = thread_soff<WB>(S, lane, warp) << sh;
     uint32_t rs[RB];
 #pragma unroll
     for (int b = 0; b < RB; ++b) rs[b] = (uint32_t)S.reg_s[b] << sh;
@@ -391,31 +406,74 @@ __device__ __forceinline__ void smem_get(const char* sm, const StageDesc& S, int
 }
 
 // ----------------------------------------------------------------- the kernel
+// Dynamic SMEM layout: [tile: 2^k amplitudes] [tile-id -> base index tables:
+// 4 x 256 u64] [per mapping m (io + stages): lane -> global bits (32 u64),
+// warp -> global bits (16 u64), lane -> SMEM byte offset (32 u32), warp -> SMEM
+// byte offset (16 u32)].  The tables are built once per CTA, so per tile and
+// per stage a thread's index bits cost a few LDS instead of bit-deposit loops.
+constexpr int kMapG = 48;   // u64 entries per mapping (32 lanes + 16 warps)
+constexpr int kMapS = 48;   // u32 entries per mapping
+__host__ __device__ constexpr size_t tables_bytes() {
+    return 4 * 256 * 8 + (kMaxStages + 1) * (kMapG * 8 + kMapS * 4);
+}
+
 template <typename Real, int RB, int WB>
 __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 : 2)
     fused_pass_kernel(const __grid_constant__ PassDesc<Real> P, typename V2<Real>::T* __restrict__ psi,
                       uint64_t rank_bits) {
     using T2 = typename V2<Real>::T;
     constexpr int R = 1 << RB;
+    constexpr int NT = 32 << WB;
+    constexpr int sh = sizeof(T2) == 8 ? 3 : 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     char* sm = reinterpret_cast<char*>(smem_raw);
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int k = P.k;
+    uint64_t* tbase = reinterpret_cast<uint64_t*>(smem_raw + ((size_t)sizeof(T2) << k));
+    uint64_t* tmg = tbase + 4 * 256;
+    uint32_t* tms = reinterpret_cast<uint32_t*>(tmg + (kMaxStages + 1) * kMapG);
     const int ns = P.n_stages;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+
+    // ---- per-CTA tables
+    const int n_comp = 64 - __clzll((long long)P.n_tiles) - 1;  // tile-id bits
+    for (int e = tid; e < 4 * 256; e += NT) {
+        const int t = e >> 8, v = e & 255;
+        uint64_t g = 0;
+        for (int j = 0; j < 8; ++j)
+            if (((v >> j) & 1) && 8 * t + j < n_comp) g |= 1ull << P.comp_q[8 * t + j];
+        tbase[e] = g;
+    }
+    for (int e = tid; e < (ns + 1) * kMapG; e += NT) {
+        const int m = e / kMapG, x = e % kMapG;
+        const StageDesc& S = P.stg[m];
+        uint64_t g = 0;
+        uint32_t so = 0;
+        if (x < 32) {
+            for (int l = 0; l < kLaneBits; ++l)
+                if ((x >> l) & 1) { g |= 1ull << S.lane_q[l]; so ^= S.lane_s[l]; }
+        } else {
+            for (int w = 0; w < WB; ++w)
+                if (((x - 32) >> w) & 1) { g |= 1ull << S.warp_q[w]; so ^= S.warp_s[w]; }
+        }
+        tmg[e] = g;
+        tms[e] = so << sh;
+    }
+    __syncthreads();
+
     const int li = P.load_direct ? 1 : 0;   // mapping used for the global load
     const int si = P.store_direct ? ns : 0; // mapping used for the global store
+    auto tgb = [&](int m) { return tmg[m * kMapG + lane] | tmg[m * kMapG + 32 + warp]; };
+    auto tso = [&](int m) { return tms[m * kMapS + lane] ^ tms[m * kMapS + 32 + warp]; };
     T2 a[R];
 
     for (uint64_t tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
-        // tile id -> index bits outside the tile (insert a zero at every tile qubit)
-        uint64_t base = tile;
-        for (int j = 0; j < P.k; ++j) {
-            const int p = P.tile_q[j];
-            base = ((base >> p) << (p + 1)) | (base & ((1ull << p) - 1ull));
-        }
+        const uint64_t base = tbase[tile & 255] | tbase[256 + ((tile >> 8) & 255)] |
+                              tbase[512 + ((tile >> 16) & 255)] | tbase[768 + ((tile >> 24) & 255)];
         {  // global load, Gray-code order over the register index
             const StageDesc& S = P.stg[li];
-            uint64_t g = base | thread_gbits<WB>(S, lane, warp);
+            uint64_t g = base | tgb(li);
 #pragma unroll
             for (int j = 0; j < R; ++j) {
                 if (j) g ^= 1ull << S.reg_q[ctz_c(j)];
@@ -428,13 +486,13 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
             const StageDesc& S = P.stg[s];
             if (cur != s) {  // SMEM transpose into this stage's mapping
                 __syncthreads();
-                smem_put<RB, WB>(sm, P.stg[cur], lane, warp, a, F);
+                smem_put<RB>(sm, P.stg[cur], tso(cur), a, F);
                 __syncthreads();
-                smem_get<RB, WB>(sm, S, lane, warp, a);
+                smem_get<RB>(sm, S, tso(s), a);
                 cur = s;
                 F = 0;
             }
-            const uint64_t tb = base | rank_bits | thread_gbits<WB>(S, lane, warp);
+            const uint64_t tb = base | rank_bits | tgb(s);
             for (int r = S.round_begin; r < S.round_end; ++r) run_round<RB>(a, P, P.rounds[r], tb, F);
             if (S.tph_end > S.tph_begin) {  // thread-level phases commute with the whole stage
                 T2 ph;
@@ -455,20 +513,23 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
         }
         if (cur != si) {
             __syncthreads();
-            smem_put<RB, WB>(sm, P.stg[cur], lane, warp, a, F);
+            smem_put<RB>(sm, P.stg[cur], tso(cur), a, F);
             __syncthreads();
-            smem_get<RB, WB>(sm, P.stg[si], lane, warp, a);
+            smem_get<RB>(sm, P.stg[si], tso(si), a);
             F = 0;
         }
-        {
+        {  // global store through the output mapping (deferred CX + flips folded in)
             const StageDesc& S = P.stg[si];
-            uint64_t g = base | thread_gbits<WB>(S, lane, warp);
+            uint64_t og[RB];
+#pragma unroll
+            for (int b = 0; b < RB; ++b) og[b] = S.out_g[b];
+            uint64_t g = base | tgb(si);
 #pragma unroll
             for (int b = 0; b < RB; ++b)
-                if ((F >> b) & 1u) g ^= 1ull << S.reg_q[b];
+                if ((F >> b) & 1u) g ^= og[b];
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-                if (j) g ^= 1ull << S.reg_q[ctz_c(j)];
+                if (j) g ^= og[ctz_c(j)];
                 __stcs(psi + g, a[gray_c(j)]);
             }
         }
@@ -517,7 +578,7 @@ template <typename Real, int RB, int WB>
 static cudaError_t launch_fused_t(const PassDesc<Real>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
     constexpr int threads = 32 << WB;
     const int k = RB + kLaneBits + WB;
-    const size_t smem = ((size_t)1 << k) * sizeof(typename V2<Real>::T);
+    const size_t smem = ((size_t)1 << k) * sizeof(typename V2<Real>::T) + tables_bytes();
     auto kern = fused_pass_kernel<Real, RB, WB>;
     static int max_blocks = -1;  // per instantiation: resident CTAs per SM x SMs
     if (max_blocks < 0) {

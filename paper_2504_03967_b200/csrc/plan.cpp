@@ -342,7 +342,7 @@ struct Emitter {
         const M2& m = pend[b];
         if (diagonal(m)) {
             if (m.a00 == cd(1) && m.a11 == cd(1)) return;
-            HostOp o = mk(A_DIAG, b, -1, 0, 0);
+            HostOp o = mk(A_CDIAG, b, -1, 0, 0);
             o.m[0] = m.a00.real(); o.m[1] = m.a00.imag(); o.m[2] = m.a11.real(); o.m[3] = m.a11.imag();
             hs.ops.push_back(o);
             return;
@@ -422,15 +422,16 @@ struct Emitter {
 };
 
 // ------------------------------------------------------------------ round packing
-// Slot execution order inside a round (must match fused.cu): dense(b) < diag(b) <
-// X(b) < CX(t,c) < CPHASE(t>c); within a group by bit / pair index.
+// Slot execution order inside a round (must match fused.cu): dense(b) < cdiag(b) <
+// diag(b) < X(b) < CX(t,c) < CPHASE(t>c); within a group by bit / pair index.
 static int slot_key(const HostOp& o) {
     switch (o.kind) {
         case A_DENSE: case A_RDENSE: return 0 * 64 + o.t;
-        case A_DIAG: return 1 * 64 + o.t;
-        case A_X: return 2 * 64 + o.t;
-        case A_CX: return 3 * 64 + 5 * o.t + o.c;
-        default: return 4 * 64 + o.t * (o.t - 1) / 2 + o.c;  // A_CP, t > c
+        case A_CDIAG: return 1 * 64 + o.t;
+        case A_DIAG: return 2 * 64 + o.t;
+        case A_X: return 3 * 64 + o.t;
+        case A_CX: return 4 * 64 + 5 * o.t + o.c;
+        default: return 5 * 64 + o.t * (o.t - 1) / 2 + o.c;  // A_CP, t > c
     }
 }
 
@@ -438,7 +439,7 @@ static int slot_key(const HostOp& o) {
 static int acts(const HostOp& o, int b) {
     switch (o.kind) {
         case A_DENSE: case A_RDENSE: case A_X: return o.t == b ? 1 : -1;
-        case A_DIAG: return o.t == b ? 0 : -1;
+        case A_DIAG: case A_CDIAG: return o.t == b ? 0 : -1;
         case A_CX: return o.t == b ? 1 : (o.c == b ? 0 : -1);
         case A_CP: return (o.t == b || o.c == b) ? 0 : -1;
         default: return -1;
@@ -451,6 +452,32 @@ static bool commute(const HostOp& x, const HostOp& y, int rb) {
         if (ax >= 0 && ay >= 0 && (ax == 1 || ay == 1)) return false;
     }
     return true;
+}
+
+// Register CX gates that commute with every later op of the stage are moved past
+// its end: their index map M (GF(2)-linear on register bits) is folded into the
+// stage's output addressing (out_vec[b] = M^-1 e_b), so they cost nothing.
+static void defer_trailing_cx(HostStage& hs, int rb) {
+    std::vector<HostOp> kept, deferred_rev;
+    for (int p = (int)hs.ops.size() - 1; p >= 0; --p) {
+        const HostOp& x = hs.ops[p];
+        bool ok = x.kind == A_CX;
+        if (ok)
+            for (const HostOp& y : kept)
+                if (!commute(x, y, rb)) { ok = false; break; }
+        if (ok) deferred_rev.push_back(x);
+        else kept.push_back(x);
+    }
+    std::reverse(kept.begin(), kept.end());
+    hs.ops.swap(kept);
+    hs.deferred.assign(deferred_rev.rbegin(), deferred_rev.rend());  // program order
+    hs.out_vec.assign(rb, 0);
+    for (int b = 0; b < rb; ++b) {
+        uint32_t v = 1u << b;
+        for (const HostOp& c : hs.deferred)  // M^-1 = C_k ... C_1 : apply C_1 first
+            if (v & (1u << c.c)) v ^= 1u << c.t;
+        hs.out_vec[b] = v;
+    }
 }
 
 static void pack_rounds(HostStage& hs, int rb) {
@@ -510,6 +537,7 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
         Emitter em(hp.stages[s], hp.tile_q, n);
         for (const Gate& g : stages[s].gates) em.gate(g);
         em.finish();
+        defer_trailing_cx(hp.stages[s], cfg.rb);
         pack_rounds(hp.stages[s], cfg.rb);
         hp.n_gates += (int)stages[s].gates.size();
     }
@@ -520,6 +548,8 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
     hp.load_direct = is_io(hp.stages[0]);
     hp.store_direct = is_io(hp.stages[S - 1]);
     assign_mapping(dtype, cfg, {}, true, hp.io);
+    hp.io.out_vec.assign(cfg.rb, 0);
+    for (int b = 0; b < cfg.rb; ++b) hp.io.out_vec[b] = 1u << b;
     return hp;
 }
 
@@ -575,6 +605,18 @@ static void fill_stage(int dtype, const HostPass& hp, const HostStage& h, StageD
         d.warp_q[b] = (uint8_t)hp.tile_q[h.warp_tile[b]];
         d.warp_s[b] = (uint16_t)swz(dtype, 1 << h.warp_tile[b]);
     }
+    for (size_t b = 0; b < h.reg_tile.size(); ++b) {
+        const uint32_t v = b < h.out_vec.size() ? h.out_vec[b] : (1u << b);
+        int tidx = 0;
+        uint64_t g = 0;
+        for (size_t r = 0; r < h.reg_tile.size(); ++r)
+            if (v & (1u << r)) {
+                tidx |= 1 << h.reg_tile[r];
+                g |= 1ull << hp.tile_q[h.reg_tile[r]];
+            }
+        d.out_s[b] = (uint16_t)swz(dtype, tidx);
+        d.out_g[b] = g;
+    }
 }
 
 template <typename Real>
@@ -593,7 +635,7 @@ static PassSize pass_size(const HostPass& hp) {
         z.ent += (int)h.tph.size();
         for (const HostRound& r : h.rounds)
             for (const HostOp& o : r.ops) {
-                if (o.kind == A_DENSE || o.kind == A_RDENSE || o.kind == A_CP) ++z.coef;
+                if (o.kind == A_DENSE || o.kind == A_RDENSE || o.kind == A_CP || o.kind == A_CDIAG) ++z.coef;
                 if (o.kind == A_DIAG || o.kind == A_X) ++z.ent;
             }
     }
@@ -615,6 +657,11 @@ static bool build_desc(int dtype, const HostPass& hp, int n_local, PassDesc<Real
     d.store_direct = hp.store_direct;
     d.n_tiles = 1ull << (n_local - d.k);
     for (int i = 0; i < d.k; ++i) d.tile_q[i] = (uint8_t)hp.tile_q[i];
+    {
+        int nc0 = 0;
+        for (int q = 0; q < n_local; ++q)
+            if (std::find(hp.tile_q.begin(), hp.tile_q.end(), q) == hp.tile_q.end()) d.comp_q[nc0++] = (uint8_t)q;
+    }
     fill_stage(dtype, hp, hp.io, d.stg[0]);
     int nr = 0, nc = 0, ne = 0;
     for (int s = 0; s < d.n_stages; ++s) {
@@ -639,6 +686,11 @@ static bool build_desc(int dtype, const HostPass& hp, int n_local, PassDesc<Real
                         break;
                     case A_RDENSE:
                         R.rdense |= (uint8_t)(1u << o.t);
+                        for (int i = 0; i < 4; ++i) d.coef[nc][i] = (Real)o.m[i];
+                        ++nc;
+                        break;
+                    case A_CDIAG:
+                        R.cdiag |= (uint8_t)(1u << o.t);
                         for (int i = 0; i < 4; ++i) d.coef[nc][i] = (Real)o.m[i];
                         ++nc;
                         break;

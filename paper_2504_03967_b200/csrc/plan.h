@@ -32,7 +32,7 @@ struct KernelCfg {
 };
 
 // abstract register-level op (planner output before round packing)
-enum AbsKind { A_DENSE = 0, A_RDENSE = 1, A_DIAG = 2, A_X = 3, A_CX = 4, A_CP = 5, A_TPH = 6 };
+enum AbsKind { A_DENSE = 0, A_RDENSE = 1, A_DIAG = 2, A_X = 3, A_CX = 4, A_CP = 5, A_TPH = 6, A_CDIAG = 7 };
 
 struct HostOp {
     int kind;       // AbsKind
@@ -52,6 +52,8 @@ struct HostStage {
     std::vector<HostOp> ops;       // program order (emitter output), excluding thread phases
     std::vector<HostOp> tph;       // thread-phase entries
     std::vector<HostRound> rounds; // packed
+    std::vector<HostOp> deferred;  // register CX gates moved past the stage end (absorbed in out map)
+    std::vector<uint32_t> out_vec; // per register bit: register-bit vector of its output tile index
 };
 
 struct HostPass {
