@@ -406,7 +406,8 @@ __device__ __forceinline__ void smem_get(const char* sm, const StageDesc& S, uin
 }
 
 // ----------------------------------------------------------------- the kernel
-// Dynamic SMEM layout: [tile: 2^k amplitudes] [tile-id -> base index tables:
+// Dynamic SMEM layout: [2 tile buffers: 2 x 2^k amplitudes, used alternately so
+// a transpose needs one barrier] [tile-id -> base index tables:
 // 4 x 256 u64] [per mapping m (io + stages): lane -> global bits (32 u64),
 // warp -> global bits (16 u64), lane -> SMEM byte offset (32 u32), warp -> SMEM
 // byte offset (16 u32)].  The tables are built once per CTA, so per tile and
@@ -428,7 +429,8 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
     extern __shared__ __align__(16) unsigned char smem_raw[];
     char* sm = reinterpret_cast<char*>(smem_raw);
     const int k = P.k;
-    uint64_t* tbase = reinterpret_cast<uint64_t*>(smem_raw + ((size_t)sizeof(T2) << k));
+    const uint32_t buf_bytes = (uint32_t)sizeof(T2) << k;
+    uint64_t* tbase = reinterpret_cast<uint64_t*>(smem_raw + 2 * (size_t)buf_bytes);
     uint64_t* tmg = tbase + 4 * 256;
     uint32_t* tms = reinterpret_cast<uint32_t*>(tmg + (kMaxStages + 1) * kMapG);
     const int ns = P.n_stages;
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
     auto tgb = [&](int m) { return tmg[m * kMapG + lane] | tmg[m * kMapG + 32 + warp]; };
     auto tso = [&](int m) { return tms[m * kMapS + lane] ^ tms[m * kMapS + 32 + warp]; };
     T2 a[R];
+    uint32_t buf = 0;  // byte offset of the tile buffer the next transpose writes
 
     for (uint64_t tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
         const uint64_t base = tbase[tile & 255] | tbase[256 + ((tile >> 8) & 255)] |
@@ -485,10 +488,10 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
         for (int s = 1; s <= ns; ++s) {
             const StageDesc& S = P.stg[s];
             if (cur != s) {  // SMEM transpose into this stage's mapping
+                smem_put<RB>(sm + buf, P.stg[cur], tso(cur), a, F);
                 __syncthreads();
-                smem_put<RB>(sm, P.stg[cur], tso(cur), a, F);
-                __syncthreads();
-                smem_get<RB>(sm, S, tso(s), a);
+                smem_get<RB>(sm + buf, S, tso(s), a);
+                buf ^= buf_bytes;
                 cur = s;
                 F = 0;
             }
@@ -512,10 +515,10 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
             }
         }
         if (cur != si) {
+            smem_put<RB>(sm + buf, P.stg[cur], tso(cur), a, F);
             __syncthreads();
-            smem_put<RB>(sm, P.stg[cur], tso(cur), a, F);
-            __syncthreads();
-            smem_get<RB>(sm, P.stg[si], tso(si), a);
+            smem_get<RB>(sm + buf, P.stg[si], tso(si), a);
+            buf ^= buf_bytes;
             F = 0;
         }
         {  // global store through the output mapping (deferred CX + flips folded in)
@@ -578,7 +581,7 @@ template <typename Real, int RB, int WB>
 static cudaError_t launch_fused_t(const PassDesc<Real>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
     constexpr int threads = 32 << WB;
     const int k = RB + kLaneBits + WB;
-    const size_t smem = ((size_t)1 << k) * sizeof(typename V2<Real>::T) + tables_bytes();
+    const size_t smem = 2 * ((size_t)1 << k) * sizeof(typename V2<Real>::T) + tables_bytes();
     auto kern = fused_pass_kernel<Real, RB, WB>;
     static int max_blocks = -1;  // per instantiation: resident CTAs per SM x SMs
     if (max_blocks < 0) {
