@@ -75,6 +75,8 @@ typedef struct {
     int32_t n_local;          /* qubits per shard */
     int32_t n_qubits;
     int32_t dtype;
+    int64_t param_bytes;      /* kernel-parameter bytes sent per execute (the program, host -> device) */
+    int64_t n_rounds;         /* register rounds over all stages */
 } qg_plan_info;
 
 /* one qubit-remap between segment `seg` and `seg + 1`: physical local

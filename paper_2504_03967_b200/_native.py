@@ -31,7 +31,7 @@ class PlanInfo(C.Structure):
     _fields_ = [("n_body_gates", C.c_int64), ("n_passes", C.c_int64), ("n_segments", C.c_int64),
                 ("n_remaps", C.c_int64), ("n_ops", C.c_int64), ("n_stages", C.c_int64),
                 ("tile_qubits", C.c_int32), ("n_local", C.c_int32), ("n_qubits", C.c_int32),
-                ("dtype", C.c_int32)]
+                ("dtype", C.c_int32), ("param_bytes", C.c_int64), ("n_rounds", C.c_int64)]
 
 
 class Remap(C.Structure):

@@ -106,6 +106,13 @@ int qg_plan_get_info(const qg_plan* plan, qg_plan_info* out) {
     out->n_local = plan->n_local;
     out->n_qubits = plan->n;
     out->dtype = plan->dtype;
+    out->n_rounds = plan->stats.n_rounds;
+    for (size_t s = 0; s < plan->segs.size(); ++s)
+        for (size_t p = 0; p < plan->segs[s].size(); ++p)
+            out->param_bytes += plan->desc_index[s][p] >= 0
+                                    ? (int64_t)(plan->dtype == QG_DTYPE_C64 ? sizeof(qg::PassDesc<float>)
+                                                                            : sizeof(qg::PassDesc<double>))
+                                    : (int64_t)sizeof(qg::GateOp);
     return QG_OK;
 }
 
