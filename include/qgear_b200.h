@@ -61,7 +61,8 @@ typedef struct {
     int32_t tile_qubits;      /* 0 = auto; else force the tile width k of fused passes */
     int32_t max_stages;       /* 0 = auto; register stages per pass (SMEM transposes + 1) */
     int32_t max_cost;         /* 0 = auto; per-amplitude instruction budget of one pass */
-    int32_t reserved[6];
+    int32_t kernel_cfg;       /* 0 = auto; else 1 + id of the fused-kernel configuration (tuning) */
+    int32_t reserved[5];
 } qg_plan_opts;
 
 typedef struct {
@@ -76,7 +77,8 @@ typedef struct {
     int32_t n_qubits;
     int32_t dtype;
     int64_t param_bytes;      /* kernel-parameter bytes sent per execute (the program, host -> device) */
-    int64_t n_rounds;         /* register rounds over all stages */
+    int64_t n_cxm;            /* register CX moves the kernel executes (all other register CX gates are
+                                 folded into transpose addresses) */
 } qg_plan_info;
 
 /* one qubit-remap between segment `seg` and `seg + 1`: physical local
@@ -104,9 +106,17 @@ int qg_plan_get_remap(const qg_plan* plan, int64_t remap_index, qg_remap* out);
 /* logical qubit q sits at physical position phys_of_logical[q] after the last
  * segment (identity unless remaps ran); n_qubits entries */
 int qg_plan_get_final_map(const qg_plan* plan, int32_t* phys_of_logical);
-/* debug/test export of the fused program at op granularity (physical qubits):
- *   rec[i*8 + ...] = {pass, stage, kind, target, control, cmask, qmask, mat}
- *   mats[m*8 + ...] = 2x2 (or diagonal / phase) coefficients in float64
+/* debug/test export of the fused program at kernel-op granularity, exactly
+ * what the fused kernel executes (slot coordinates, desc.h):
+ *   rec[i*8 + ...] = {pass, stage, kind, t, c, cmask, qmask, mat}
+ *   kind 0 RD / 1 CD (2x2 on slot pairs {p, p^t}, logical |0> member where
+ *   parity(c & p ^ c & F) = 0; mats row = complex 2x2), 2 PH (phase e where
+ *   parity(t & (p ^ F)) = 1, thread predicate cmask), 3 CXM (slot move along t
+ *   where slot bit c = 1), 4 PH2 (phase on |11> of slot bits t, c), 5 XF (flip
+ *   vector t where cmask holds), 6 TPH (thread phase v0 / v1 by qmask, where cmask
+ *   holds), 100/101 single-gate kernel (GateOp kind 0/1), 200 stage header
+ *   (t = register bits, c = packed out vectors 5 bits each, mats row = physical
+ *   qubit of each register bit).
  * Call with NULL buffers to get the counts. */
 int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* mats, int64_t* n_mats);
 

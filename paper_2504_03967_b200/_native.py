@@ -24,14 +24,14 @@ DTYPE_C128 = 1
 class PlanOpts(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("log2_ranks", C.c_int32), ("fuse", C.c_int32),
                 ("tile_qubits", C.c_int32), ("max_stages", C.c_int32), ("max_cost", C.c_int32),
-                ("reserved", C.c_int32 * 6)]
+                ("kernel_cfg", C.c_int32), ("reserved", C.c_int32 * 5)]
 
 
 class PlanInfo(C.Structure):
     _fields_ = [("n_body_gates", C.c_int64), ("n_passes", C.c_int64), ("n_segments", C.c_int64),
                 ("n_remaps", C.c_int64), ("n_ops", C.c_int64), ("n_stages", C.c_int64),
                 ("tile_qubits", C.c_int32), ("n_local", C.c_int32), ("n_qubits", C.c_int32),
-                ("dtype", C.c_int32), ("param_bytes", C.c_int64), ("n_rounds", C.c_int64)]
+                ("dtype", C.c_int32), ("param_bytes", C.c_int64), ("n_cxm", C.c_int64)]
 
 
 class Remap(C.Structure):

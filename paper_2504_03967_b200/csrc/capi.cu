@@ -106,7 +106,7 @@ int qg_plan_get_info(const qg_plan* plan, qg_plan_info* out) {
     out->n_local = plan->n_local;
     out->n_qubits = plan->n;
     out->dtype = plan->dtype;
-    out->n_rounds = plan->stats.n_rounds;
+    out->n_cxm = plan->stats.n_cxm;
     for (size_t s = 0; s < plan->segs.size(); ++s)
         for (size_t p = 0; p < plan->segs[s].size(); ++p)
             out->param_bytes += plan->desc_index[s][p] >= 0
@@ -132,47 +132,61 @@ int qg_plan_get_final_map(const qg_plan* plan, int32_t* phys_of_logical) {
 int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* mats, int64_t* n_mats) {
     if (!plan || !n_rec || !n_mats) return fail(QG_E_INVALID_ARG, "NULL argument");
     int64_t nr = 0, nm = 0, pass_id = 0;
-    for (const auto& seg : plan->segs) {
-        for (const auto& hp : seg) {
+    auto row = [&](int64_t s, int64_t kind, int64_t t, int64_t c, uint64_t cmask, uint64_t qmask, const double* m) {
+        if (rec) {
+            int64_t* r = rec + 8 * nr;
+            r[0] = pass_id; r[1] = s; r[2] = kind; r[3] = t; r[4] = c;
+            r[5] = (int64_t)cmask; r[6] = (int64_t)qmask; r[7] = nm;
+        }
+        if (mats) std::memcpy(mats + 8 * nm, m, 8 * sizeof(double));
+        ++nr; ++nm;
+    };
+    const size_t last_seg = plan->segs.size() - 1;
+    for (size_t si = 0; si < plan->segs.size(); ++si) {
+        const auto& seg = plan->segs[si];
+        for (size_t pi = 0; pi < seg.size(); ++pi) {
+            const auto& hp = seg[pi];
             if (hp.fused) {
-                // kernel execution order: per stage the thread phases, then rounds slot by slot
-                static const int kExport[] = {0, 0, 1, 2, 3, 4, 5, 1};  // AbsKind -> interpreter op kind
                 for (size_t s = 0; s < hp.stages.size(); ++s) {
                     const auto& st = hp.stages[s];
-                    auto emit = [&](const qg::HostOp& o) {
-                        if (rec) {
-                            int64_t* r = rec + 8 * nr;
-                            r[0] = pass_id; r[1] = (int64_t)s; r[2] = kExport[o.kind]; r[3] = o.tq; r[4] = o.cq;
-                            r[5] = (int64_t)o.cmask; r[6] = (int64_t)o.qmask; r[7] = nm;
+                    double hdr[8] = {0};
+                    int64_t packed = 0;
+                    for (size_t b = 0; b < st.reg_tile.size(); ++b) {
+                        hdr[b] = hp.tile_q[st.reg_tile[b]];
+                        packed |= (int64_t)st.out_vec[b] << (5 * b);
+                    }
+                    row((int64_t)s, 200, (int64_t)st.reg_tile.size(), packed, 0, 0, hdr);
+                    for (const auto& o : st.ops) {
+                        double m[8] = {0};
+                        if (o.kind == qg::A_RD) {  // real 2x2 in complex layout
+                            m[0] = o.m[0]; m[2] = o.m[1]; m[4] = o.m[2]; m[6] = o.m[3];
+                        } else {
+                            std::memcpy(m, o.m, sizeof(m));
                         }
-                        if (mats) {
-                            double* m = mats + 8 * nm;
-                            if (o.kind == qg::A_RDENSE) {  // expand the real 2x2 to complex layout
-                                const double v[8] = {o.m[0], 0, o.m[1], 0, o.m[2], 0, o.m[3], 0};
-                                std::memcpy(m, v, sizeof(v));
-                            } else {
-                                std::memcpy(m, o.m, 8 * sizeof(double));
-                            }
+                        int64_t t = o.t, c = o.c;
+                        if (o.kind == qg::A_RD || o.kind == qg::A_CD) {  // pair vector V, role vector W
+                            const int64_t e = 1ll << o.t, f = o.c >= 0 ? (1ll << o.c) : 0;
+                            t = o.form == 2 ? (e | f) : e;
+                            c = o.form == 1 ? (e | f) : e;
+                        } else if (o.kind == qg::A_PH) {  // role vector W
+                            t = (1ll << o.t) | (o.c >= 0 ? (1ll << o.c) : 0);
+                            c = -1;
                         }
-                        ++nr; ++nm;
-                    };
-                    for (const auto& o : st.tph) emit(o);
-                    for (const auto& r : st.rounds)
-                        for (const auto& o : r.ops) emit(o);
-                    for (const auto& o : st.deferred) emit(o);  // absorbed into the out map
+                        row((int64_t)s, o.kind, t, c, o.cmask, o.qmask, m);
+                    }
+                    for (const auto& o : st.tph) row((int64_t)s, qg::A_TPH, -1, -1, o.cmask, o.qmask, o.m);
+                    const bool last = si == last_seg && pi + 1 == seg.size() && s + 1 == hp.stages.size();
+                    if (last && (plan->gphase_re != 1.0 || plan->gphase_im != 0.0)) {
+                        const double g[8] = {plan->gphase_re, plan->gphase_im, plan->gphase_re, plan->gphase_im};
+                        row((int64_t)s, qg::A_TPH, -1, -1, 0, 0, g);
+                    }
                 }
             } else {
-                if (rec) {
-                    int64_t* r = rec + 8 * nr;
-                    r[0] = pass_id; r[1] = -1; r[2] = 100 + hp.gop.kind; r[3] = hp.gop.t; r[4] = -1;
-                    r[5] = (int64_t)hp.gop.cmask; r[6] = (int64_t)hp.gop.qmask; r[7] = nm;
-                }
-                if (mats) std::memcpy(mats + 8 * nm, hp.gop.m, 8 * sizeof(double));
-                ++nr; ++nm;
+                row(-1, 100 + hp.gop.kind, hp.gop.t, -1, hp.gop.cmask, hp.gop.qmask, hp.gop.m);
             }
             ++pass_id;
         }
-        ++pass_id;  // a segment boundary (remap) consumes one id
+        ++pass_id;  // a skipped pass id marks a segment boundary (remap)
     }
     *n_rec = nr;
     *n_mats = nm;

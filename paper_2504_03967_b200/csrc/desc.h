@@ -8,48 +8,88 @@
 //   pass   = tile of k qubits (2^k amplitudes, one CTA at a time)
 //   stage  = one register mapping (RB register bits, 5 lane bits, WB warp bits
 //            -> tile bits); switching stage = one SMEM transpose
-//   round  = a FIXED sequence of slots, each bound to compile-time register
-//            bits, enabled by bit masks (so the kernel never dispatches on a
-//            runtime register index — that would force register-array copies):
-//              1. 1q dense slots   b = 0..RB-1  (complex 2x2, or real 2x2)
-//              2. diag slots       b = 0..RB-1  (thread-dependent diag(d0, d1):
-//                                                 product of predicated entries)
-//              3. X slots          b = 0..RB-1  (swap if an odd number of entry
-//                                                 predicates hold)
-//              4. CX slots         (t, c) register pairs
-//              5. CPHASE slots     {t, c} register pairs
-//   thread phase = product of predicated scalar entries over thread-level
-//            qubits, applied once per stage (commutes with every slot).
+//   op     = one 32-bit word: body code (compile-time register bits baked in,
+//            so the amplitude array is never indexed at run time), a thread
+//            predicate index and a coefficient offset.  The kernel walks the
+//            stage's op list and dispatches each word through one switch.
+//
+// Register layout inside a stage (what makes CX gates free): thread slot p
+// holds the amplitude of logical register index i with
+//        p = L i  xor  F
+// L is a GF(2)-linear map shared by every thread (the register CX gates of the
+// stage so far — the planner tracks it and never touches data for them), F a
+// per-thread flip vector (X gates under a thread-level control: OC_XF).  The
+// planner emits each op in slot coordinates; at the end of the stage the map
+// (L, F) is folded into the transpose / store addresses (StageDesc.out_*).
 #pragma once
 #include <stdint.h>
+
+#ifdef __CUDACC__
+#define QG_HD __host__ __device__
+#else
+#define QG_HD
+#endif
 
 namespace qg {
 
 constexpr int kMaxStages = 8;
-constexpr int kMaxRounds = 128;
-constexpr int kMaxCoef = 96;
-constexpr int kMaxEnt = 400;
+constexpr int kMaxOps = 640;    // op words per pass
+constexpr int kMaxPred = 48;    // thread predicates (global-index masks) per pass
+constexpr int kMaxTph = 128;    // thread-phase entries per pass
 constexpr int kLaneBits = 5;
 constexpr int kMaxRegBits = 5;
 constexpr int kMaxWarpBits = 4;
 constexpr int kMaxTile = 16;
-
-struct RoundDesc {
-    uint8_t dense;       // complex 2x2 on reg bit b       (coef: 8 reals)
-    uint8_t rdense;      // real 2x2 on reg bit b          (coef: 4 reals)
-    uint8_t cdiag;       // constant diag(d0, d1) on reg bit b (coef: 4 reals)
-    uint8_t diag;        // predicated diag slot on reg bit b (dcnt[b] entries)
-    uint8_t xs;          // X slot on reg bit b            (xcnt[b] entries): folded into the
-                         // thread's register flip mask, no data movement
-    uint32_t cx;         // bit 5*t + c: swap pairs of reg bit t where reg bit c = 1
-    uint16_t cp;         // bit t*(t-1)/2 + c (t > c): amps with both bits *= coef
-    uint8_t dhi;         // diag slots whose d0 == 1 for every entry (only the |1> half changes)
-    uint8_t dcnt[kMaxRegBits];
-    uint8_t xcnt[kMaxRegBits];
-    uint16_t coef;       // first coef row: dense/rdense in bit order, cdiag in bit order, then cp
-    uint16_t ent;        // first entry: diag entries (bit order), then X entries (bit order)
-    uint16_t pad2;
+template <typename Real>
+struct CoefCap;
+template <>
+struct CoefCap<float> {
+    static constexpr int value = 2560;  // coefficient reals per pass
 };
+template <>
+struct CoefCap<double> {
+    static constexpr int value = 1280;
+};
+
+// op word: bits 0-7 body code, 8-15 predicate index (0xff = none),
+//          16-31 coefficient offset in reals / payload
+//
+// Pair ops act on slot pairs {p, p ^ V}; the member with parity(W & p) = 0 plays
+// the logical |0> role (W . V = 1).  Standard ops have V = W = e_T; the W form
+// (V = e_T, W = e_T + e_C) and the V form (V = e_T + e_C, W = e_T) cover the
+// register qubits touched by an unexecuted register CX, so those need no moves.
+// A thread whose flip vector F has parity(W & F) = 1 sees the roles swapped.
+//
+// Body codes are dense for the kernel's register width RB (one jump table):
+//   fam 0 RD   + T            real 2x2, V = W = e_T          coef: m00 m01 m10 m11
+//   fam 1 CD   + T            complex 2x2 (coef: 8 reals, row major)
+//   fam 2 PH   + T            x e where parity(W & p) ^ f = 1, W = e_T; coef: e;
+//                             predicate -> e or 1
+//   fam 3 RDW, 4 RDV, 5 CDW, 6 CDV  + pair index (T, C)   the W / V forms
+//   fam 7 PHW  + tri index (T > C)   phase with W = e_T + e_C
+//   fam 8 PH2  + tri index (T > C)   x e on logical |11> of slot bits (T, C); coef: e
+//   OC_XF      F ^= payload where the predicate holds
+//   OC_CXM     payload T | C << 4: move slot p -> p ^ (p_C) e_T (materialises part of
+//              L), F_T ^= F_C.  Executed outside the jump table (see fused.cu).
+enum OpFam { F_RD = 0, F_CD, F_PH, F_RDW, F_RDV, F_CDW, F_CDV, F_PHW, F_PH2 };
+constexpr uint32_t OC_XF = 0xfe;
+constexpr uint32_t OC_CXM = 0xff;
+constexpr uint32_t kNoPred = 0xff;
+
+QG_HD constexpr int oc_base(int fam, int rb) {
+    return fam <= F_PH ? fam * rb
+                       : (fam <= F_CDV ? 3 * rb + (fam - F_RDW) * rb * (rb - 1)
+                                       : 3 * rb + 4 * rb * (rb - 1) + (fam - F_PHW) * rb * (rb - 1) / 2);
+}
+QG_HD constexpr int oc_std(int fam, int rb, int t) { return oc_base(fam, rb) + t; }
+QG_HD constexpr int oc_pair(int fam, int rb, int t, int c) {
+    return oc_base(fam, rb) + t * (rb - 1) + (c < t ? c : c - 1);
+}
+QG_HD constexpr int oc_tri(int fam, int rb, int t, int c) { return oc_base(fam, rb) + t * (t - 1) / 2 + c; }
+
+QG_HD constexpr uint32_t op_word(uint32_t code, uint32_t pred, uint32_t coef) {
+    return code | (pred << 8) | (coef << 16);
+}
 
 template <typename Real>
 struct Entry {
@@ -59,8 +99,8 @@ struct Entry {
 };
 
 struct StageDesc {
-    uint16_t round_begin, round_end;
-    uint16_t tph_begin, tph_end;  // thread-phase entries
+    uint16_t op_begin, op_end;
+    uint16_t tph_begin, tph_end;  // thread-phase entries (applied after the ops)
     uint8_t reg_q[kMaxRegBits];
     uint8_t lane_q[kLaneBits];
     uint8_t warp_q[kMaxWarpBits];
@@ -68,9 +108,9 @@ struct StageDesc {
     uint16_t reg_s[kMaxRegBits];   // input mapping: SMEM offset of each register bit
     uint16_t lane_s[kLaneBits];
     uint16_t warp_s[kMaxWarpBits];
-    // output mapping (transpose out / global store): the register bits' tile-index
-    // vectors after the stage's deferred register CX gates (a GF(2)-linear map),
-    // as SMEM offsets and as global index masks
+    // output mapping (transpose out / global store): for slot bit j the tile-index
+    // vector of L^-1 e_j (the stage's register CX gates, GF(2)-linear), as SMEM
+    // offsets and as global index masks
     uint16_t out_s[kMaxRegBits];
     uint64_t out_g[kMaxRegBits];
 };
@@ -86,9 +126,10 @@ struct PassDesc {
     uint8_t comp_q[48];        // local positions outside the tile, ascending (tile id bits)
     // stg[0] = coalesced io mapping (lanes = tile bits 0..4); stg[1 + s] = compute stage s
     StageDesc stg[kMaxStages + 1];
-    RoundDesc rounds[kMaxRounds];
-    Real coef[kMaxCoef][8];
-    Entry<Real> ent[kMaxEnt];
+    uint64_t pred[kMaxPred];
+    uint32_t ops[kMaxOps];
+    Entry<Real> tph[kMaxTph];
+    Real coef[CoefCap<Real>::value];
 };
 
 // single-gate (unfused) op on global index bits

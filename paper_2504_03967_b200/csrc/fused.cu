@@ -114,67 +114,72 @@ __host__ __device__ constexpr int ctz_c(int x) {  // x in 1..31 (unrolled loop c
 __host__ __device__ constexpr int gray_c(int x) { return x ^ (x >> 1); }
 
 // ----------------------------------------------------------------- register ops
-// Every body below is bound to compile-time register bits (TB, CB), so the
-// amplitude array never needs runtime indexing; the round loop enables them
-// with warp-uniform mask tests (if-then diamonds the register allocator keeps
-// in place).
-template <int RB, int TB, typename T2, typename Real>
-__device__ __forceinline__ void r_dense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
-    if constexpr (TB < RB) {
-        const Real m00r = m[0], m00i = m[1], m01r = m[2], m01i = m[3];
-        const Real m10r = m[4], m10i = m[5], m11r = m[6], m11i = m[7];
+// Every body below is bound to compile-time slot vectors (V, W, TB, CB), so the
+// amplitude array is never indexed at run time: after unrolling, each body is
+// straight-line FMA code on fixed registers.
+__host__ __device__ constexpr int parity_c(uint32_t x) {
+    x ^= x >> 16; x ^= x >> 8; x ^= x >> 4; x ^= x >> 2; x ^= x >> 1;
+    return (int)(x & 1u);
+}
+
+// complex 2x2 on pairs {i, i ^ V}, i the member with parity(W & i) = 0
+template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
+__device__ __forceinline__ void p_dense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
+    const Real m00r = m[0], m00i = m[1], m01r = m[2], m01i = m[3];
+    const Real m10r = m[4], m10i = m[5], m11r = m[6], m11i = m[7];
 #pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            if (i & (1 << TB)) continue;
-            const int j = i | (1 << TB);
-            const T2 x = a[i], y = a[j];
-            a[i] = c_fma(c_mul(x, m00r, m00i), y, m01r, m01i);
-            a[j] = c_fma(c_mul(x, m10r, m10i), y, m11r, m11i);
-        }
+    for (int i = 0; i < (1 << RB); ++i) {
+        if (parity_c(W & (uint32_t)i)) continue;
+        const int j = i ^ (int)V;
+        // each output's final FMA is the last use of its own input, so the
+        // allocator writes it in place (no copies back into the array registers)
+        const T2 x = a[i], y = a[j];
+        const T2 ty = c_mul(y, m01r, m01i), tx = c_mul(x, m10r, m10i);
+        a[i] = c_fma(ty, x, m00r, m00i);
+        a[j] = c_fma(tx, y, m11r, m11i);
     }
 }
 
 // real 2x2 (H, RY and their products): half the work of the complex case
-template <int RB, int TB, typename T2, typename Real>
-__device__ __forceinline__ void r_rdense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
-    if constexpr (TB < RB) {
-        const Real m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
+template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
+__device__ __forceinline__ void p_rdense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
+    const Real m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
 #pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            if (i & (1 << TB)) continue;
-            const int j = i | (1 << TB);
-            const T2 x = a[i], y = a[j];
-            a[i] = r_fma(r_mul(x, m00), y, m01);
-            a[j] = r_fma(r_mul(x, m10), y, m11);
-        }
+    for (int i = 0; i < (1 << RB); ++i) {
+        if (parity_c(W & (uint32_t)i)) continue;
+        const int j = i ^ (int)V;
+        const T2 x = a[i], y = a[j];
+        const T2 ty = r_mul(y, m01), tx = r_mul(x, m10);
+        a[i] = r_fma(ty, x, m00);
+        a[j] = r_fma(tx, y, m11);
     }
 }
 
-template <int RB, int TB, typename T2>
-__device__ __forceinline__ void r_diag(T2 (&a)[1 << RB], T2 d0, T2 d1, bool lo_id) {
-    if constexpr (TB < RB) {
-        if (lo_id) {
+// x e on the slots with parity(W & i) == P
+template <int RB, uint32_t W, int P, typename T2>
+__device__ __forceinline__ void p_phase(T2 (&a)[1 << RB], T2 e) {
 #pragma unroll
-            for (int i = 0; i < (1 << RB); ++i)
-                if (i & (1 << TB)) a[i] = cmul(a[i], d1);
-        } else {
-#pragma unroll
-            for (int i = 0; i < (1 << RB); ++i) a[i] = cmul(a[i], (i & (1 << TB)) ? d1 : d0);
-        }
-    }
+    for (int i = 0; i < (1 << RB); ++i)
+        if (parity_c(W & (uint32_t)i) == P) a[i] = cmul(a[i], e);
 }
 
-template <int RB, int TB, typename T2>
-__device__ __forceinline__ void r_x(T2 (&a)[1 << RB]) {
-    if constexpr (TB < RB) {
+// x d0 / d1 on the slots with parity(W & i) == 0 / 1
+template <int RB, uint32_t W, typename T2>
+__device__ __forceinline__ void p_diag(T2 (&a)[1 << RB], T2 d0, T2 d1) {
 #pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            if (i & (1 << TB)) continue;
-            const T2 x = a[i];
-            a[i] = a[i | (1 << TB)];
-            a[i | (1 << TB)] = x;
-        }
-    }
+    for (int i = 0; i < (1 << RB); ++i) a[i] = cmul(a[i], parity_c(W & (uint32_t)i) ? d1 : d0);
+}
+
+// value copy through the FP pipe (x * 1): opaque to the register allocator's copy
+// coalescing, so a permuting body writes its results into the loop-carried
+// registers like any arithmetic body (plain moves make ptxas copy the whole
+// amplitude array at the op loop head)
+__device__ __forceinline__ float2 ocopy(float2 x) { return upk(mul2(pk(x.x, x.y), pk(1.0f, 1.0f))); }
+__device__ __forceinline__ double2 ocopy(double2 x) {
+    double2 r;
+    asm("mul.rn.f64 %0, %1, 0d3FF0000000000000;" : "=d"(r.x) : "d"(x.x));
+    asm("mul.rn.f64 %0, %1, 0d3FF0000000000000;" : "=d"(r.y) : "d"(x.y));
+    return r;
 }
 
 template <int RB, int TB, int CB, typename T2>
@@ -183,8 +188,8 @@ __device__ __forceinline__ void r_cx(T2 (&a)[1 << RB]) {
 #pragma unroll
         for (int i = 0; i < (1 << RB); ++i) {
             if ((i & (1 << TB)) || !(i & (1 << CB))) continue;
-            const T2 x = a[i];
-            a[i] = a[i | (1 << TB)];
+            const T2 x = ocopy(a[i]);
+            a[i] = ocopy(a[i | (1 << TB)]);
             a[i | (1 << TB)] = x;
         }
     }
@@ -199,7 +204,7 @@ __device__ __forceinline__ void r_cphase(T2 (&a)[1 << RB], T2 e) {
     }
 }
 
-// CPHASE when the thread's register flips move the |11> quadrant to (1^ft, 1^fc)
+// CPHASE when the thread's flips move the |11> quadrant to (1^ft, 1^fc)
 template <int RB, int TB, int CB, typename T2>
 __device__ __forceinline__ void r_cphase_flip(T2 (&a)[1 << RB], T2 e, uint32_t ft, uint32_t fc) {
     if constexpr (TB < RB && CB < RB && TB != CB) {
@@ -218,137 +223,158 @@ __device__ __forceinline__ void r_cphase_flip(T2 (&a)[1 << RB], T2 e, uint32_t f
 template <typename Real>
 __device__ __forceinline__ Real sel(bool c, Real a, Real b) { return c ? a : b; }
 
-// One round: slots in the fixed order dense < cdiag < diag < X < CX < CPHASE (desc.h).
-// F is the thread's register flip mask: register slot i holds the amplitude of
-// logical register index i ^ F (X ops under thread-level controls only toggle
-// F; the next transpose / store writes through the flipped addresses).
-template <int RB, typename T2, typename Real>
-__device__ __forceinline__ void run_round(T2 (&a)[1 << RB], const PassDesc<Real>& P, const RoundDesc& R, uint64_t tb,
-                                          uint32_t& F) {
-    int ci = R.coef;
-    int ei = R.ent;
-    const uint32_t md = R.dense, mr = R.rdense;
-    if (md | mr) {
-        // flipped bit: X U X = U with rows and columns swapped
-#define QG_DENSE(B)                                                                      \
-    if (B < RB) {                                                                        \
-        if (md & (1u << B)) {                                                            \
-            const Real* m = P.coef[ci];                                                  \
-            const bool f = (F >> B) & 1u;                                                \
-            Real c[8];                                                                   \
-            c[0] = sel(f, m[6], m[0]); c[1] = sel(f, m[7], m[1]);                        \
-            c[2] = sel(f, m[4], m[2]); c[3] = sel(f, m[5], m[3]);                        \
-            c[4] = sel(f, m[2], m[4]); c[5] = sel(f, m[3], m[5]);                        \
-            c[6] = sel(f, m[0], m[6]); c[7] = sel(f, m[1], m[7]);                        \
-            r_dense<RB, B>(a, c);                                                        \
-            ++ci;                                                                        \
-        }                                                                                \
-        if (mr & (1u << B)) {                                                            \
-            const Real* m = P.coef[ci];                                                  \
-            const bool f = (F >> B) & 1u;                                                \
-            Real c[4];                                                                   \
-            c[0] = sel(f, m[3], m[0]); c[1] = sel(f, m[2], m[1]);                        \
-            c[2] = sel(f, m[1], m[2]); c[3] = sel(f, m[0], m[3]);                        \
-            r_rdense<RB, B>(a, c);                                                       \
-            ++ci;                                                                        \
-        }                                                                                \
+// Thread predicate of an op: every global-index bit of the mask is 1 for this thread.
+__device__ __forceinline__ bool pred_ok(uint64_t tb, uint64_t m) { return (tb & m) == m; }
+
+// pair-op bodies: flip-select the coefficients (X U X when the thread's roles
+// are swapped), then run the compile-time body
+template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
+__device__ __forceinline__ void op_rd(T2 (&a)[1 << RB], const Real* m, uint32_t F) {
+    const bool f = parity_c(W & F);
+    Real c[4];
+    c[0] = sel(f, m[3], m[0]); c[1] = sel(f, m[2], m[1]);
+    c[2] = sel(f, m[1], m[2]); c[3] = sel(f, m[0], m[3]);
+    p_rdense<RB, V, W>(a, c);
+}
+template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
+__device__ __forceinline__ void op_cd(T2 (&a)[1 << RB], const Real* m, uint32_t F) {
+    const bool f = parity_c(W & F);
+    Real c[8];
+    c[0] = sel(f, m[6], m[0]); c[1] = sel(f, m[7], m[1]);
+    c[2] = sel(f, m[4], m[2]); c[3] = sel(f, m[5], m[3]);
+    c[4] = sel(f, m[2], m[4]); c[5] = sel(f, m[3], m[5]);
+    c[6] = sel(f, m[0], m[6]); c[7] = sel(f, m[1], m[7]);
+    p_dense<RB, V, W>(a, c);
+}
+// x e on logical |1> = slots with parity(W & p) ^ f = 1; warp-uniform f takes the
+// half-multiply path (1 complex multiply per 2 amplitudes)
+template <int RB, uint32_t W, typename T2, typename Real>
+__device__ __forceinline__ void op_ph(T2 (&a)[1 << RB], T2 e, uint32_t F) {
+    const bool f = parity_c(W & F);
+    const uint32_t bal = __ballot_sync(0xffffffffu, f);
+    if (bal == 0u) {
+        p_phase<RB, W, 1>(a, e);
+    } else if (bal == 0xffffffffu) {
+        p_phase<RB, W, 0>(a, e);
+    } else {
+        T2 d0, d1;
+        d0.x = sel(f, e.x, Real(1)); d0.y = sel(f, e.y, Real(0));
+        d1.x = sel(f, Real(1), e.x); d1.y = sel(f, Real(0), e.y);
+        p_diag<RB, W>(a, d0, d1);
     }
-        QG_DENSE(0) QG_DENSE(1) QG_DENSE(2) QG_DENSE(3) QG_DENSE(4)
-#undef QG_DENSE
-    }
-    const uint32_t mk = R.cdiag;
-    if (mk) {
-#define QG_CDIAG(B)                                                                      \
-    if (B < RB && (mk & (1u << B))) {                                                    \
-        const Real* m = P.coef[ci];                                                      \
-        ++ci;                                                                            \
-        const bool f = (F >> B) & 1u;                                                    \
-        T2 d0, d1;                                                                       \
-        d0.x = sel(f, m[2], m[0]); d0.y = sel(f, m[3], m[1]);                            \
-        d1.x = sel(f, m[0], m[2]); d1.y = sel(f, m[1], m[3]);                            \
-        r_diag<RB, B>(a, d0, d1, false);                                                 \
-    }
-        QG_CDIAG(0) QG_CDIAG(1) QG_CDIAG(2) QG_CDIAG(3) QG_CDIAG(4)
-#undef QG_CDIAG
-    }
-    const uint32_t mg = R.diag;
-    if (mg) {
-        const uint32_t mh = R.dhi;
-#define QG_DIAG(B)                                                                       \
-    if (B < RB && (mg & (1u << B))) {                                                    \
-        T2 d0, d1;                                                                       \
-        d0.x = Real(1); d0.y = Real(0); d1 = d0;                                         \
-        const int ne = R.dcnt[B];                                                        \
-        for (int e = 0; e < ne; ++e, ++ei) {                                             \
-            const Entry<Real>& E = P.ent[ei];                                            \
-            if ((tb & E.cmask) != E.cmask) continue;                                     \
-            T2 v0, v1;                                                                   \
-            v0.x = E.v[0]; v0.y = E.v[1]; v1.x = E.v[2]; v1.y = E.v[3];                  \
-            d0 = cmul(d0, v0);                                                           \
-            d1 = cmul(d1, v1);                                                           \
-        }                                                                                \
-        const bool f = (F >> B) & 1u;                                                    \
-        if ((mh & (1u << B)) && !f) {                                                    \
-            r_diag<RB, B>(a, d0, d1, true);                                              \
-        } else {                                                                         \
-            T2 e0, e1;                                                                   \
-            e0.x = sel(f, d1.x, d0.x); e0.y = sel(f, d1.y, d0.y);                        \
-            e1.x = sel(f, d0.x, d1.x); e1.y = sel(f, d0.y, d1.y);                        \
-            r_diag<RB, B>(a, e0, e1, false);                                             \
-        }                                                                                \
-    }
-        QG_DIAG(0) QG_DIAG(1) QG_DIAG(2) QG_DIAG(3) QG_DIAG(4)
-#undef QG_DIAG
-    }
-    const uint32_t mx = R.xs;
-    if (mx) {
-#define QG_X(B)                                                                          \
-    if (B < RB && (mx & (1u << B))) {                                                    \
-        uint32_t odd = 0;                                                                \
-        const int ne = R.xcnt[B];                                                        \
-        for (int e = 0; e < ne; ++e, ++ei) {                                             \
-            const uint64_t cm = P.ent[ei].cmask;                                         \
-            odd ^= (tb & cm) == cm ? 1u : 0u;                                            \
-        }                                                                                \
-        F ^= odd << B;                                                                   \
-    }
-        QG_X(0) QG_X(1) QG_X(2) QG_X(3) QG_X(4)
-#undef QG_X
-    }
-    uint32_t mc = R.cx;
-    // iterate over the set CX slots in (t, c) order; one switch case per slot keeps
-    // every body a real branch (if-converted bodies would all be issued predicated)
-    while (mc) {
-        const int k = __ffs(mc) - 1;
-        mc &= mc - 1;
-        switch (k) {
-#define QG_CXK(T, C)                                                                     \
-    case 5 * T + C:                                                                      \
+}
+
+// materialising register CX (OC_CXM): kept out of run_op's jump table — a body
+// that permutes registers in the same loop as the others makes the register
+// allocator copy the whole amplitude array at the loop head of every op
+template <int RB, typename T2>
+__device__ __forceinline__ void run_cxm(T2 (&a)[1 << RB], uint32_t w, uint32_t& F) {
+    const uint32_t tc = (w >> 16) & 0xffu;
+    switch (tc) {
+#define QG_CXM(T, C)                                                                     \
+    case T | (C << 4):                                                                   \
         if constexpr (T < RB && C < RB && T != C) {                                      \
             r_cx<RB, T, C>(a);                                                           \
             F ^= ((F >> C) & 1u) << T;                                                   \
         }                                                                                \
         break;
-#define QG_CXT(T) QG_CXK(T, 0) QG_CXK(T, 1) QG_CXK(T, 2) QG_CXK(T, 3) QG_CXK(T, 4)
-            QG_CXT(0) QG_CXT(1) QG_CXT(2) QG_CXT(3) QG_CXT(4)
-#undef QG_CXT
-#undef QG_CXK
-            default: break;
+#define QG_CXMT(T) QG_CXM(T, 0) QG_CXM(T, 1) QG_CXM(T, 2) QG_CXM(T, 3) QG_CXM(T, 4)
+        QG_CXMT(0) QG_CXMT(1) QG_CXMT(2) QG_CXMT(3) QG_CXMT(4)
+#undef QG_CXMT
+#undef QG_CXM
+        default: break;
+    }
+}
+
+// One op word (desc.h).  F is the thread's flip vector: slot p holds logical
+// register index L^-1 (p ^ F).  Case labels are the dense codes of desc.h for
+// this RB; bodies that do not exist for this RB get unique unreachable labels.
+#define QG_LAB(ok, code, junk) ((ok) ? (code) : 1000 + (junk))
+template <int RB, typename T2, typename Real>
+__device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P, uint32_t w, uint64_t tb,
+                                       uint32_t& F) {
+    const Real* m = P.coef + (w >> 16);
+    switch (w & 0xffu) {
+#define QG_STD(T)                                                                        \
+    case QG_LAB(T < RB, oc_std(F_RD, RB, T), T):                                         \
+        if constexpr (T < RB) op_rd<RB, 1u << T, 1u << T>(a, m, F);                      \
+        break;                                                                           \
+    case QG_LAB(T < RB, oc_std(F_CD, RB, T), 8 + T):                                     \
+        if constexpr (T < RB) op_cd<RB, 1u << T, 1u << T>(a, m, F);                      \
+        break;                                                                           \
+    case QG_LAB(T < RB, oc_std(F_PH, RB, T), 16 + T):                                    \
+        if constexpr (T < RB) {                                                          \
+            T2 e;                                                                        \
+            e.x = m[0]; e.y = m[1];                                                      \
+            const uint32_t pi = (w >> 8) & 0xffu;                                        \
+            if (pi != kNoPred && !pred_ok(tb, P.pred[pi])) { e.x = Real(1); e.y = Real(0); } \
+            op_ph<RB, 1u << T, T2, Real>(a, e, F);                                       \
+        }                                                                                \
+        break;
+        QG_STD(0) QG_STD(1) QG_STD(2) QG_STD(3) QG_STD(4)
+#undef QG_STD
+#define QG_OKP(T, C) (T < RB && C < RB && T != C)
+#define QG_PAIR(T, C)                                                                    \
+    case QG_LAB(QG_OKP(T, C), oc_pair(F_RDW, RB, T, C), 100 + 5 * T + C):                \
+        if constexpr (QG_OKP(T, C)) op_rd<RB, 1u << T, (1u << T) | (1u << C)>(a, m, F);  \
+        break;                                                                           \
+    case QG_LAB(QG_OKP(T, C), oc_pair(F_RDV, RB, T, C), 200 + 5 * T + C):                \
+        if constexpr (QG_OKP(T, C)) op_rd<RB, (1u << T) | (1u << C), 1u << T>(a, m, F);  \
+        break;                                                                           \
+    case QG_LAB(QG_OKP(T, C), oc_pair(F_CDW, RB, T, C), 300 + 5 * T + C):                \
+        if constexpr (QG_OKP(T, C)) op_cd<RB, 1u << T, (1u << T) | (1u << C)>(a, m, F);  \
+        break;                                                                           \
+    case QG_LAB(QG_OKP(T, C), oc_pair(F_CDV, RB, T, C), 400 + 5 * T + C):                \
+        if constexpr (QG_OKP(T, C)) op_cd<RB, (1u << T) | (1u << C), 1u << T>(a, m, F);  \
+        break;                                                                           \
+    case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PHW, RB, T, C), 500 + 5 * T + C):        \
+        if constexpr (QG_OKP(T, C) && C < T) {                                           \
+            T2 e;                                                                        \
+            e.x = m[0]; e.y = m[1];                                                      \
+            const uint32_t pi = (w >> 8) & 0xffu;                                        \
+            if (pi != kNoPred && !pred_ok(tb, P.pred[pi])) { e.x = Real(1); e.y = Real(0); } \
+            op_ph<RB, (1u << T) | (1u << C), T2, Real>(a, e, F);                         \
+        }                                                                                \
+        break;                                                                           \
+    case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PH2, RB, T, C), 600 + 5 * T + C):        \
+        if constexpr (QG_OKP(T, C) && C < T) {                                           \
+            T2 e;                                                                        \
+            e.x = m[0]; e.y = m[1];                                                      \
+            const uint32_t ft = (F >> T) & 1u, fc = (F >> C) & 1u;                       \
+            if (__ballot_sync(0xffffffffu, ft | fc) == 0u) r_cphase<RB, T, C>(a, e);     \
+            else r_cphase_flip<RB, T, C>(a, e, ft, fc);                                  \
+        }                                                                                \
+        break;
+#define QG_PAIRT(T) QG_PAIR(T, 0) QG_PAIR(T, 1) QG_PAIR(T, 2) QG_PAIR(T, 3) QG_PAIR(T, 4)
+        QG_PAIRT(0) QG_PAIRT(1) QG_PAIRT(2) QG_PAIRT(3) QG_PAIRT(4)
+#undef QG_PAIRT
+#undef QG_PAIR
+#undef QG_OKP
+        case OC_XF: {
+            const uint32_t pi = (w >> 8) & 0xffu;
+            if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (w >> 16) & 31u;
+            break;
         }
+        default: __builtin_unreachable();
     }
-    const uint32_t mp = R.cp;
-    if (mp) {
-        // flipped bits move the phased quadrant: use the general 4-quadrant form then
-#define QG_CP(T, C)                                                                      \
-    if (T < RB && (mp & (1u << (T * (T - 1) / 2 + C)))) {                                \
-        T2 e;                                                                            \
-        e.x = P.coef[ci][0]; e.y = P.coef[ci][1]; ++ci;                                  \
-        if (((F >> T) | (F >> C)) & 1u) r_cphase_flip<RB, T, C>(a, e, (F >> T) & 1u, (F >> C) & 1u); \
-        else r_cphase<RB, T, C>(a, e);                                                   \
-    }
-        QG_CP(1, 0) QG_CP(2, 0) QG_CP(2, 1) QG_CP(3, 0) QG_CP(3, 1) QG_CP(3, 2)
-        QG_CP(4, 0) QG_CP(4, 1) QG_CP(4, 2) QG_CP(4, 3)
-#undef QG_CP
+}
+#undef QG_LAB
+
+// a stage's op list: runs of jump-table ops separated by runs of OC_CXM words
+template <int RB, typename T2, typename Real>
+__device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<Real>& P, int o, const int end,
+                                              uint64_t tb, uint32_t& F) {
+    while (o < end) {
+        for (; o < end; ++o) {
+            const uint32_t w = P.ops[o];
+            if ((w & 0xffu) == OC_CXM) break;
+            run_op<RB>(a, P, w, tb, F);
+        }
+        for (; o < end; ++o) {
+            const uint32_t w = P.ops[o];
+            if ((w & 0xffu) != OC_CXM) break;
+            run_cxm<RB>(a, w, F);
+        }
     }
 }
 
@@ -418,7 +444,10 @@ __host__ __device__ constexpr size_t tables_bytes() {
     return 4 * 256 * 8 + (kMaxStages + 1) * (kMapG * 8 + kMapS * 4);
 }
 
-template <typename Real, int RB, int WB>
+// NBUF = 2: transposes alternate two tile buffers (one barrier each);
+// NBUF = 1: one buffer, a second barrier before it is rewritten (half the SMEM,
+// so two CTAs fit on an SM)
+template <typename Real, int RB, int WB, int NBUF>
 __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 : 2)
     fused_pass_kernel(const __grid_constant__ PassDesc<Real> P, typename V2<Real>::T* __restrict__ psi,
                       uint64_t rank_bits) {
@@ -430,7 +459,7 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
     char* sm = reinterpret_cast<char*>(smem_raw);
     const int k = P.k;
     const uint32_t buf_bytes = (uint32_t)sizeof(T2) << k;
-    uint64_t* tbase = reinterpret_cast<uint64_t*>(smem_raw + 2 * (size_t)buf_bytes);
+    uint64_t* tbase = reinterpret_cast<uint64_t*>(smem_raw + NBUF * (size_t)buf_bytes);
     uint64_t* tmg = tbase + 4 * 256;
     uint32_t* tms = reinterpret_cast<uint32_t*>(tmg + (kMaxStages + 1) * kMapG);
     const int ns = P.n_stages;
@@ -488,21 +517,22 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
         for (int s = 1; s <= ns; ++s) {
             const StageDesc& S = P.stg[s];
             if (cur != s) {  // SMEM transpose into this stage's mapping
+                if (NBUF == 1) __syncthreads();  // every thread has read the previous transpose
                 smem_put<RB>(sm + buf, P.stg[cur], tso(cur), a, F);
                 __syncthreads();
                 smem_get<RB>(sm + buf, S, tso(s), a);
-                buf ^= buf_bytes;
+                if (NBUF == 2) buf ^= buf_bytes;
                 cur = s;
                 F = 0;
             }
             const uint64_t tb = base | rank_bits | tgb(s);
-            for (int r = S.round_begin; r < S.round_end; ++r) run_round<RB>(a, P, P.rounds[r], tb, F);
+            run_stage_ops<RB>(a, P, S.op_begin, S.op_end, tb, F);
             if (S.tph_end > S.tph_begin) {  // thread-level phases commute with the whole stage
                 T2 ph;
                 ph.x = Real(1);
                 ph.y = Real(0);
                 for (int e = S.tph_begin; e < S.tph_end; ++e) {
-                    const Entry<Real>& E = P.ent[e];
+                    const Entry<Real>& E = P.tph[e];
                     if ((tb & E.cmask) != E.cmask) continue;
                     const bool hi = (tb & E.qmask) != 0;
                     T2 v;
@@ -515,10 +545,11 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
             }
         }
         if (cur != si) {
+            if (NBUF == 1) __syncthreads();
             smem_put<RB>(sm + buf, P.stg[cur], tso(cur), a, F);
             __syncthreads();
             smem_get<RB>(sm + buf, P.stg[si], tso(si), a);
-            buf ^= buf_bytes;
+            if (NBUF == 2) buf ^= buf_bytes;
             F = 0;
         }
         {  // global store through the output mapping (deferred CX + flips folded in)
@@ -577,12 +608,12 @@ __global__ void gate_kernel(typename V2<Real>::T* __restrict__ psi, int n_local,
 }
 
 // ----------------------------------------------------------------- launchers
-template <typename Real, int RB, int WB>
+template <typename Real, int RB, int WB, int NBUF = 2>
 static cudaError_t launch_fused_t(const PassDesc<Real>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
     constexpr int threads = 32 << WB;
     const int k = RB + kLaneBits + WB;
-    const size_t smem = 2 * ((size_t)1 << k) * sizeof(typename V2<Real>::T) + tables_bytes();
-    auto kern = fused_pass_kernel<Real, RB, WB>;
+    const size_t smem = NBUF * ((size_t)1 << k) * sizeof(typename V2<Real>::T) + tables_bytes();
+    auto kern = fused_pass_kernel<Real, RB, WB, NBUF>;
     static int max_blocks = -1;  // per instantiation: resident CTAs per SM x SMs
     if (max_blocks < 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -607,6 +638,7 @@ cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uin
             case 0: return launch_fused_t<float, 4, 4>(P, psi, rank_bits, st);
             case 1: return launch_fused_t<float, 4, 3>(P, psi, rank_bits, st);
             case 2: return launch_fused_t<float, 4, 2>(P, psi, rank_bits, st);
+            case 4: return launch_fused_t<float, 5, 3, 1>(P, psi, rank_bits, st);
             default: return launch_fused_t<float, 3, 0>(P, psi, rank_bits, st);
         }
     }

@@ -121,22 +121,34 @@ static int validate(const int32_t* gt, const double* gp, int64_t n_gates, int n,
 
 // ------------------------------------------------------------------ kernel configs
 // must match launch_fused in fused.cu
-static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}};
+// auto choice = first entry with >= 8 qubits outside the tile; kernel_cfg (1 + id)
+// forces one (tuning)
+// (ids must match launch_fused in fused.cu; array index = id)
+static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}, {4, 5, 3}};
 static const KernelCfg kCfgC128[] = {{0, 4, 3}, {1, 3, 2}, {2, 3, 0}};
-static int n_cfgs(int dtype) { return dtype == QG_DTYPE_C64 ? 4 : 3; }
+// auto preference order (ids)
+static const int kAutoC64[] = {4, 1, 2, 3};
+static const int kAutoC128[] = {0, 1, 2};
 
-static bool pick_cfg(int dtype, int n_local, int force_k, KernelCfg& out) {
+static bool pick_cfg(int dtype, int n_local, int force_k, int force_cfg, KernelCfg& out) {
     const KernelCfg* cfgs = dtype == QG_DTYPE_C64 ? kCfgC64 : kCfgC128;
-    const int nc = n_cfgs(dtype);
+    const int n_all = dtype == QG_DTYPE_C64 ? 5 : 3;
+    const int* order = dtype == QG_DTYPE_C64 ? kAutoC64 : kAutoC128;
+    const int nc = dtype == QG_DTYPE_C64 ? 4 : 3;
+    if (force_cfg > 0) {
+        if (force_cfg > n_all || cfgs[force_cfg - 1].k() > n_local) return false;
+        out = cfgs[force_cfg - 1];
+        return true;
+    }
     if (force_k > 0) {
         for (int i = 0; i < nc; ++i)
-            if (cfgs[i].k() == force_k && force_k <= n_local) { out = cfgs[i]; return true; }
+            if (cfgs[order[i]].k() == force_k && force_k <= n_local) { out = cfgs[order[i]]; return true; }
         return false;
     }
     for (int i = 0; i < nc; ++i)
-        if (n_local - cfgs[i].k() >= 8) { out = cfgs[i]; return true; }
+        if (n_local - cfgs[order[i]].k() >= 8) { out = cfgs[order[i]]; return true; }
     for (int i = 0; i < nc; ++i)
-        if (cfgs[i].k() <= n_local) { out = cfgs[i]; return true; }
+        if (cfgs[order[i]].k() <= n_local) { out = cfgs[order[i]]; return true; }
     return false;
 }
 
@@ -313,56 +325,161 @@ static bool disjoint_low5(const std::vector<int>& bits) {
 }
 
 // ------------------------------------------------------------------ op emission
-// Converts the stage's gates (program order) to register-level ops: consecutive
-// 1-qubit gates on one register qubit are multiplied into one 2x2 in fp64 (real
-// when possible); diagonal actions become predicated entries.
+// Converts a stage's gates (program order, physical qubits) to slot-coordinate
+// ops (desc.h).  Register CX gates are never executed: they update the stage's
+// GF(2) map L (slot p holds logical register index i with p = L i ^ F) and the
+// kernel folds L into the transpose / store addresses at the stage end.  An op
+// on logical register bit b is emitted on slot bit T when L e_b = e_T and row b
+// of L^-1 is e_T (diagonal ops only need the latter); otherwise L is first
+// materialised by OC_CXM register moves (Gaussian elimination).
+// Consecutive 1-qubit gates on one register qubit are multiplied in fp64 into
+// at most [real 2x2][diag] factors (cheapest kernel ops: 2 + 1 FMA/amp) or one
+// complex 2x2; diagonal factors are split into diag(1, e) and a global phase
+// that the plan applies once (its last stage's thread-phase list).
+static bool m_diag(const M2& m) { return m.a01 == cd(0) && m.a10 == cd(0); }
+static bool m_real(const M2& m) {
+    return m.a00.imag() == 0 && m.a01.imag() == 0 && m.a10.imag() == 0 && m.a11.imag() == 0;
+}
+static bool m_ident(const M2& m) { return m.a00 == cd(1) && m.a11 == cd(1) && m.a01 == cd(0) && m.a10 == cd(0); }
+
 struct Emitter {
     HostStage& hs;
     const std::vector<int>& tile_q;
-    std::vector<int> reg_of;  // physical qubit -> register bit or -1
-    std::vector<M2> pend;
-    std::vector<char> has;
-    Emitter(HostStage& h, const std::vector<int>& tq, int n) : hs(h), tile_q(tq), reg_of(n, -1) {
+    const int rb;
+    cd& gphase;
+    std::vector<int> reg_of;  // physical qubit -> logical register bit or -1
+    uint32_t row[kMaxRegBits];  // L as rows over logical bits
+    std::vector<std::vector<M2>> pend;  // per logical bit: factors in application order
+    int n_cxm = 0;
+    Emitter(HostStage& h, const std::vector<int>& tq, int n, int rb_, cd& gp)
+        : hs(h), tile_q(tq), rb(rb_), gphase(gp), reg_of(n, -1), pend(h.reg_tile.size()) {
         for (size_t b = 0; b < hs.reg_tile.size(); ++b) reg_of[tile_q[hs.reg_tile[b]]] = (int)b;
-        pend.resize(hs.reg_tile.size());
-        has.assign(hs.reg_tile.size(), 0);
+        for (int r = 0; r < kMaxRegBits; ++r) row[r] = 1u << r;
     }
-    static bool diagonal(const M2& m) { return m.a01 == cd(0) && m.a10 == cd(0); }
-    HostOp mk(int kind, int t, int c, uint64_t cmask, uint64_t qmask) {
-        HostOp o{};
-        o.kind = kind; o.t = t; o.c = c;
-        o.tq = t >= 0 ? tile_q[hs.reg_tile[t]] : -1;
-        o.cq = c >= 0 ? tile_q[hs.reg_tile[c]] : -1;
-        o.cmask = cmask; o.qmask = qmask;
-        return o;
-    }
-    void flush(int b) {
-        if (!has[b]) return;
-        has[b] = 0;
-        const M2& m = pend[b];
-        if (diagonal(m)) {
-            if (m.a00 == cd(1) && m.a11 == cd(1)) return;
-            HostOp o = mk(A_CDIAG, b, -1, 0, 0);
-            o.m[0] = m.a00.real(); o.m[1] = m.a00.imag(); o.m[2] = m.a11.real(); o.m[3] = m.a11.imag();
-            hs.ops.push_back(o);
-            return;
+    int qphys(int b) const { return tile_q[hs.reg_tile[b]]; }
+    // rows of L^-1
+    void inverse(uint32_t* inv) const {
+        uint32_t a[kMaxRegBits];
+        for (int r = 0; r < rb; ++r) { a[r] = row[r]; inv[r] = 1u << r; }
+        for (int j = 0; j < rb; ++j) {
+            int p = j;
+            while (!((a[p] >> j) & 1u)) ++p;
+            std::swap(a[p], a[j]); std::swap(inv[p], inv[j]);
+            for (int r = 0; r < rb; ++r)
+                if (r != j && ((a[r] >> j) & 1u)) { a[r] ^= a[j]; inv[r] ^= inv[j]; }
         }
-        const bool real = m.a00.imag() == 0 && m.a01.imag() == 0 && m.a10.imag() == 0 && m.a11.imag() == 0;
-        HostOp o = mk(real ? A_RDENSE : A_DENSE, b, -1, 0, 0);
-        if (real) { o.m[0] = m.a00.real(); o.m[1] = m.a01.real(); o.m[2] = m.a10.real(); o.m[3] = m.a11.real(); }
-        else put(o.m, m);
+    }
+    uint32_t col(int b) const {  // L e_b as a slot-bit vector
+        uint32_t v = 0;
+        for (int r = 0; r < rb; ++r) if ((row[r] >> b) & 1u) v |= 1u << r;
+        return v;
+    }
+    void push(int kind, int t, int c, uint64_t cmask = 0) {
+        HostOp o{};
+        o.kind = kind; o.t = t; o.c = c; o.cmask = cmask;
+        o.tq = (kind != A_XF && t >= 0) ? qphys(t) : -1;
+        o.cq = c >= 0 ? qphys(c) : -1;
         hs.ops.push_back(o);
     }
-    // an op acting diagonally on b: a pending diagonal commutes with it, a dense one must go first
-    void flush_nondiag(int b) {
-        if (has[b] && !diagonal(pend[b])) flush(b);
+    void materialise() {  // emit CXM row operations reducing L to the identity
+        for (int j = 0; j < rb; ++j) {
+            if (!((row[j] >> j) & 1u)) {
+                int i = j + 1;
+                while (!((row[i] >> j) & 1u)) ++i;
+                row[j] ^= row[i];
+                push(A_CXM, j, i);
+                ++n_cxm;
+            }
+            for (int i = 0; i < rb; ++i)
+                if (i != j && ((row[i] >> j) & 1u)) {
+                    row[i] ^= row[j];
+                    push(A_CXM, i, j);
+                    ++n_cxm;
+                }
+        }
     }
-    void fold(int b, const M2& m) {
-        pend[b] = has[b] ? mul(m, pend[b]) : m;
-        has[b] = 1;
+    static int unit(uint32_t v) { return (v && !(v & (v - 1))) ? __builtin_ctz(v) : -1; }
+    static bool two(uint32_t v) { return v && unit(v) < 0 && unit(v & (v - 1)) >= 0; }
+    int slot_w(int b) {  // slot bit whose value is logical bit b (materialising if needed)
+        uint32_t inv[kMaxRegBits] = {};
+        inverse(inv);
+        int t = unit(inv[b]);
+        if (t < 0) { materialise(); t = b; }
+        return t;
+    }
+    // phase e on logical |1> of b: role vector W = row b of L^-1 (one or two slot bits)
+    void emit_phase(int b, cd e, uint64_t cmask) {
+        if (e == cd(1)) return;
+        uint32_t inv[kMaxRegBits] = {};
+        inverse(inv);
+        uint32_t w = inv[b];
+        if (unit(w) < 0 && !two(w)) { materialise(); w = 1u << b; }
+        if (unit(w) >= 0) push(A_PH, unit(w), -1, cmask);
+        else push(A_PH, 31 - __builtin_clz(w), __builtin_ctz(w), cmask);  // W form, T > C
+        hs.ops.back().m[0] = e.real(); hs.ops.back().m[1] = e.imag();
+    }
+    void emit_diag(int b, const M2& m) {  // diag(d0, d1) = d0 * diag(1, d1 / d0)
+        if (m.a00 != cd(1)) gphase *= m.a00;
+        emit_phase(b, m.a11 / m.a00, 0);
+    }
+    // 2x2 on logical b: pairs along V = L e_b, roles by W = row b of L^-1; the kernel
+    // has bodies for V = W = e_T, (V = e_T, W = e_T + e_C) and (V = e_T + e_C, W = e_T)
+    void emit_dense(int b, const M2& m) {
+        uint32_t inv[kMaxRegBits] = {};
+        inverse(inv);
+        uint32_t v = col(b), w = inv[b];
+        int t = -1, c = -1;
+        if (unit(v) >= 0 && v == w) {
+            t = unit(v);
+        } else if (unit(v) >= 0 && two(w) && (w & v)) {
+            t = unit(v); c = unit(w & ~v);
+        } else if (unit(w) >= 0 && two(v) && (w & v)) {
+            t = unit(w); c = unit(v & ~w);
+        } else {
+            materialise();
+            t = b; v = w = 1u << b;
+        }
+        push(m_real(m) ? A_RD : A_CD, t, c);
+        HostOp& o = hs.ops.back();
+        o.form = c < 0 ? 0 : (v == (1u << t) ? 1 : 2);
+        if (m_real(m)) {
+            double* d = o.m;
+            d[0] = m.a00.real(); d[1] = m.a01.real(); d[2] = m.a10.real(); d[3] = m.a11.real();
+        } else {
+            put(o.m, m);
+        }
+    }
+    void flush(int b) {
+        std::vector<M2>& f = pend[b];
+        if (f.empty()) return;
+        auto cls = [](const M2& m) { return m_diag(m) ? 0 : (m_real(m) ? 1 : 2); };
+        std::vector<M2> runs;  // runs of one class, merged (application order)
+        for (const M2& m : f) {
+            if (!runs.empty() && cls(runs.back()) == cls(m)) runs.back() = mul(m, runs.back());
+            else runs.push_back(m);
+        }
+        f.clear();
+        bool one = runs.size() > 2;
+        for (const M2& m : runs) if (cls(m) == 2) one = true;
+        if (one) {
+            M2 u = runs[0];
+            for (size_t i = 1; i < runs.size(); ++i) u = mul(runs[i], u);
+            runs.assign(1, u);
+        }
+        for (const M2& m : runs) {
+            if (m_ident(m)) continue;
+            if (m_diag(m)) emit_diag(b, m);
+            else emit_dense(b, m);
+        }
+    }
+    void flush_nondiag(int b) {
+        for (const M2& m : pend[b])
+            if (!m_diag(m)) { flush(b); return; }
     }
     void tph(uint64_t cmask, uint64_t qmask, cd v0, cd v1) {
-        HostOp o = mk(A_TPH, -1, -1, cmask, qmask);
+        HostOp o{};
+        o.kind = A_TPH; o.t = o.c = o.tq = o.cq = -1;
+        o.cmask = cmask; o.qmask = qmask;
         o.m[0] = v0.real(); o.m[1] = v0.imag(); o.m[2] = v1.real(); o.m[3] = v1.imag();
         hs.tph.push_back(o);
     }
@@ -370,11 +487,11 @@ struct Emitter {
         const int rt = reg_of[g.t];
         switch (g.kind) {
             case K_H: case K_RX: case K_RY:
-                fold(rt, gate_matrix(g.kind, g.p));
+                pend[rt].push_back(gate_matrix(g.kind, g.p));
                 break;
             case K_RZ: {
                 const M2 m = gate_matrix(K_RZ, g.p);
-                if (rt >= 0) fold(rt, m);
+                if (rt >= 0) pend[rt].push_back(m);
                 else tph(0, 1ull << g.t, m.a00, m.a11);
                 break;
             }
@@ -383,11 +500,13 @@ struct Emitter {
                 const int rc = reg_of[g.c];
                 if (rc >= 0) {
                     flush_nondiag(rc);
-                    hs.ops.push_back(mk(A_CX, rt, rc, 0, 0));
+                    for (int r = 0; r < rb; ++r)  // L <- L * CX(c -> t)
+                        if ((row[r] >> rt) & 1u) row[r] ^= 1u << rc;
                 } else {
-                    HostOp o = mk(A_X, rt, -1, 1ull << g.c, 0);
-                    o.cq = g.c;
-                    hs.ops.push_back(o);
+                    const uint32_t v = col(rt);
+                    push(A_XF, (int)v, -1, 1ull << g.c);
+                    hs.ops.back().tq = g.t;
+                    hs.ops.back().cq = g.c;
                 }
                 break;
             }
@@ -397,17 +516,17 @@ struct Emitter {
                 if (rt >= 0 && rc >= 0) {
                     flush_nondiag(rt);
                     flush_nondiag(rc);
-                    HostOp o = mk(A_CP, std::max(rt, rc), std::min(rt, rc), 0, 0);
-                    o.m[0] = e.real(); o.m[1] = e.imag();
-                    hs.ops.push_back(o);
+                    uint32_t inv[kMaxRegBits] = {};
+                    inverse(inv);
+                    if (unit(inv[rt]) < 0 || unit(inv[rc]) < 0) materialise();
+                    const int a = slot_w(rt), b = slot_w(rc);  // both unit now
+                    push(A_PH2, std::max(a, b), std::min(a, b));
+                    hs.ops.back().m[0] = e.real(); hs.ops.back().m[1] = e.imag();
                 } else if (rt >= 0 || rc >= 0) {
                     const int b = rt >= 0 ? rt : rc;
                     const int other = rt >= 0 ? g.c : g.t;
                     flush_nondiag(b);
-                    HostOp o = mk(A_DIAG, b, -1, 1ull << other, 0);
-                    o.cq = other;
-                    o.m[0] = 1.0; o.m[1] = 0.0; o.m[2] = e.real(); o.m[3] = e.imag();
-                    hs.ops.push_back(o);
+                    emit_phase(b, e, 1ull << other);
                 } else {
                     tph((1ull << g.t) | (1ull << g.c), 0, e, e);
                 }
@@ -417,106 +536,15 @@ struct Emitter {
         }
     }
     void finish() {
-        for (size_t b = 0; b < has.size(); ++b) flush((int)b);
+        for (size_t b = 0; b < pend.size(); ++b) flush((int)b);
+        uint32_t inv[kMaxRegBits] = {};
+        inverse(inv);
+        hs.out_vec.assign(rb, 0);
+        for (int j = 0; j < rb; ++j)  // column j of L^-1
+            for (int b = 0; b < rb; ++b)
+                if ((inv[b] >> j) & 1u) hs.out_vec[j] |= 1u << b;
     }
 };
-
-// ------------------------------------------------------------------ round packing
-// Slot execution order inside a round (must match fused.cu): dense(b) < cdiag(b) <
-// diag(b) < X(b) < CX(t,c) < CPHASE(t>c); within a group by bit / pair index.
-static int slot_key(const HostOp& o) {
-    switch (o.kind) {
-        case A_DENSE: case A_RDENSE: return 0 * 64 + o.t;
-        case A_CDIAG: return 1 * 64 + o.t;
-        case A_DIAG: return 2 * 64 + o.t;
-        case A_X: return 3 * 64 + o.t;
-        case A_CX: return 4 * 64 + 5 * o.t + o.c;
-        default: return 5 * 64 + o.t * (o.t - 1) / 2 + o.c;  // A_CP, t > c
-    }
-}
-
-// does op act non-diagonally on register bit b? (-1 = does not touch b)
-static int acts(const HostOp& o, int b) {
-    switch (o.kind) {
-        case A_DENSE: case A_RDENSE: case A_X: return o.t == b ? 1 : -1;
-        case A_DIAG: case A_CDIAG: return o.t == b ? 0 : -1;
-        case A_CX: return o.t == b ? 1 : (o.c == b ? 0 : -1);
-        case A_CP: return (o.t == b || o.c == b) ? 0 : -1;
-        default: return -1;
-    }
-}
-
-static bool commute(const HostOp& x, const HostOp& y, int rb) {
-    for (int b = 0; b < rb; ++b) {
-        const int ax = acts(x, b), ay = acts(y, b);
-        if (ax >= 0 && ay >= 0 && (ax == 1 || ay == 1)) return false;
-    }
-    return true;
-}
-
-// Register CX gates that commute with every later op of the stage are moved past
-// its end: their index map M (GF(2)-linear on register bits) is folded into the
-// stage's output addressing (out_vec[b] = M^-1 e_b), so they cost nothing.
-static void defer_trailing_cx(HostStage& hs, int rb) {
-    std::vector<HostOp> kept, deferred_rev;
-    for (int p = (int)hs.ops.size() - 1; p >= 0; --p) {
-        const HostOp& x = hs.ops[p];
-        bool ok = x.kind == A_CX;
-        if (ok)
-            for (const HostOp& y : kept)
-                if (!commute(x, y, rb)) { ok = false; break; }
-        if (ok) deferred_rev.push_back(x);
-        else kept.push_back(x);
-    }
-    std::reverse(kept.begin(), kept.end());
-    hs.ops.swap(kept);
-    hs.deferred.assign(deferred_rev.rbegin(), deferred_rev.rend());  // program order
-    hs.out_vec.assign(rb, 0);
-    for (int b = 0; b < rb; ++b) {
-        uint32_t v = 1u << b;
-        for (const HostOp& c : hs.deferred)  // M^-1 = C_k ... C_1 : apply C_1 first
-            if (v & (1u << c.c)) v ^= 1u << c.t;
-        hs.out_vec[b] = v;
-    }
-}
-
-static void pack_rounds(HostStage& hs, int rb) {
-    struct Placed { const HostOp* op; int round; int key; };
-    std::vector<Placed> placed;
-    // slot occupancy per round: key -> index in round op list (list slots may repeat)
-    std::vector<std::vector<int>> used;  // used[r] = keys occupied by single-op slots
-    std::vector<std::vector<HostOp>> rops;
-    for (const HostOp& x : hs.ops) {
-        const int kx = slot_key(x);
-        int lo = 0;
-        for (const Placed& p : placed)
-            if (!commute(x, *p.op, rb)) lo = std::max(lo, kx > p.key ? p.round : p.round + 1);
-        const bool list_slot = x.kind == A_DIAG || x.kind == A_X;
-        int r = lo;
-        for (;; ++r) {
-            if (r == (int)rops.size()) { rops.emplace_back(); used.emplace_back(); }
-            if (list_slot) {
-                // diag / X slot on bit t: a list; only the slot *type* must match
-                bool clash = false;
-                for (int k : used[r]) if (k == kx) clash = true;  // a single-op slot with this key? (never)
-                if (!clash) break;
-            } else {
-                bool clash = false;
-                for (int k : used[r]) if (k == kx) clash = true;
-                if (!clash) break;
-            }
-        }
-        if (!list_slot) used[r].push_back(kx);
-        rops[r].push_back(x);
-        placed.push_back(Placed{&x, r, kx});
-    }
-    hs.rounds.clear();
-    for (auto& ops : rops) {
-        std::stable_sort(ops.begin(), ops.end(),
-                         [](const HostOp& a, const HostOp& b) { return slot_key(a) < slot_key(b); });
-        hs.rounds.push_back(HostRound{ops});
-    }
-}
 
 static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const std::vector<int>& tile,
                                 const std::vector<StageSched>& stages) {
@@ -528,19 +556,21 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
     for (size_t i = 0; i < tile.size(); ++i) tbit[tile[i]] = (int)i;
     const int S = (int)stages.size();
     hp.stages.resize(S);
+    cd gphase(1, 0);
     for (int s = 0; s < S; ++s) {
         std::vector<int> need;
         for (int q : stages[s].regs) need.push_back(tbit[q]);
         const bool compat = disjoint_low5(need);
         const bool io = compat && (s == 0 || s == S - 1);
         assign_mapping(dtype, cfg, need, io, hp.stages[s]);
-        Emitter em(hp.stages[s], hp.tile_q, n);
+        Emitter em(hp.stages[s], hp.tile_q, n, cfg.rb, gphase);
         for (const Gate& g : stages[s].gates) em.gate(g);
         em.finish();
-        defer_trailing_cx(hp.stages[s], cfg.rb);
-        pack_rounds(hp.stages[s], cfg.rb);
+        hp.n_cxm += em.n_cxm;
         hp.n_gates += (int)stages[s].gates.size();
     }
+    hp.gph_re = gphase.real();
+    hp.gph_im = gphase.imag();
     auto is_io = [](const HostStage& h) {
         for (int l = 0; l < kLaneBits; ++l) if (h.lane_tile[l] != l) return false;
         return true;
@@ -626,31 +656,62 @@ static void put_entry(Entry<Real>& e, const HostOp& o) {
     for (int i = 0; i < 4; ++i) e.v[i] = (Real)o.m[i];
 }
 
+static int n_coef(const HostOp& o) {
+    switch (o.kind) {
+        case A_RD: return 4;
+        case A_CD: return 8;
+        case A_PH: case A_PH2: return 2;
+        default: return 0;
+    }
+}
+
 // resource needs of a pass (descriptor capacity is checked by the scheduler)
-struct PassSize { int rounds = 0, coef = 0, ent = 0; };
+struct PassSize { int ops = 0, coef = 0, tph = 0, pred = 0; };
 static PassSize pass_size(const HostPass& hp) {
     PassSize z;
+    std::vector<uint64_t> preds;
     for (const HostStage& h : hp.stages) {
-        z.rounds += (int)h.rounds.size();
-        z.ent += (int)h.tph.size();
-        for (const HostRound& r : h.rounds)
-            for (const HostOp& o : r.ops) {
-                if (o.kind == A_DENSE || o.kind == A_RDENSE || o.kind == A_CP || o.kind == A_CDIAG) ++z.coef;
-                if (o.kind == A_DIAG || o.kind == A_X) ++z.ent;
-            }
+        z.ops += (int)h.ops.size();
+        z.tph += (int)h.tph.size();
+        for (const HostOp& o : h.ops) {
+            z.coef += n_coef(o);
+            if ((o.kind == A_PH || o.kind == A_XF) && o.cmask &&
+                std::find(preds.begin(), preds.end(), o.cmask) == preds.end())
+                preds.push_back(o.cmask);
+        }
     }
+    z.pred = (int)preds.size();
     return z;
 }
 
-static bool fits(const HostPass& hp) {
+template <typename Real>
+static bool fits_t(const HostPass& hp) {
     const PassSize z = pass_size(hp);
-    return z.rounds <= kMaxRounds && z.coef <= kMaxCoef && z.ent <= kMaxEnt;
+    // one thread-phase slot is kept free for the plan's global phase
+    return z.ops <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph && z.pred <= kMaxPred;
+}
+static bool fits(int dtype, const HostPass& hp) {
+    return dtype == QG_DTYPE_C64 ? fits_t<float>(hp) : fits_t<double>(hp);
+}
+
+static uint32_t op_code(const HostOp& o, int rb) {
+    switch (o.kind) {
+        case A_RD:
+            return o.form == 0 ? oc_std(F_RD, rb, o.t) : oc_pair(o.form == 1 ? F_RDW : F_RDV, rb, o.t, o.c);
+        case A_CD:
+            return o.form == 0 ? oc_std(F_CD, rb, o.t) : oc_pair(o.form == 1 ? F_CDW : F_CDV, rb, o.t, o.c);
+        case A_PH: return o.c < 0 ? oc_std(F_PH, rb, o.t) : oc_tri(F_PHW, rb, o.t, o.c);
+        case A_PH2: return oc_tri(F_PH2, rb, o.t, o.c);
+        case A_CXM: return OC_CXM;
+        default: return OC_XF;
+    }
 }
 
 template <typename Real>
-static bool build_desc(int dtype, const HostPass& hp, int n_local, PassDesc<Real>& d, std::string& err) {
+static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::string& err) {
     std::memset(&d, 0, sizeof(d));
-    if (!fits(hp)) { err = "pass exceeds descriptor capacity"; return false; }
+    if (!fits_t<Real>(hp)) { err = "pass exceeds descriptor capacity"; return false; }
+    const int dtype = sizeof(Real) == 4 ? QG_DTYPE_C64 : QG_DTYPE_C128;
     d.n_stages = (int)hp.stages.size();
     d.k = hp.cfg.k();
     d.load_direct = hp.load_direct;
@@ -663,64 +724,48 @@ static bool build_desc(int dtype, const HostPass& hp, int n_local, PassDesc<Real
             if (std::find(hp.tile_q.begin(), hp.tile_q.end(), q) == hp.tile_q.end()) d.comp_q[nc0++] = (uint8_t)q;
     }
     fill_stage(dtype, hp, hp.io, d.stg[0]);
-    int nr = 0, nc = 0, ne = 0;
+    int no = 0, nc = 0, nt = 0, np = 0;
+    auto pred_index = [&](uint64_t m) -> uint32_t {
+        if (!m) return kNoPred;
+        for (int i = 0; i < np; ++i) if (d.pred[i] == m) return (uint32_t)i;
+        d.pred[np] = m;
+        return (uint32_t)np++;
+    };
     for (int s = 0; s < d.n_stages; ++s) {
         const HostStage& h = hp.stages[s];
         StageDesc& sd = d.stg[1 + s];
         fill_stage(dtype, hp, h, sd);
-        sd.tph_begin = (uint16_t)ne;
-        for (const HostOp& o : h.tph) put_entry(d.ent[ne++], o);
-        sd.tph_end = (uint16_t)ne;
-        sd.round_begin = (uint16_t)nr;
-        for (const HostRound& hr : h.rounds) {
-            RoundDesc& R = d.rounds[nr++];
-            R.coef = (uint16_t)nc;
-            R.ent = (uint16_t)ne;
-            // slot order: ops are sorted by slot key, so appending in order matches the kernel
-            for (const HostOp& o : hr.ops) {
-                switch (o.kind) {
-                    case A_DENSE:
-                        R.dense |= (uint8_t)(1u << o.t);
-                        for (int i = 0; i < 8; ++i) d.coef[nc][i] = (Real)o.m[i];
-                        ++nc;
-                        break;
-                    case A_RDENSE:
-                        R.rdense |= (uint8_t)(1u << o.t);
-                        for (int i = 0; i < 4; ++i) d.coef[nc][i] = (Real)o.m[i];
-                        ++nc;
-                        break;
-                    case A_CDIAG:
-                        R.cdiag |= (uint8_t)(1u << o.t);
-                        for (int i = 0; i < 4; ++i) d.coef[nc][i] = (Real)o.m[i];
-                        ++nc;
-                        break;
-                    case A_DIAG:
-                        if (!(R.diag & (1u << o.t))) R.dhi |= (uint8_t)(1u << o.t);
-                        if (!(o.m[0] == 1.0 && o.m[1] == 0.0)) R.dhi &= (uint8_t)~(1u << o.t);
-                        R.diag |= (uint8_t)(1u << o.t);
-                        R.dcnt[o.t]++;
-                        put_entry(d.ent[ne++], o);
-                        break;
-                    case A_X:
-                        R.xs |= (uint8_t)(1u << o.t);
-                        R.xcnt[o.t]++;
-                        put_entry(d.ent[ne++], o);
-                        break;
-                    case A_CX:
-                        R.cx |= 1u << (5 * o.t + o.c);
-                        break;
-                    case A_CP:
-                        R.cp |= (uint16_t)(1u << (o.t * (o.t - 1) / 2 + o.c));
-                        d.coef[nc][0] = (Real)o.m[0];
-                        d.coef[nc][1] = (Real)o.m[1];
-                        ++nc;
-                        break;
-                }
+        sd.op_begin = (uint16_t)no;
+        for (const HostOp& o : h.ops) {
+            uint32_t w;
+            if (o.kind == A_XF) {
+                w = op_word(OC_XF, pred_index(o.cmask), (uint32_t)o.t);
+            } else if (o.kind == A_CXM) {
+                w = op_word(OC_CXM, kNoPred, (uint32_t)(o.t | (o.c << 4)));
+            } else {
+                w = op_word(op_code(o, hp.cfg.rb), o.kind == A_PH ? pred_index(o.cmask) : kNoPred, (uint32_t)nc);
+                for (int i = 0; i < n_coef(o); ++i) d.coef[nc++] = (Real)o.m[i];
             }
+            d.ops[no++] = w;
         }
-        sd.round_end = (uint16_t)nr;
+        sd.op_end = (uint16_t)no;
+        sd.tph_begin = (uint16_t)nt;
+        for (const HostOp& o : h.tph) put_entry(d.tph[nt++], o);
+        sd.tph_end = (uint16_t)nt;
     }
     return true;
+}
+
+// appends the plan's accumulated global phase to the last stage of a built descriptor
+template <typename Real>
+static void add_global_phase(PassDesc<Real>& d, cd g) {
+    StageDesc& sd = d.stg[d.n_stages];
+    Entry<Real>& e = d.tph[sd.tph_end];
+    e.cmask = 0;
+    e.qmask = 0;
+    e.v[0] = e.v[2] = (Real)g.real();
+    e.v[1] = e.v[3] = (Real)g.imag();
+    sd.tph_end = (uint16_t)(sd.tph_end + 1);
 }
 
 // ------------------------------------------------------------------ driver
@@ -745,8 +790,8 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
     const int n = n_qubits, n_local = plan.n_local;
 
     KernelCfg cfg{};
-    bool fused = opts.fuse != 0 && pick_cfg(opts.dtype, n_local, opts.tile_qubits, cfg);
-    if (opts.fuse != 0 && opts.tile_qubits > 0 && !fused) {
+    bool fused = opts.fuse != 0 && pick_cfg(opts.dtype, n_local, opts.tile_qubits, opts.kernel_cfg, cfg);
+    if (opts.fuse != 0 && (opts.tile_qubits > 0 || opts.kernel_cfg > 0) && !fused) {
         err = "tile_qubits not available for this dtype / size";
         return QG_E_INVALID_ARG;
     }
@@ -774,7 +819,7 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
             if (fused) {
                 std::vector<int> tile;
                 std::vector<StageSched> stages;
-                int max_gates = kMaxEnt;  // shrunk below if the descriptor overflows
+                int max_gates = kMaxOps;  // shrunk below if the descriptor overflows
                 HostPass hp;
                 for (;;) {
                     std::vector<Gate> trial(rem);
@@ -782,7 +827,7 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
                                   tile, stages);
                     if (stages.empty()) break;
                     hp = make_fused_pass(opts.dtype, cfg, n, tile, stages);
-                    if (fits(hp) || max_gates <= 1) { rem.swap(trial); break; }
+                    if (fits(opts.dtype, hp) || max_gates <= 1) { rem.swap(trial); break; }
                     max_gates = std::max(1, hp.n_gates * 3 / 4);
                 }
                 if (stages.empty()) break;
@@ -827,31 +872,39 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
     plan.final_phys = phys;
 
     // device descriptors
+    cd gphase(1, 0);
+    int64_t last_desc = -1;
     plan.desc_index.resize(plan.segs.size());
     for (size_t s = 0; s < plan.segs.size(); ++s) {
         for (const HostPass& hp : plan.segs[s]) {
             int64_t idx = -1;
             if (hp.fused) {
+                gphase *= cd(hp.gph_re, hp.gph_im);
                 if (plan.dtype == QG_DTYPE_C64) {
                     plan.d32.emplace_back();
-                    if (!build_desc<float>(plan.dtype, hp, n_local, plan.d32.back(), err)) return QG_E_INVALID_ARG;
+                    if (!build_desc<float>(hp, n_local, plan.d32.back(), err)) return QG_E_INVALID_ARG;
                     idx = (int64_t)plan.d32.size() - 1;
                 } else {
                     plan.d64.emplace_back();
-                    if (!build_desc<double>(plan.dtype, hp, n_local, plan.d64.back(), err)) return QG_E_INVALID_ARG;
+                    if (!build_desc<double>(hp, n_local, plan.d64.back(), err)) return QG_E_INVALID_ARG;
                     idx = (int64_t)plan.d64.size() - 1;
                 }
+                last_desc = idx;
                 plan.stats.n_stages += (int64_t)hp.stages.size();
-                for (const HostStage& h : hp.stages) {
-                    plan.stats.n_ops += (int64_t)(h.ops.size() + h.tph.size());
-                    plan.stats.n_rounds += (int64_t)h.rounds.size();
-                }
+                plan.stats.n_cxm += hp.n_cxm;
+                for (const HostStage& h : hp.stages) plan.stats.n_ops += (int64_t)(h.ops.size() + h.tph.size());
             } else {
                 plan.stats.n_ops += 1;
             }
             plan.desc_index[s].push_back(idx);
         }
     }
+    if (last_desc >= 0 && gphase != cd(1, 0)) {
+        if (plan.dtype == QG_DTYPE_C64) add_global_phase(plan.d32[last_desc], gphase);
+        else add_global_phase(plan.d64[last_desc], gphase);
+    }
+    plan.gphase_re = gphase.real();
+    plan.gphase_im = gphase.imag();
     return QG_OK;
 }
 

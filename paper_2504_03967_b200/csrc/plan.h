@@ -31,29 +31,23 @@ struct KernelCfg {
     int k() const { return rb + kLaneBits + wb; }
 };
 
-// abstract register-level op (planner output before round packing)
-enum AbsKind { A_DENSE = 0, A_RDENSE = 1, A_DIAG = 2, A_X = 3, A_CX = 4, A_CP = 5, A_TPH = 6, A_CDIAG = 7 };
+// register-level op in slot coordinates (desc.h OpCode), planner output
+enum AbsKind { A_RD = 0, A_CD = 1, A_PH = 2, A_CXM = 3, A_PH2 = 4, A_XF = 5, A_TPH = 6 };
 
 struct HostOp {
     int kind;       // AbsKind
-    int t, c;       // register bits (-1 unused)
+    int t, c;       // slot bits (-1 unused); A_XF: t = flip vector
+    int form;       // A_RD / A_CD: 0 V = W = e_t; 1 V = e_t, W = e_t + e_c; 2 V = e_t + e_c, W = e_t
     int tq, cq;     // physical qubits (export / debugging)
-    uint64_t cmask, qmask;
-    double m[8];    // dense: 2x2 complex; rdense: m[0..3] real a00 a01 a10 a11;
-                    // diag / tph: v0 = (m0,m1), v1 = (m2,m3); cp: (m0, m1)
-};
-
-struct HostRound {
-    std::vector<HostOp> ops;  // in kernel slot-execution order
+    uint64_t cmask, qmask;  // thread predicate (all bits 1) / thread-phase select bit
+    double m[8];    // A_RD: m00 m01 m10 m11; A_CD: 2x2 complex; A_PH/A_PH2: e; A_TPH: v0, v1
 };
 
 struct HostStage {
     std::vector<int> reg_tile, lane_tile, warp_tile;  // tile-bit index per register / lane / warp bit
-    std::vector<HostOp> ops;       // program order (emitter output), excluding thread phases
+    std::vector<HostOp> ops;       // kernel order (slot coordinates), excluding thread phases
     std::vector<HostOp> tph;       // thread-phase entries
-    std::vector<HostRound> rounds; // packed
-    std::vector<HostOp> deferred;  // register CX gates moved past the stage end (absorbed in out map)
-    std::vector<uint32_t> out_vec; // per register bit: register-bit vector of its output tile index
+    std::vector<uint32_t> out_vec; // per slot bit j: logical register-bit vector L^-1 e_j
 };
 
 struct HostPass {
@@ -65,10 +59,12 @@ struct HostPass {
     bool load_direct = true, store_direct = true;
     GateOp gop{};                     // unfused single gate
     int n_gates = 0;                  // circuit gates covered by this pass
+    int n_cxm = 0;                    // materialised register CX ops
+    double gph_re = 1.0, gph_im = 0.0; // global phase factored out of this pass's diagonal ops
 };
 
 struct PlanStats {
-    int64_t n_ops = 0, n_stages = 0, n_rounds = 0;
+    int64_t n_ops = 0, n_stages = 0, n_cxm = 0;
 };
 
 }  // namespace qg
@@ -81,6 +77,7 @@ struct qg_plan {
     std::vector<qg_remap> remaps;
     std::vector<int> final_phys;  // logical qubit -> physical position at the end
     qg::PlanStats stats;
+    double gphase_re = 1.0, gphase_im = 0.0;  // global phase applied in the last fused pass
     // device descriptors, built once at plan time (index = running fused-pass id)
     std::vector<qg::PassDesc<float>> d32;
     std::vector<qg::PassDesc<double>> d64;
