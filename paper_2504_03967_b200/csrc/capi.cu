@@ -168,9 +168,13 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
                             const int64_t e = 1ll << o.t, f = o.c >= 0 ? (1ll << o.c) : 0;
                             t = o.form == 2 ? (e | f) : e;
                             c = o.form == 1 ? (e | f) : e;
-                        } else if (o.kind == qg::A_PH) {  // role vector W
+                        } else if (o.kind == qg::A_PH) {  // role vector W; one row per list factor
                             t = (1ll << o.t) | (o.c >= 0 ? (1ll << o.c) : 0);
-                            c = -1;
+                            for (const auto& x : o.ph) {
+                                const double e[8] = {x.second.first, x.second.second};
+                                row((int64_t)s, o.kind, t, -1, x.first, 0, e);
+                            }
+                            continue;
                         }
                         row((int64_t)s, o.kind, t, c, o.cmask, o.qmask, m);
                     }

@@ -36,6 +36,7 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxOps = 640;    // op words per pass
 constexpr int kMaxPred = 48;    // thread predicates (global-index masks) per pass
 constexpr int kMaxTph = 128;    // thread-phase entries per pass
+constexpr int kMaxPhe = 320;    // PH list entries per pass
 constexpr int kLaneBits = 5;
 constexpr int kMaxRegBits = 5;
 constexpr int kMaxWarpBits = 4;
@@ -63,23 +64,25 @@ struct CoefCap<double> {
 // Body codes are dense for the kernel's register width RB (one jump table):
 //   fam 0 RD   + T            real 2x2, V = W = e_T          coef: m00 m01 m10 m11
 //   fam 1 CD   + T            complex 2x2 (coef: 8 reals, row major)
-//   fam 2 PH   + T            x e where parity(W & p) ^ f = 1, W = e_T; coef: e;
-//                             predicate -> e or 1
-//   fam 3 RDW, 4 RDV, 5 CDW, 6 CDV  + pair index (T, C)   the W / V forms
-//   fam 7 PHW  + tri index (T > C)   phase with W = e_T + e_C
-//   fam 8 PH2  + tri index (T > C)   x e on logical |11> of slot bits (T, C); coef: e
+//   fam 2 PH   + T            x e where parity(W & p) ^ f = 1, W = e_T; the phase is
+//                             the product of a list of predicated entries (ph[]):
+//                             word bits 8-15 = entry count, 16-31 = first entry;
+//                             entry 0 is unconditional (its cmask is ignored)
+//   fam 3 RDW, 4 RDV  + pair index (T, C)   the W / V forms of RD
+//   fam 5 PHW  + tri index (T > C)   PH with W = e_T + e_C
+//   fam 6 PH2  + tri index (T > C)   x e on logical |11> of slot bits (T, C); coef: e
 //   OC_XF      F ^= payload where the predicate holds
 //   OC_CXM     payload T | C << 4: move slot p -> p ^ (p_C) e_T (materialises part of
 //              L), F_T ^= F_C.  Executed outside the jump table (see fused.cu).
-enum OpFam { F_RD = 0, F_CD, F_PH, F_RDW, F_RDV, F_CDW, F_CDV, F_PHW, F_PH2 };
+enum OpFam { F_RD = 0, F_CD, F_PH, F_RDW, F_RDV, F_PHW, F_PH2 };
 constexpr uint32_t OC_XF = 0xfe;
 constexpr uint32_t OC_CXM = 0xff;
 constexpr uint32_t kNoPred = 0xff;
 
 QG_HD constexpr int oc_base(int fam, int rb) {
     return fam <= F_PH ? fam * rb
-                       : (fam <= F_CDV ? 3 * rb + (fam - F_RDW) * rb * (rb - 1)
-                                       : 3 * rb + 4 * rb * (rb - 1) + (fam - F_PHW) * rb * (rb - 1) / 2);
+                       : (fam <= F_RDV ? 3 * rb + (fam - F_RDW) * rb * (rb - 1)
+                                       : 3 * rb + 2 * rb * (rb - 1) + (fam - F_PHW) * rb * (rb - 1) / 2);
 }
 QG_HD constexpr int oc_std(int fam, int rb, int t) { return oc_base(fam, rb) + t; }
 QG_HD constexpr int oc_pair(int fam, int rb, int t, int c) {
@@ -96,6 +99,13 @@ struct Entry {
     uint64_t cmask;      // global index bits that must all be 1
     uint64_t qmask;      // thread phase: bit selecting v1 over v0
     Real v[4];           // v0 = (v[0], v[1]), v1 = (v[2], v[3])
+};
+
+// one factor of an OC_PH phase: e where every bit of cmask is 1 in the thread's index
+template <typename Real>
+struct PhEnt {
+    uint64_t cmask;
+    Real e[2];
 };
 
 struct StageDesc {
@@ -129,6 +139,7 @@ struct PassDesc {
     uint64_t pred[kMaxPred];
     uint32_t ops[kMaxOps];
     Entry<Real> tph[kMaxTph];
+    PhEnt<Real> ph[kMaxPhe];
     Real coef[CoefCap<Real>::value];
 };
 

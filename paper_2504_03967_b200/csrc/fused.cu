@@ -286,6 +286,26 @@ __device__ __forceinline__ void run_cxm(T2 (&a)[1 << RB], uint32_t w, uint32_t& 
     }
 }
 
+// the thread's phase of an OC_PH word: product of its list entries whose
+// predicate holds (e.g. all the CR1 gates of a QFT row sharing one register target)
+template <typename T2, typename Real>
+__device__ __forceinline__ T2 ph_product(const PassDesc<Real>& P, uint32_t w, uint64_t tb) {
+    const int n = (w >> 8) & 0xffu, b = w >> 16;
+    T2 e;  // entry 0 is the unconditional factor (planner: flush_ph)
+    e.x = P.ph[b].e[0];
+    e.y = P.ph[b].e[1];
+    for (int k = 1; k < n; ++k) {
+        const PhEnt<Real>& E = P.ph[b + k];
+        if (pred_ok(tb, E.cmask)) {
+            T2 v;
+            v.x = E.e[0];
+            v.y = E.e[1];
+            e = cmul(e, v);
+        }
+    }
+    return e;
+}
+
 // One op word (desc.h).  F is the thread's flip vector: slot p holds logical
 // register index L^-1 (p ^ F).  Case labels are the dense codes of desc.h for
 // this RB; bodies that do not exist for this RB get unique unreachable labels.
@@ -303,13 +323,7 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
         if constexpr (T < RB) op_cd<RB, 1u << T, 1u << T>(a, m, F);                      \
         break;                                                                           \
     case QG_LAB(T < RB, oc_std(F_PH, RB, T), 16 + T):                                    \
-        if constexpr (T < RB) {                                                          \
-            T2 e;                                                                        \
-            e.x = m[0]; e.y = m[1];                                                      \
-            const uint32_t pi = (w >> 8) & 0xffu;                                        \
-            if (pi != kNoPred && !pred_ok(tb, P.pred[pi])) { e.x = Real(1); e.y = Real(0); } \
-            op_ph<RB, 1u << T, T2, Real>(a, e, F);                                       \
-        }                                                                                \
+        if constexpr (T < RB) op_ph<RB, 1u << T, T2, Real>(a, ph_product<T2>(P, w, tb), F); \
         break;
         QG_STD(0) QG_STD(1) QG_STD(2) QG_STD(3) QG_STD(4)
 #undef QG_STD
@@ -321,20 +335,9 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
     case QG_LAB(QG_OKP(T, C), oc_pair(F_RDV, RB, T, C), 200 + 5 * T + C):                \
         if constexpr (QG_OKP(T, C)) op_rd<RB, (1u << T) | (1u << C), 1u << T>(a, m, F);  \
         break;                                                                           \
-    case QG_LAB(QG_OKP(T, C), oc_pair(F_CDW, RB, T, C), 300 + 5 * T + C):                \
-        if constexpr (QG_OKP(T, C)) op_cd<RB, 1u << T, (1u << T) | (1u << C)>(a, m, F);  \
-        break;                                                                           \
-    case QG_LAB(QG_OKP(T, C), oc_pair(F_CDV, RB, T, C), 400 + 5 * T + C):                \
-        if constexpr (QG_OKP(T, C)) op_cd<RB, (1u << T) | (1u << C), 1u << T>(a, m, F);  \
-        break;                                                                           \
     case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PHW, RB, T, C), 500 + 5 * T + C):        \
-        if constexpr (QG_OKP(T, C) && C < T) {                                           \
-            T2 e;                                                                        \
-            e.x = m[0]; e.y = m[1];                                                      \
-            const uint32_t pi = (w >> 8) & 0xffu;                                        \
-            if (pi != kNoPred && !pred_ok(tb, P.pred[pi])) { e.x = Real(1); e.y = Real(0); } \
-            op_ph<RB, (1u << T) | (1u << C), T2, Real>(a, e, F);                         \
-        }                                                                                \
+        if constexpr (QG_OKP(T, C) && C < T)                                             \
+            op_ph<RB, (1u << T) | (1u << C), T2, Real>(a, ph_product<T2>(P, w, tb), F);  \
         break;                                                                           \
     case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PH2, RB, T, C), 600 + 5 * T + C):        \
         if constexpr (QG_OKP(T, C) && C < T) {                                           \

@@ -350,9 +350,13 @@ struct Emitter {
     std::vector<int> reg_of;  // physical qubit -> logical register bit or -1
     uint32_t row[kMaxRegBits];  // L as rows over logical bits
     std::vector<std::vector<M2>> pend;  // per logical bit: factors in application order
+    // per logical bit: pending phases on its |1> (predicate, e), applied as ONE
+    // OC_PH op; they commute with everything but non-diagonal actions on the bit
+    std::vector<std::vector<std::pair<uint64_t, cd>>> pph;
     int n_cxm = 0;
     Emitter(HostStage& h, const std::vector<int>& tq, int n, int rb_, cd& gp)
-        : hs(h), tile_q(tq), rb(rb_), gphase(gp), reg_of(n, -1), pend(h.reg_tile.size()) {
+        : hs(h), tile_q(tq), rb(rb_), gphase(gp), reg_of(n, -1), pend(h.reg_tile.size()),
+          pph(h.reg_tile.size()) {
         for (size_t b = 0; b < hs.reg_tile.size(); ++b) reg_of[tile_q[hs.reg_tile[b]]] = (int)b;
         for (int r = 0; r < kMaxRegBits; ++r) row[r] = 1u << r;
     }
@@ -407,16 +411,28 @@ struct Emitter {
         if (t < 0) { materialise(); t = b; }
         return t;
     }
-    // phase e on logical |1> of b: role vector W = row b of L^-1 (one or two slot bits)
+    // phase e on logical |1> of b (where the thread predicate cmask holds): queued
     void emit_phase(int b, cd e, uint64_t cmask) {
         if (e == cd(1)) return;
+        pph[b].emplace_back(cmask, e);
+    }
+    // one OC_PH op for b's queued phases; role vector W = row b of L^-1 (1 or 2 slot bits)
+    void flush_ph(int b) {
+        if (pph[b].empty()) return;
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         uint32_t w = inv[b];
         if (unit(w) < 0 && !two(w)) { materialise(); w = 1u << b; }
-        if (unit(w) >= 0) push(A_PH, unit(w), -1, cmask);
-        else push(A_PH, 31 - __builtin_clz(w), __builtin_ctz(w), cmask);  // W form, T > C
-        hs.ops.back().m[0] = e.real(); hs.ops.back().m[1] = e.imag();
+        if (unit(w) >= 0) push(A_PH, unit(w), -1);
+        else push(A_PH, 31 - __builtin_clz(w), __builtin_ctz(w));  // W form, T > C
+        HostOp& o = hs.ops.back();
+        // merge the unconditional factors into one
+        cd e0(1, 0);
+        for (const auto& x : pph[b]) if (!x.first) e0 *= x.second;
+        o.ph.push_back({0, {e0.real(), e0.imag()}});
+        for (const auto& x : pph[b])
+            if (x.first) o.ph.push_back({x.first, {x.second.real(), x.second.imag()}});
+        pph[b].clear();
     }
     void emit_diag(int b, const M2& m) {  // diag(d0, d1) = d0 * diag(1, d1 / d0)
         if (m.a00 != cd(1)) gphase *= m.a00;
@@ -425,15 +441,16 @@ struct Emitter {
     // 2x2 on logical b: pairs along V = L e_b, roles by W = row b of L^-1; the kernel
     // has bodies for V = W = e_T, (V = e_T, W = e_T + e_C) and (V = e_T + e_C, W = e_T)
     void emit_dense(int b, const M2& m) {
+        flush_ph(b);
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         uint32_t v = col(b), w = inv[b];
         int t = -1, c = -1;
         if (unit(v) >= 0 && v == w) {
             t = unit(v);
-        } else if (unit(v) >= 0 && two(w) && (w & v)) {
+        } else if (unit(v) >= 0 && two(w) && (w & v) && m_real(m)) {  // (no complex W/V bodies)
             t = unit(v); c = unit(w & ~v);
-        } else if (unit(w) >= 0 && two(v) && (w & v)) {
+        } else if (unit(w) >= 0 && two(v) && (w & v) && m_real(m)) {
             t = unit(w); c = unit(v & ~w);
         } else {
             materialise();
@@ -487,6 +504,7 @@ struct Emitter {
         const int rt = reg_of[g.t];
         switch (g.kind) {
             case K_H: case K_RX: case K_RY:
+                if (!pph[rt].empty()) { flush(rt); flush_ph(rt); }  // queued phases act first
                 pend[rt].push_back(gate_matrix(g.kind, g.p));
                 break;
             case K_RZ: {
@@ -497,6 +515,7 @@ struct Emitter {
             }
             case K_CX: {
                 flush(rt);
+                flush_ph(rt);
                 const int rc = reg_of[g.c];
                 if (rc >= 0) {
                     flush_nondiag(rc);
@@ -537,6 +556,7 @@ struct Emitter {
     }
     void finish() {
         for (size_t b = 0; b < pend.size(); ++b) flush((int)b);
+        for (size_t b = 0; b < pph.size(); ++b) flush_ph((int)b);
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         hs.out_vec.assign(rb, 0);
@@ -660,13 +680,13 @@ static int n_coef(const HostOp& o) {
     switch (o.kind) {
         case A_RD: return 4;
         case A_CD: return 8;
-        case A_PH: case A_PH2: return 2;
+        case A_PH2: return 2;
         default: return 0;
     }
 }
 
 // resource needs of a pass (descriptor capacity is checked by the scheduler)
-struct PassSize { int ops = 0, coef = 0, tph = 0, pred = 0; };
+struct PassSize { int ops = 0, coef = 0, tph = 0, pred = 0, phe = 0; };
 static PassSize pass_size(const HostPass& hp) {
     PassSize z;
     std::vector<uint64_t> preds;
@@ -675,7 +695,8 @@ static PassSize pass_size(const HostPass& hp) {
         z.tph += (int)h.tph.size();
         for (const HostOp& o : h.ops) {
             z.coef += n_coef(o);
-            if ((o.kind == A_PH || o.kind == A_XF) && o.cmask &&
+            z.phe += (int)o.ph.size();
+            if (o.kind == A_XF && o.cmask &&
                 std::find(preds.begin(), preds.end(), o.cmask) == preds.end())
                 preds.push_back(o.cmask);
         }
@@ -688,7 +709,8 @@ template <typename Real>
 static bool fits_t(const HostPass& hp) {
     const PassSize z = pass_size(hp);
     // one thread-phase slot is kept free for the plan's global phase
-    return z.ops <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph && z.pred <= kMaxPred;
+    return z.ops <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph && z.pred <= kMaxPred &&
+           z.phe <= kMaxPhe;
 }
 static bool fits(int dtype, const HostPass& hp) {
     return dtype == QG_DTYPE_C64 ? fits_t<float>(hp) : fits_t<double>(hp);
@@ -699,7 +721,7 @@ static uint32_t op_code(const HostOp& o, int rb) {
         case A_RD:
             return o.form == 0 ? oc_std(F_RD, rb, o.t) : oc_pair(o.form == 1 ? F_RDW : F_RDV, rb, o.t, o.c);
         case A_CD:
-            return o.form == 0 ? oc_std(F_CD, rb, o.t) : oc_pair(o.form == 1 ? F_CDW : F_CDV, rb, o.t, o.c);
+            return oc_std(F_CD, rb, o.t);  // complex ops only in the standard form
         case A_PH: return o.c < 0 ? oc_std(F_PH, rb, o.t) : oc_tri(F_PHW, rb, o.t, o.c);
         case A_PH2: return oc_tri(F_PH2, rb, o.t, o.c);
         case A_CXM: return OC_CXM;
@@ -724,7 +746,7 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
             if (std::find(hp.tile_q.begin(), hp.tile_q.end(), q) == hp.tile_q.end()) d.comp_q[nc0++] = (uint8_t)q;
     }
     fill_stage(dtype, hp, hp.io, d.stg[0]);
-    int no = 0, nc = 0, nt = 0, np = 0;
+    int no = 0, nc = 0, nt = 0, np = 0, nph = 0;
     auto pred_index = [&](uint64_t m) -> uint32_t {
         if (!m) return kNoPred;
         for (int i = 0; i < np; ++i) if (d.pred[i] == m) return (uint32_t)i;
@@ -742,8 +764,16 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
                 w = op_word(OC_XF, pred_index(o.cmask), (uint32_t)o.t);
             } else if (o.kind == A_CXM) {
                 w = op_word(OC_CXM, kNoPred, (uint32_t)(o.t | (o.c << 4)));
+            } else if (o.kind == A_PH) {
+                w = op_word(op_code(o, hp.cfg.rb), (uint32_t)o.ph.size(), (uint32_t)nph);
+                for (const auto& x : o.ph) {
+                    d.ph[nph].cmask = x.first;
+                    d.ph[nph].e[0] = (Real)x.second.first;
+                    d.ph[nph].e[1] = (Real)x.second.second;
+                    ++nph;
+                }
             } else {
-                w = op_word(op_code(o, hp.cfg.rb), o.kind == A_PH ? pred_index(o.cmask) : kNoPred, (uint32_t)nc);
+                w = op_word(op_code(o, hp.cfg.rb), kNoPred, (uint32_t)nc);
                 for (int i = 0; i < n_coef(o); ++i) d.coef[nc++] = (Real)o.m[i];
             }
             d.ops[no++] = w;
@@ -796,8 +826,8 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
         return QG_E_INVALID_ARG;
     }
     plan.cfg = cfg;
-    const int max_stages = opts.max_stages > 0 ? std::min(opts.max_stages, kMaxStages) : 4;
-    const double max_cost = opts.max_cost > 0 ? (double)opts.max_cost : 96.0;
+    const int max_stages = opts.max_stages > 0 ? std::min(opts.max_stages, kMaxStages) : kMaxStages;
+    const double max_cost = opts.max_cost > 0 ? (double)opts.max_cost : 250.0;
     const int c_low = n_local >= 20 ? kLaneBits : 0;  // small states live in L2: no coalescing constraint
 
     std::vector<int> phys(n), inv(n);  // logical -> physical, physical -> logical

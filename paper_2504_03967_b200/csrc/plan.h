@@ -40,7 +40,8 @@ struct HostOp {
     int form;       // A_RD / A_CD: 0 V = W = e_t; 1 V = e_t, W = e_t + e_c; 2 V = e_t + e_c, W = e_t
     int tq, cq;     // physical qubits (export / debugging)
     uint64_t cmask, qmask;  // thread predicate (all bits 1) / thread-phase select bit
-    double m[8];    // A_RD: m00 m01 m10 m11; A_CD: 2x2 complex; A_PH/A_PH2: e; A_TPH: v0, v1
+    double m[8];    // A_RD: m00 m01 m10 m11; A_CD: 2x2 complex; A_PH2: e; A_TPH: v0, v1
+    std::vector<std::pair<uint64_t, std::pair<double, double>>> ph;  // A_PH: (predicate, e) factors
 };
 
 struct HostStage {

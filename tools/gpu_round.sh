@@ -2,6 +2,7 @@
 # One GPU session: tests, smoke, bench, ncu launch list + one full capture of the fused kernel.
 # usage (under gpurun): bash tools/gpu_round.sh [tag]
 tag=${1:-r01}
+set -x
 out=gpurun_out
 mkdir -p $out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > $out/gpu_$tag.txt 2>&1
