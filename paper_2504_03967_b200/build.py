@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import os
+import re
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -17,7 +18,27 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 SOURCES = ["plan.cpp", "capi.cu", "fused.cu", "reduce.cu"]
-HEADERS = ["desc.h", "kernels.h", "plan.h"]
+HEADERS = ["desc.h", "kernels.h", "plan.h", "jt_lists.h"]
+
+
+def jump_table_ok(ptx: str) -> bool:
+    """fused.cu's run_op enters its switch through a PTX jump table whose targets
+    are inline-asm labels (QGJ_*).  Jumping to a label skips whatever NVVM placed
+    before it in the same basic block, so every label must directly follow a
+    block label or a branch."""
+    lines = ptx.split("\n")
+    n = 0
+    for i, line in enumerate(lines):
+        if not re.match(r"\s*QGJ_\w+:\s*$", line):
+            continue
+        n += 1
+        j = i - 1
+        while j >= 0 and (not lines[j].strip() or lines[j].strip().startswith(("//", ".loc"))):
+            j -= 1
+        prev = lines[j].strip() if j >= 0 else ""
+        if not (re.match(r"^\$L__BB\w+:$", prev) or re.match(r"^(@!?%p\d+ )?bra(\.uni)?\s", prev)):
+            return False
+    return n > 0 and ptx.count("brx.idx") > 0
 
 
 def _newest_input() -> float:
@@ -29,7 +50,15 @@ def _newest_input() -> float:
 
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    extra = []
+    if src == "fused.cu":
+        ptx = os.path.join(BUILD, "fused.ptx")
+        r = subprocess.run([NVCC, *ARCH, *FLAGS, "-ptx", os.path.join(CSRC, src), "-o", ptx],
+                           capture_output=True, text=True)
+        if r.returncode != 0 or not jump_table_ok(open(ptx).read()):
+            sys.stderr.write("fused.cu: PTX jump-table check failed; building the compare-tree dispatch\n")
+            extra = ["-DQG_NO_JT"]
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-warn-spills"]
     r = subprocess.run(cmd, capture_output=True, text=True)

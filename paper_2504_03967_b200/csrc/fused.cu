@@ -21,6 +21,7 @@
 #include <stdint.h>
 
 #include "desc.h"
+#include "jt_lists.h"
 #include "kernels.h"
 
 namespace qg {
@@ -309,38 +310,89 @@ __device__ __forceinline__ T2 ph_product(const PassDesc<Real>& P, uint32_t w, ui
 // One op word (desc.h).  F is the thread's flip vector: slot p holds logical
 // register index L^-1 (p ^ F).  Case labels are the dense codes of desc.h for
 // this RB; bodies that do not exist for this RB get unique unreachable labels.
+//
+// Dispatch: NVVM lowers this switch to a compare tree (~7 dependent ISETP+BRA
+// levels per op, the largest single overhead of the interpreter).  With
+// QG_JT the switch is entered through a PTX jump table instead: `brx.idx` on
+// the body code (ptxas emits one BRX and drops the then-unreachable tree), its
+// targets being PTX labels placed as the first statement of every case.  The
+// labels re-define the live values (w, tb, F) so everything a body computes
+// sits after its label; build.py verifies in the PTX that each label starts its
+// basic block and rebuilds without QG_JT otherwise.
+#ifndef QG_NO_JT
+#define QG_JT 1
+#endif
+#ifdef QG_JT
+#define QGJ_ENTER(name) asm volatile(name ":" ::: "memory")
+#else
+#define QGJ_ENTER(name) ((void)0)
+#endif
 #define QG_LAB(ok, code, junk) ((ok) ? (code) : 1000 + (junk))
 template <int RB, typename T2, typename Real>
 __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P, uint32_t w, uint64_t tb,
                                        uint32_t& F) {
-    const Real* m = P.coef + (w >> 16);
+#ifdef QG_JT
+    {
+        const uint32_t code = w & 0xffu;
+        if constexpr (RB == 5) {
+            const uint32_t idx = code == OC_XF ? QGJ_N_5 : code;
+            asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_5 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
+        } else if constexpr (RB == 4) {
+            const uint32_t idx = code == OC_XF ? QGJ_N_4 : code;
+            asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_4 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
+        } else {
+            static_assert(RB == 3, "jump tables exist for RB = 3, 4, 5");
+            const uint32_t idx = code == OC_XF ? QGJ_N_3 : code;
+            asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_3 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
+        }
+    }
+#endif
     switch (w & 0xffu) {
 #define QG_STD(T)                                                                        \
     case QG_LAB(T < RB, oc_std(F_RD, RB, T), T):                                         \
-        if constexpr (T < RB) op_rd<RB, 1u << T, 1u << T>(a, m, F);                      \
+        if constexpr (T < RB) {                                                          \
+            QGJ_ENTER("QGJ_RD_" #T);                                                     \
+            op_rd<RB, 1u << T, 1u << T>(a, P.coef + (w >> 16), F);                       \
+        }                                                                                \
         break;                                                                           \
     case QG_LAB(T < RB, oc_std(F_CD, RB, T), 8 + T):                                     \
-        if constexpr (T < RB) op_cd<RB, 1u << T, 1u << T>(a, m, F);                      \
+        if constexpr (T < RB) {                                                          \
+            QGJ_ENTER("QGJ_CD_" #T);                                                     \
+            op_cd<RB, 1u << T, 1u << T>(a, P.coef + (w >> 16), F);                       \
+        }                                                                                \
         break;                                                                           \
     case QG_LAB(T < RB, oc_std(F_PH, RB, T), 16 + T):                                    \
-        if constexpr (T < RB) op_ph<RB, 1u << T, T2, Real>(a, ph_product<T2>(P, w, tb), F); \
+        if constexpr (T < RB) {                                                          \
+            QGJ_ENTER("QGJ_PH_" #T);                                                     \
+            op_ph<RB, 1u << T, T2, Real>(a, ph_product<T2>(P, w, tb), F);                \
+        }                                                                                \
         break;
         QG_STD(0) QG_STD(1) QG_STD(2) QG_STD(3) QG_STD(4)
 #undef QG_STD
 #define QG_OKP(T, C) (T < RB && C < RB && T != C)
 #define QG_PAIR(T, C)                                                                    \
     case QG_LAB(QG_OKP(T, C), oc_pair(F_RDW, RB, T, C), 100 + 5 * T + C):                \
-        if constexpr (QG_OKP(T, C)) op_rd<RB, 1u << T, (1u << T) | (1u << C)>(a, m, F);  \
+        if constexpr (QG_OKP(T, C)) {                                                    \
+            QGJ_ENTER("QGJ_RDW_" #T "_" #C);                                             \
+            op_rd<RB, 1u << T, (1u << T) | (1u << C)>(a, P.coef + (w >> 16), F);         \
+        }                                                                                \
         break;                                                                           \
     case QG_LAB(QG_OKP(T, C), oc_pair(F_RDV, RB, T, C), 200 + 5 * T + C):                \
-        if constexpr (QG_OKP(T, C)) op_rd<RB, (1u << T) | (1u << C), 1u << T>(a, m, F);  \
+        if constexpr (QG_OKP(T, C)) {                                                    \
+            QGJ_ENTER("QGJ_RDV_" #T "_" #C);                                             \
+            op_rd<RB, (1u << T) | (1u << C), 1u << T>(a, P.coef + (w >> 16), F);         \
+        }                                                                                \
         break;                                                                           \
     case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PHW, RB, T, C), 500 + 5 * T + C):        \
-        if constexpr (QG_OKP(T, C) && C < T)                                             \
+        if constexpr (QG_OKP(T, C) && C < T) {                                           \
+            QGJ_ENTER("QGJ_PHW_" #T "_" #C);                                             \
             op_ph<RB, (1u << T) | (1u << C), T2, Real>(a, ph_product<T2>(P, w, tb), F);  \
+        }                                                                                \
         break;                                                                           \
     case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PH2, RB, T, C), 600 + 5 * T + C):        \
         if constexpr (QG_OKP(T, C) && C < T) {                                           \
+            QGJ_ENTER("QGJ_PH2_" #T "_" #C);                                             \
+            const Real* m = P.coef + (w >> 16);                                          \
             T2 e;                                                                        \
             e.x = m[0]; e.y = m[1];                                                      \
             const uint32_t ft = (F >> T) & 1u, fc = (F >> C) & 1u;                       \
@@ -354,6 +406,7 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
 #undef QG_PAIR
 #undef QG_OKP
         case OC_XF: {
+            QGJ_ENTER("QGJ_XF");
             const uint32_t pi = (w >> 8) & 0xffu;
             if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (w >> 16) & 31u;
             break;
@@ -362,6 +415,7 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
     }
 }
 #undef QG_LAB
+#undef QGJ_ENTER
 
 // a stage's op list: runs of jump-table ops separated by runs of OC_CXM words
 template <int RB, typename T2, typename Real>
