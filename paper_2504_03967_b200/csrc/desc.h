@@ -73,7 +73,7 @@ struct CoefCap<double> {
 //   fam 6 PH2  + tri index (T > C)   x e on logical |11> of slot bits (T, C); coef: e
 //   OC_XF      F ^= payload where the predicate holds
 //   OC_CXM     payload T | C << 4: move slot p -> p ^ (p_C) e_T (materialises part of
-//              L), F_T ^= F_C.  Executed outside the jump table (see fused.cu).
+//              L), F_T ^= F_C.
 enum OpFam { F_RD = 0, F_CD, F_PH, F_RDW, F_RDV, F_PHW, F_PH2 };
 constexpr uint32_t OC_XF = 0xfe;
 constexpr uint32_t OC_CXM = 0xff;
@@ -137,7 +137,7 @@ struct PassDesc {
     // stg[0] = coalesced io mapping (lanes = tile bits 0..4); stg[1 + s] = compute stage s
     StageDesc stg[kMaxStages + 1];
     uint64_t pred[kMaxPred];
-    uint32_t ops[kMaxOps];
+    uint32_t ops[kMaxOps + 1];  // + 1: the kernel prefetches one word past a stage's list
     Entry<Real> tph[kMaxTph];
     PhEnt<Real> ph[kMaxPhe];
     Real coef[CoefCap<Real>::value];

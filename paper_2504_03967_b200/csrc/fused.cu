@@ -335,14 +335,14 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
     {
         const uint32_t code = w & 0xffu;
         if constexpr (RB == 5) {
-            const uint32_t idx = code == OC_XF ? QGJ_N_5 : code;
+            const uint32_t idx = code == OC_XF ? QGJ_N_5 : (code == OC_CXM ? QGJ_N_5 + 1 : code);
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_5 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
         } else if constexpr (RB == 4) {
-            const uint32_t idx = code == OC_XF ? QGJ_N_4 : code;
+            const uint32_t idx = code == OC_XF ? QGJ_N_4 : (code == OC_CXM ? QGJ_N_4 + 1 : code);
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_4 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
         } else {
             static_assert(RB == 3, "jump tables exist for RB = 3, 4, 5");
-            const uint32_t idx = code == OC_XF ? QGJ_N_3 : code;
+            const uint32_t idx = code == OC_XF ? QGJ_N_3 : (code == OC_CXM ? QGJ_N_3 + 1 : code);
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_3 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
         }
     }
@@ -411,27 +411,27 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
             if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (w >> 16) & 31u;
             break;
         }
+        case OC_CXM: {
+            QGJ_ENTER("QGJ_CXM");
+            run_cxm<RB>(a, w, F);
+            break;
+        }
         default: __builtin_unreachable();
     }
 }
 #undef QG_LAB
 #undef QGJ_ENTER
 
-// a stage's op list: runs of jump-table ops separated by runs of OC_CXM words
+// a stage's op list; the next op word is fetched before the current op runs
+// (the descriptor has slack after the last word, so the read is in bounds)
 template <int RB, typename T2, typename Real>
 __device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<Real>& P, int o, const int end,
                                               uint64_t tb, uint32_t& F) {
-    while (o < end) {
-        for (; o < end; ++o) {
-            const uint32_t w = P.ops[o];
-            if ((w & 0xffu) == OC_CXM) break;
-            run_op<RB>(a, P, w, tb, F);
-        }
-        for (; o < end; ++o) {
-            const uint32_t w = P.ops[o];
-            if ((w & 0xffu) != OC_CXM) break;
-            run_cxm<RB>(a, w, F);
-        }
+    uint32_t w = P.ops[o];
+    for (; o < end; ++o) {
+        const uint32_t wn = P.ops[o + 1];
+        run_op<RB>(a, P, w, tb, F);
+        w = wn;
     }
 }
 
