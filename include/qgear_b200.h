@@ -48,6 +48,7 @@ extern "C" {
 #define QG_E_NONFINITE_PARAM -11     /* NonFiniteParamError */
 #define QG_E_INVALID_GATE -12        /* InvalidGateError */
 #define QG_E_OUT_OF_MEMORY -13
+#define QG_E_CONTAINER_FORMAT -14    /* ContainerFormatError   container.py:87-115 */
 
 #define QG_DTYPE_C64 0
 #define QG_DTYPE_C128 1
@@ -101,6 +102,12 @@ typedef struct {
 int qg_plan_create(const int32_t* gate_type, const double* gate_param, int64_t n_gates,
                    int32_t n_qubits, const qg_plan_opts* opts, qg_plan** out);
 int qg_plan_destroy(qg_plan* plan);
+/* batched parameter sets (CircuitSet circuits that share one gate structure):
+ * new gate_param (n_gates >= the plan's body gates, same order as at create)
+ * for the same gate_type; re-emits each pass from its stored schedule (no
+ * rescheduling) and rebuilds the device program.  Same errors as create for
+ * the parameters (QG_E_NONFINITE_PARAM). */
+int qg_plan_rebind(qg_plan* plan, const double* gate_param, int64_t n_gates);
 int qg_plan_get_info(const qg_plan* plan, qg_plan_info* out);
 int qg_plan_get_remap(const qg_plan* plan, int64_t remap_index, qg_remap* out);
 /* logical qubit q sits at physical position phys_of_logical[q] after the last
@@ -137,6 +144,18 @@ int qg_apply_cx(void* state, int32_t n_local, int32_t dtype, int32_t control, in
 int qg_apply_cr1(void* state, int32_t n_local, int32_t dtype, int32_t control, int32_t target, double lam,
                  void* stream);
 
+/* ---- QCrank data register: uniformly controlled RY --------
+ * For every assignment a of the m address qubits (bit k of a = qubit
+ * addr_qubits[k]) apply RY(alpha_dev[a * n_targets + j]) to qubit targets[j],
+ * j < n_targets <= 5, in one pass.  Equivalent to the Gray-code gate block
+ * (2^m RY + 2^m CX per target) that qcrank.build_qcrank_circuit emits; the host
+ * collapses that block to this call.  alpha_dev: float64 device array.
+ * workspace >= qg_ucry_workspace_bytes (per-address cos/sin table). */
+int64_t qg_ucry_workspace_bytes(int32_t m, int32_t n_targets, int32_t dtype);
+int qg_apply_ucry(void* state, int32_t n_local, int32_t dtype, const int32_t* addr_qubits, int32_t m,
+                  const int32_t* targets, int32_t n_targets, const double* alpha_dev, void* workspace,
+                  int64_t workspace_bytes, void* stream);
+
 /* ---- reductions and sampling (statevec.py:47-50, 215-234) ----------------- */
 /* sum |a|^2 in float64; result written to *out_host (synchronises `stream`) */
 int qg_norm_sq(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
@@ -155,6 +174,27 @@ int qg_sample(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, u
               const double* uniforms_dev, double norm_tol, void* workspace, int64_t workspace_bytes,
               int64_t* out_index_dev, int64_t* out_count_dev, int64_t* n_unique_host,
               double* norm_sq_host, void* stream);
+
+/* ---- QGIR1 container (container.py:1-16, 71-115): native parse / write ------
+ * qg_qgir1_parse validates a whole file image and reports the byte offsets of
+ * its arrays (zero-copy ingest: map the file, pass the int32 / float64 arrays
+ * to qg_plan_create); errors (bad magic, truncated, trailing bytes) return
+ * QG_E_CONTAINER_FORMAT with the message in qg_container_last_error(). */
+typedef struct {
+    uint32_t capacity, n_circ, n_meta, pad;
+    int64_t headers_off;      /* int32 (n_circ, 3) */
+    int64_t gate_type_off;    /* int32 (n_circ, capacity, 3) */
+    int64_t gate_param_off;   /* float64 (n_circ, capacity) */
+    int64_t meta_off;         /* n_meta x (u32 len, key, u32 len, value) */
+    int64_t total_bytes;
+} qg_qgir1_info;
+int qg_qgir1_parse(const void* buf, int64_t len, qg_qgir1_info* out);
+int64_t qg_qgir1_size(uint32_t capacity, uint32_t n_circ, uint32_t n_meta, const int64_t* meta_lens);
+/* meta: 2*n_meta strings (key0, value0, key1, ...) in sorted key order, byte lengths in meta_lens */
+int qg_qgir1_write(void* buf, int64_t len, uint32_t capacity, uint32_t n_circ, const int32_t* headers,
+                   const int32_t* gate_type, const double* gate_param, uint32_t n_meta, const char* const* meta,
+                   const int64_t* meta_lens);
+const char* qg_container_last_error(void);
 
 const char* qg_last_error(void);
 int qg_abi_version(void);

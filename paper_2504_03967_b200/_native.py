@@ -27,6 +27,12 @@ class PlanOpts(C.Structure):
                 ("kernel_cfg", C.c_int32), ("reserved", C.c_int32 * 5)]
 
 
+class Qgir1Info(C.Structure):
+    _fields_ = [("capacity", C.c_uint32), ("n_circ", C.c_uint32), ("n_meta", C.c_uint32), ("pad", C.c_uint32),
+                ("headers_off", C.c_int64), ("gate_type_off", C.c_int64), ("gate_param_off", C.c_int64),
+                ("meta_off", C.c_int64), ("total_bytes", C.c_int64)]
+
+
 class PlanInfo(C.Structure):
     _fields_ = [("n_body_gates", C.c_int64), ("n_passes", C.c_int64), ("n_segments", C.c_int64),
                 ("n_remaps", C.c_int64), ("n_ops", C.c_int64), ("n_stages", C.c_int64),
@@ -46,6 +52,7 @@ _P = C.c_void_p
 _SIGS = {
     "qg_plan_create": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.POINTER(PlanOpts), C.POINTER(_P)]),
     "qg_plan_destroy": (C.c_int, [_P]),
+    "qg_plan_rebind": (C.c_int, [_P, _P, C.c_int64]),
     "qg_plan_get_info": (C.c_int, [_P, C.POINTER(PlanInfo)]),
     "qg_plan_get_remap": (C.c_int, [_P, C.c_int64, C.POINTER(Remap)]),
     "qg_plan_get_final_map": (C.c_int, [_P, _P]),
@@ -56,11 +63,17 @@ _SIGS = {
     "qg_apply_matrix": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "qg_apply_cx": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "qg_apply_cr1": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _P]),
+    "qg_ucry_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "qg_apply_ucry": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int32, _P, C.c_int32, _P, _P, C.c_int64, _P]),
     "qg_norm_sq": (C.c_int, [_P, C.c_int64, C.c_int32, _P, C.c_int64, C.POINTER(C.c_double), _P]),
     "qg_probabilities": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P]),
     "qg_sample_workspace_bytes": (C.c_int64, [C.c_int64, C.c_int64]),
     "qg_sample": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int64, C.c_uint64, _P, C.c_double, _P, C.c_int64,
                             _P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_double), _P]),
+    "qg_qgir1_parse": (C.c_int, [_P, C.c_int64, C.POINTER(Qgir1Info)]),
+    "qg_qgir1_size": (C.c_int64, [C.c_uint32, C.c_uint32, C.c_uint32, _P]),
+    "qg_qgir1_write": (C.c_int, [_P, C.c_int64, C.c_uint32, C.c_uint32, _P, _P, _P, C.c_uint32, _P, _P]),
+    "qg_container_last_error": (C.c_char_p, []),
     "qg_last_error": (C.c_char_p, []),
     "qg_abi_version": (C.c_int, []),
 }
@@ -93,8 +106,8 @@ def lib() -> C.CDLL:
 
 def check(code: int) -> None:
     if code != 0:
-        msg = lib().qg_last_error().decode(errors="replace")
-        raise_for_status(code, msg)
+        err = lib().qg_container_last_error if code == -14 else lib().qg_last_error
+        raise_for_status(code, err().decode(errors="replace"))
 
 
 def call(name: str, *args) -> None:

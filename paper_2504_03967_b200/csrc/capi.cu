@@ -6,6 +6,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/qgear_b200.h"
 #include "kernels.h"
@@ -86,6 +87,19 @@ int qg_plan_create(const int32_t* gate_type, const double* gate_param, int64_t n
     }
     *out = p;
     return QG_OK;
+}
+
+int qg_plan_rebind(qg_plan* plan, const double* gate_param, int64_t n_gates) {
+    if (!plan) return fail(QG_E_INVALID_ARG, "plan is NULL");
+    std::string err;
+    int rc;
+    try {
+        rc = qg::rebind_plan(*plan, gate_param, n_gates, err);
+    } catch (const std::bad_alloc&) {
+        rc = QG_E_OUT_OF_MEMORY;
+        err = "out of host memory while rebinding";
+    }
+    return rc == QG_OK ? QG_OK : fail(rc, err);
 }
 
 int qg_plan_destroy(qg_plan* plan) {
@@ -256,6 +270,51 @@ int qg_apply_matrix(void* state, int32_t n_local, int32_t dtype, int32_t target,
     op.t = target;
     std::memcpy(op.m, u, sizeof(op.m));
     return single_gate(state, n_local, dtype, op, stream);
+}
+
+int64_t qg_ucry_workspace_bytes(int32_t m, int32_t n_targets, int32_t dtype) {
+    if (m < 0 || m > 34 || n_targets < 1 || n_targets > qg::kMaxUcryTargets) return -1;
+    return qg::ucry_workspace_bytes(m, n_targets, dtype);
+}
+
+int qg_apply_ucry(void* state, int32_t n_local, int32_t dtype, const int32_t* addr_qubits, int32_t m,
+                  const int32_t* targets, int32_t n_targets, const double* alpha_dev, void* workspace,
+                  int64_t workspace_bytes, void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (!state || !alpha_dev || !workspace || (m > 0 && !addr_qubits) || !targets)
+        return fail(QG_E_INVALID_ARG, "NULL argument");
+    if (n_targets < 1 || n_targets > qg::kMaxUcryTargets)
+        return fail(QG_E_INVALID_ARG, "n_targets must be in [1, 5]");
+    if (m < 0 || m > 34 || m + n_targets > n_local) return fail(QG_E_INVALID_ARG, "bad address register size");
+    if (workspace_bytes < qg::ucry_workspace_bytes(m, n_targets, dtype))
+        return fail(QG_E_INVALID_ARG, "workspace too small");
+    std::vector<int> used(n_local, 0);
+    qg::UcryOp op{};
+    op.m = m;
+    op.n_t = n_targets;
+    auto take = [&](int q) -> int {
+        if (q < 0 || q >= n_local)
+            return fail(QG_E_INDEX_OUT_OF_RANGE, "qubit " + std::to_string(q) + " out of range for " +
+                                                     std::to_string(n_local) + " qubits");
+        if (used[q]) return fail(QG_E_SELF_PAIR, "qubit " + std::to_string(q) + " listed twice");
+        used[q] = 1;
+        return QG_OK;
+    };
+    op.addr_contig = 1;
+    for (int k = 0; k < m; ++k) {
+        if (int rc = take(addr_qubits[k])) return rc;
+        op.addr_pos[k] = (uint8_t)addr_qubits[k];
+        if (k > 0 && addr_qubits[k] != addr_qubits[k - 1] + 1) op.addr_contig = 0;
+    }
+    if (m == 0) op.addr_pos[0] = 0;
+    for (int j = 0; j < n_targets; ++j) {
+        if (int rc = take(targets[j])) return rc;
+        op.tgt_pos[j] = (uint8_t)targets[j];
+    }
+    for (int q = 0; q < n_local; ++q)
+        if (!used[q]) op.rest_pos[op.n_rest++] = (uint8_t)q;
+    QG_CUDA(qg::launch_ucry(dtype, state, op, alpha_dev, workspace, (cudaStream_t)stream), "ucry launch");
+    return QG_OK;
 }
 
 static int check_pair(int32_t n, int32_t c, int32_t t) {

@@ -10,6 +10,17 @@ namespace qg {
 cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uint64_t rank_bits, cudaStream_t st);
 cudaError_t launch_gate(int dtype, const GateOp& op, void* psi, int n_local, uint64_t rank_bits, cudaStream_t st);
 
+// uniformly controlled RY (ucry.cu): up to 5 targets per pass
+constexpr int kMaxUcryTargets = 5;
+struct UcryOp {
+    int32_t m, n_t, n_rest, addr_contig;  // address bits, targets, remaining bits, address = contiguous run
+    uint8_t addr_pos[40];
+    uint8_t tgt_pos[kMaxUcryTargets];
+    uint8_t rest_pos[64];
+};
+int64_t ucry_workspace_bytes(int m, int n_t, int dtype);
+cudaError_t launch_ucry(int dtype, void* psi, const UcryOp& op, const double* alpha_dev, void* ws, cudaStream_t st);
+
 cudaError_t launch_init_zero(void* psi, int n_local, int dtype, int rank, cudaStream_t st);
 // partial fp64 sums of |a|^2: grid-stride, one double per CTA into `partial`, then
 // a single-CTA finish into partial[n_parts]

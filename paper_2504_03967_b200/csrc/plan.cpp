@@ -114,7 +114,7 @@ static int validate(const int32_t* gt, const double* gp, int64_t n_gates, int n,
             err = "gate " + std::to_string(i) + ": non-finite parameter";
             return QG_E_NONFINITE_PARAM;
         }
-        body.push_back(Gate{k, (k == K_CX || k == K_CR1) ? c : -1, t, p});
+        body.push_back(Gate{k, (k == K_CX || k == K_CR1) ? c : -1, t, p, i});
     }
     return QG_OK;
 }
@@ -192,11 +192,6 @@ static double gate_cost(const Gate& g, const std::vector<char>& in_reg) {
     }
 }
 constexpr double kStageCost = 6.0;
-
-struct StageSched {
-    std::vector<int> regs;   // physical register qubits demanded (<= rb)
-    std::vector<Gate> gates; // executed in this order (physical qubits)
-};
 
 // Schedules one fused pass from `rem` (physical-qubit gates, valid order);
 // leaves the unscheduled gates in `rem` (still a valid order).
@@ -798,6 +793,82 @@ static void add_global_phase(PassDesc<Real>& d, cd g) {
     sd.tph_end = (uint16_t)(sd.tph_end + 1);
 }
 
+// device descriptors of every pass, stats, and the plan's global phase
+static int build_descriptors(qg_plan& plan, std::string& err) {
+    cd gphase(1, 0);
+    int64_t last_desc = -1;
+    plan.d32.clear();
+    plan.d64.clear();
+    plan.desc_index.assign(plan.segs.size(), {});
+    plan.stats = PlanStats{};
+    for (size_t s = 0; s < plan.segs.size(); ++s) {
+        for (const HostPass& hp : plan.segs[s]) {
+            int64_t idx = -1;
+            if (hp.fused) {
+                gphase *= cd(hp.gph_re, hp.gph_im);
+                if (plan.dtype == QG_DTYPE_C64) {
+                    plan.d32.emplace_back();
+                    if (!build_desc<float>(hp, plan.n_local, plan.d32.back(), err)) return QG_E_INVALID_ARG;
+                    idx = (int64_t)plan.d32.size() - 1;
+                } else {
+                    plan.d64.emplace_back();
+                    if (!build_desc<double>(hp, plan.n_local, plan.d64.back(), err)) return QG_E_INVALID_ARG;
+                    idx = (int64_t)plan.d64.size() - 1;
+                }
+                last_desc = idx;
+                plan.stats.n_stages += (int64_t)hp.stages.size();
+                plan.stats.n_cxm += hp.n_cxm;
+                for (const HostStage& h : hp.stages) plan.stats.n_ops += (int64_t)(h.ops.size() + h.tph.size());
+            } else {
+                plan.stats.n_ops += 1;
+            }
+            plan.desc_index[s].push_back(idx);
+        }
+    }
+    if (last_desc >= 0 && gphase != cd(1, 0)) {
+        if (plan.dtype == QG_DTYPE_C64) add_global_phase(plan.d32[last_desc], gphase);
+        else add_global_phase(plan.d64[last_desc], gphase);
+    }
+    plan.gphase_re = gphase.real();
+    plan.gphase_im = gphase.imag();
+    return QG_OK;
+}
+
+int rebind_plan(qg_plan& plan, const double* gate_param, int64_t n_gates, std::string& err) {
+    if (n_gates < plan.n_body || (plan.n_body > 0 && !gate_param)) {
+        err = "rebind needs the parameters of all " + std::to_string(plan.n_body) + " body gates";
+        return QG_E_INVALID_ARG;
+    }
+    for (int64_t i = 0; i < plan.n_body; ++i) {
+        const int k = plan.body[i].kind;
+        if ((k == K_RX || k == K_RY || k == K_RZ || k == K_CR1) && !std::isfinite(gate_param[i])) {
+            err = "gate " + std::to_string(i) + ": non-finite parameter";
+            return QG_E_NONFINITE_PARAM;
+        }
+    }
+    for (int64_t i = 0; i < plan.n_body; ++i) plan.body[i].p = gate_param[i];
+    for (auto& seg : plan.segs)
+        for (HostPass& hp : seg) {
+            if (hp.fused) {
+                for (StageSched& st : hp.sched)
+                    for (Gate& g : st.gates) g.p = gate_param[g.idx];
+                HostPass fresh = make_fused_pass(plan.dtype, hp.cfg, plan.n, hp.tile_q, hp.sched);
+                if (!fits(plan.dtype, fresh)) {
+                    err = "rebound pass exceeds descriptor capacity (plan the circuit afresh)";
+                    return QG_E_INVALID_ARG;
+                }
+                fresh.sched = std::move(hp.sched);
+                hp = std::move(fresh);
+            } else {
+                Gate g = hp.gate;
+                g.p = gate_param[g.idx];
+                hp = make_unfused_pass(g, plan.n_local);
+                hp.gate = g;
+            }
+        }
+    return build_descriptors(plan, err);
+}
+
 // ------------------------------------------------------------------ driver
 int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gates, int n_qubits,
                const qg_plan_opts& opts, qg_plan& plan, std::string& err) {
@@ -861,11 +932,13 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
                     max_gates = std::max(1, hp.n_gates * 3 / 4);
                 }
                 if (stages.empty()) break;
+                hp.sched = stages;
                 plan.segs.back().push_back(std::move(hp));
             } else {
                 const Gate& g = rem.front();
                 if (!is_diag(g) && g.t >= n_local) break;
                 plan.segs.back().push_back(make_unfused_pass(g, n_local));
+                plan.segs.back().back().gate = g;
                 rem.erase(rem.begin());
             }
             if (rem.size() == before) break;
@@ -901,40 +974,8 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
     }
     plan.final_phys = phys;
 
-    // device descriptors
-    cd gphase(1, 0);
-    int64_t last_desc = -1;
-    plan.desc_index.resize(plan.segs.size());
-    for (size_t s = 0; s < plan.segs.size(); ++s) {
-        for (const HostPass& hp : plan.segs[s]) {
-            int64_t idx = -1;
-            if (hp.fused) {
-                gphase *= cd(hp.gph_re, hp.gph_im);
-                if (plan.dtype == QG_DTYPE_C64) {
-                    plan.d32.emplace_back();
-                    if (!build_desc<float>(hp, n_local, plan.d32.back(), err)) return QG_E_INVALID_ARG;
-                    idx = (int64_t)plan.d32.size() - 1;
-                } else {
-                    plan.d64.emplace_back();
-                    if (!build_desc<double>(hp, n_local, plan.d64.back(), err)) return QG_E_INVALID_ARG;
-                    idx = (int64_t)plan.d64.size() - 1;
-                }
-                last_desc = idx;
-                plan.stats.n_stages += (int64_t)hp.stages.size();
-                plan.stats.n_cxm += hp.n_cxm;
-                for (const HostStage& h : hp.stages) plan.stats.n_ops += (int64_t)(h.ops.size() + h.tph.size());
-            } else {
-                plan.stats.n_ops += 1;
-            }
-            plan.desc_index[s].push_back(idx);
-        }
-    }
-    if (last_desc >= 0 && gphase != cd(1, 0)) {
-        if (plan.dtype == QG_DTYPE_C64) add_global_phase(plan.d32[last_desc], gphase);
-        else add_global_phase(plan.d64[last_desc], gphase);
-    }
-    plan.gphase_re = gphase.real();
-    plan.gphase_im = gphase.imag();
+    plan.body = body;
+    return build_descriptors(plan, err);
     return QG_OK;
 }
 

@@ -22,6 +22,13 @@ struct Gate {
     int kind;
     int c, t;    // logical qubits (c = -1 for 1q kinds)
     double p;
+    int64_t idx = -1;  // position in the circuit body (qg_plan_rebind)
+};
+
+// one register stage of a pass as scheduled (kept for qg_plan_rebind)
+struct StageSched {
+    std::vector<int> regs;   // physical register qubits demanded (<= rb)
+    std::vector<Gate> gates; // executed in this order (physical qubits)
 };
 
 // a fused-kernel configuration: RB register bits, WB warp bits, k = RB + 5 + WB
@@ -61,6 +68,8 @@ struct HostPass {
     GateOp gop{};                     // unfused single gate
     int n_gates = 0;                  // circuit gates covered by this pass
     int n_cxm = 0;                    // materialised register CX ops
+    std::vector<StageSched> sched;    // the schedule this pass was emitted from
+    Gate gate{};                      // unfused: the gate
     double gph_re = 1.0, gph_im = 0.0; // global phase factored out of this pass's diagonal ops
 };
 
@@ -79,6 +88,7 @@ struct qg_plan {
     std::vector<int> final_phys;  // logical qubit -> physical position at the end
     qg::PlanStats stats;
     double gphase_re = 1.0, gphase_im = 0.0;  // global phase applied in the last fused pass
+    std::vector<qg::Gate> body;       // validated circuit body (logical qubits), for rebind
     // device descriptors, built once at plan time (index = running fused-pass id)
     std::vector<qg::PassDesc<float>> d32;
     std::vector<qg::PassDesc<double>> d64;
@@ -89,4 +99,7 @@ namespace qg {
 // returns QG_OK or an error code; message in `err`
 int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gates, int n_qubits,
                const qg_plan_opts& opts, qg_plan& plan, std::string& err);
+// new parameters for the same gate structure: re-emits every pass from its
+// stored schedule (no rescheduling) and rebuilds the device descriptors
+int rebind_plan(qg_plan& plan, const double* gate_param, int64_t n_gates, std::string& err);
 }  // namespace qg

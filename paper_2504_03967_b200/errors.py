@@ -118,6 +118,7 @@ _BY_CODE = {
     -11: NonFiniteParamError,       # QG_E_NONFINITE_PARAM
     -12: InvalidGateError,          # QG_E_INVALID_GATE
     -13: MemoryError,               # QG_E_OUT_OF_MEMORY
+    -14: ContainerFormatError,      # QG_E_CONTAINER_FORMAT
 }
 
 

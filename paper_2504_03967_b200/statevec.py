@@ -298,6 +298,16 @@ class CompiledCircuit:
         N.check(self._lib.qg_plan_get_final_map(self._h, fm.ctypes.data_as(C.c_void_p)))
         self.final_map = fm  # logical qubit -> physical position
 
+    def rebind(self, gate_param: np.ndarray) -> "CompiledCircuit":
+        """New parameters for the same gate structure (a CircuitSet's batched
+        parameter sets): reuses the schedule, rebuilds only the program."""
+        gp = np.ascontiguousarray(gate_param, dtype=np.float64).reshape(-1)
+        N.check(self._lib.qg_plan_rebind(self._h, gp.ctypes.data_as(C.c_void_p), gp.shape[0]))
+        info = N.PlanInfo()
+        N.check(self._lib.qg_plan_get_info(self._h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in N.PlanInfo._fields_}
+        return self
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
@@ -346,7 +356,14 @@ def run_circuit(circuit, options: SimOptions | None = None):
     """Apply the live gates in order; sample once iff shots > 0 (statevec.py:200-212)."""
     options = options or SimOptions()
     gt, gp, n = circuit_arrays(circuit)
-    _trailing_split_arrays(gt[:, 0])                               # MeasureMidCircuitError first
+    nb = _trailing_split_arrays(gt[:, 0])                          # MeasureMidCircuitError first
+    if options.fuse and nb >= 32:
+        # QCrank-style uniformly controlled RY blocks (2^m RY + 2^m CX each) run as
+        # one-pass UCRY kernels instead of 2^(m+1) gates (qcrank.collapse_ucry)
+        from . import qcrank
+
+        if any(it[0] == "ucry" for it in qcrank.collapse_ucry(gt[:nb], gp[:nb])):
+            return qcrank.run_gates(gt, gp, n, options)
     _check_budget(n, options.precision, options.memory_budget)     # then TooManyQubitsError
     plan = CompiledCircuit(gt, gp, n, options.precision, 0, options.fuse, options.tile_qubits,
                            options.max_stages, options.max_cost)   # then gate errors
