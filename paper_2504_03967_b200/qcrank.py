@@ -216,71 +216,85 @@ class UcrySegment:
     alpha: np.ndarray   # (2^m,) net RY angle per address
 
 
-def _match_block(gt: np.ndarray, gp: np.ndarray, start: int, min_addr: int):
-    """A Gray-code UCRY block starting at `start`: (end, UcrySegment) or None."""
-    n_rows = gt.shape[0]
-    if gt[start, 0] != GateKind.RY or start + 1 >= n_rows or gt[start + 1, 0] != GateKind.CX:
-        return None
+def _block_at(gt: np.ndarray, gp: np.ndarray, start: int, pairs: int, min_addr: int):
+    """Largest Gray-code UCRY block (m >= min_addr) at `start` within a run of
+    `pairs` (RY(t), CX(*, t)) row pairs: (n_pairs_used, UcrySegment) or None."""
     target = int(gt[start, 2])
-    # candidate m from the run of alternating RY(target) / CX(*, target) rows
-    k = start
-    while k + 1 < n_rows and gt[k, 0] == GateKind.RY and gt[k, 2] == target and \
-            gt[k + 1, 0] == GateKind.CX and gt[k + 1, 2] == target:
-        k += 2
-    pairs = (k - start) // 2
     m = pairs.bit_length() - 1
     while m >= min_addr:
         n = 1 << m
         ctrls = gt[start + 1:start + 2 * n:2, 1]
         bits = gray_controls(m)
-        # address qubit of bit b = the control at the first rotation whose change bit is b
-        addr = [-1] * m
-        ok = True
-        for b in range(m):
-            first = int(np.argmax(bits == b))
-            addr[b] = int(ctrls[first])
-        if len(set(addr)) != m or target in addr:
-            ok = False
-        if ok and np.array_equal(ctrls, np.asarray(addr)[bits]):
-            alpha = inverse_gray_walsh(gp[start:start + 2 * n:2])
-            return start + 2 * n, UcrySegment(target, addr, alpha)
+        first = np.array([int(np.argmax(bits == b)) for b in range(m)])
+        addr = ctrls[first]
+        if len(set(addr.tolist())) == m and target not in addr and np.array_equal(ctrls, addr[bits]):
+            return n, UcrySegment(target, addr.tolist(), inverse_gray_walsh(gp[start:start + 2 * n:2]))
         m -= 1
     return None
+
+
+def _pair_runs(gt: np.ndarray, min_pairs: int):
+    """(start row, pairs) of maximal runs of (RY(t), CX(*, t)) row pairs on one t."""
+    k, t = gt[:, 0], gt[:, 2]
+    if k.size < 2:
+        return []
+    pair = (k[:-1] == GateKind.RY) & (k[1:] == GateKind.CX) & (t[:-1] == t[1:])
+    runs = []
+    for par in (0, 1):
+        ok = pair[par::2]
+        tt = t[par::2][:ok.size]
+        cont = np.zeros(ok.size, dtype=bool)  # cont[j]: pair j continues the run of pair j - 1
+        cont[1:] = ok[1:] & ok[:-1] & (tt[1:] == tt[:-1])
+        starts = np.flatnonzero(ok & ~cont)
+        ends = np.flatnonzero(ok & ~np.append(cont[1:], False))
+        for j0, j1 in zip(starts.tolist(), ends.tolist()):
+            if j1 - j0 + 1 >= min_pairs:
+                runs.append((par + 2 * j0, j1 - j0 + 1))
+    return sorted(runs)
 
 
 def collapse_ucry(gate_type: np.ndarray, gate_param: np.ndarray, min_addr: int = 4):
     """Split a gate array into [("gates", gt, gp) | ("ucry", UcrySegment)] items,
     replacing every Gray-code uniformly controlled RY block over >= min_addr
-    address qubits by one UCRY item (its angles recovered exactly up to fp64)."""
+    address qubits by one UCRY item (its angles recovered exactly up to fp64).
+    Candidate runs are found with vectorised scans (2.7e8-row QCrank tensors)."""
     gt = np.asarray(gate_type, dtype=np.int32).reshape(-1, 3)
     gp = np.asarray(gate_param, dtype=np.float64).reshape(-1)
-    items, i, last = [], 0, 0
-    while i < gt.shape[0]:
-        hit = _match_block(gt, gp, i, min_addr) if gt[i, 0] == GateKind.RY else None
-        if hit is None:
-            i += 1
+    items, last = [], 0
+    for start, pairs in _pair_runs(gt, 1 << min_addr):
+        if start < last:
             continue
-        end, seg = hit
-        if i > last:
-            items.append(("gates", gt[last:i], gp[last:i]))
-        items.append(("ucry", seg))
-        i = last = end
-    if last < gt.shape[0]:
+        pos, left = start, pairs
+        while left >= (1 << min_addr):
+            hit = _block_at(gt, gp, pos, left, min_addr)
+            if hit is None:
+                pos, left = pos + 2, left - 1
+                continue
+            used, seg = hit
+            if pos > last:
+                items.append(("gates", gt[last:pos], gp[last:pos]))
+            items.append(("ucry", seg))
+            pos, left = pos + 2 * used, left - used
+            last = pos
+    if last < gt.shape[0] or not items:
         items.append(("gates", gt[last:], gp[last:]))
     return items
 
 
-def apply_ucry(state: sv.StateVector, addr_qubits, targets, alpha: np.ndarray) -> None:
-    """RY(alpha[a, j]) on targets[j] for every address a (one HBM pass per 5 targets)."""
+def apply_ucry(state: sv.StateVector, addr_qubits, targets, alpha) -> None:
+    """RY(alpha[a, j]) on targets[j] for every address a (one HBM pass per 5 targets).
+    alpha: (2^m, len(targets)) float64, numpy or a CUDA tensor (no host copy)."""
     amps = state.amplitudes
     n = sv._check_amps(amps)
     addr = np.ascontiguousarray(addr_qubits, dtype=np.int32)
     tg = np.ascontiguousarray(targets, dtype=np.int32)
-    alpha = np.asarray(alpha, dtype=np.float64).reshape(1 << addr.size, tg.size)
+    if not isinstance(alpha, torch.Tensor):
+        alpha = torch.from_numpy(np.ascontiguousarray(alpha, dtype=np.float64))
+    alpha = alpha.to(device=amps.device, dtype=torch.float64).reshape(1 << addr.size, tg.size)
     dt = sv._QG_DTYPE[state.precision]
     for j0 in range(0, tg.size, 5):
         tj = np.ascontiguousarray(tg[j0:j0 + 5])
-        al = torch.from_numpy(np.ascontiguousarray(alpha[:, j0:j0 + 5])).to(amps.device)
+        al = alpha[:, j0:j0 + 5].contiguous()
         ws_bytes = N.lib().qg_ucry_workspace_bytes(addr.size, tj.size, dt)
         if ws_bytes < 0:
             raise ValueError("bad UCRY register sizes")
@@ -326,10 +340,33 @@ def run_gates(gate_type: np.ndarray, gate_param: np.ndarray, n_qubits: int, opti
     return state, counts
 
 
-def simulate(angles: np.ndarray, options: sv.SimOptions | None = None):
-    """Build the QCrank circuit for an AngleTensor and run it (collapsed)."""
-    gt, gp, n = build_qcrank_circuit(angles)
-    return run_gates(gt, gp, n, options)
+def simulate(angles: np.ndarray, options: sv.SimOptions | None = None, state: sv.StateVector | None = None):
+    """Run the QCrank circuit of an AngleTensor without materialising its gate
+    arrays: H on the address register (fused pass) then the data register's
+    uniformly controlled RYs (qg_apply_ucry, 5 data qubits per pass) — the same
+    kernels run_gates uses after collapse_ucry.  `state` (optional) is a reusable
+    buffer of the right size (batched images)."""
+    options = options or sv.SimOptions()
+    if not isinstance(angles, torch.Tensor):
+        angles = np.asarray(angles, dtype=np.float64)
+    m = int(angles.shape[0]).bit_length() - 1
+    nd = angles.shape[1]
+    n = m + nd
+    sv._check_budget(n, options.precision, options.memory_budget)
+    h_t = np.array([[int(GateKind.H), -1, q] for q in range(m)], dtype=np.int32).reshape(-1, 3)
+    plan = sv.CompiledCircuit(h_t, np.zeros(m), n, options.precision, 0, options.fuse, options.tile_qubits,
+                              options.max_stages, options.max_cost)
+    if state is None:
+        state = sv.init_zero_state(n, options.precision, options.memory_budget, options.device)
+    else:
+        N.call("qg_state_init_zero", C.c_void_p(state.amplitudes.data_ptr()), n, sv._QG_DTYPE[options.precision],
+               0, sv._stream(state.amplitudes.device))
+    plan.execute(state)
+    apply_ucry(state, list(range(m)), list(range(m, n)), angles)
+    counts = None
+    if options.shots > 0:
+        counts = sv.sample_counts(state, options.shots, options.rng_seed, options.sampler)
+    return state, counts
 
 
 # ------------------------------------------------------------------ decode

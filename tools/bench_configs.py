@@ -1,0 +1,131 @@
+"""Secondary BASELINE configs (evidence for profiles/, not the driver's bench line).
+
+  python tools/bench_configs.py c1|c2|c4 [--images B]
+
+c1: random CX-block 16q x 100 blocks, complex128, 3000 shots (configs[0])
+c2: QFT 28q complex64 + 1e5 shots (configs[1])
+c4: QCrank 24 address + 8 data qubits, complex64, a batch of random images
+    (configs[3]); gate-equivalents = 24 H + 8 x 2^24 x (RY + CX).
+Each prints one JSON line: device time (CUDA events), gates/s, HBM GB/s of the
+fused / UCRY passes, and the reference CPU algorithm (oracle port, 1 core)
+timed on a bounded sample where the full config is infeasible.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import oracle
+from paper_2504_03967_b200 import qcrank as qc
+from paper_2504_03967_b200 import statevec as sv
+from paper_2504_03967_b200.generators import RandomSpec, qft_arrays, random_arrays
+
+
+def timed(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, out
+
+
+def c1():
+    gt, gp = random_arrays(RandomSpec(16, 100, 0))
+    plan = sv.CompiledCircuit(gt, gp, 16, "fp64")
+    st = sv.init_zero_state(16, "fp64")
+
+    def step():
+        sv.N.call("qg_state_init_zero", sv.C.c_void_p(st.amplitudes.data_ptr()), 16, 1, 0, sv._stream(st.amplitudes.device))
+        plan.execute(st)
+        return sv.sample_indices(st.amplitudes, 3000, 0)
+    ms, _ = timed(step, 20)
+    t0 = time.perf_counter()
+    psi = oracle.run_arrays(gt, gp, 16, gt.shape[0], "fp64")
+    oracle.sample_counts_arrays(psi, 3000, 0, "fp64")
+    ref_ms = (time.perf_counter() - t0) * 1e3
+    return {"config": "c1 random 16q x 100 blocks c128 + 3000 shots", "ms": ms, "gates_per_s": 300 / ms * 1e3,
+            "passes": plan.info["n_passes"], "cpu_ref_ms": ref_ms, "cpu_ref": "oracle port, full config, 1 core"}
+
+
+def c2():
+    n = 28
+    gt, gp = qft_arrays(n)
+    plan = sv.CompiledCircuit(gt, gp, n, "fp32")
+    st = sv.init_zero_state(n, "fp32")
+
+    def gates():
+        sv.N.call("qg_state_init_zero", sv.C.c_void_p(st.amplitudes.data_ptr()), n, 0, 0, sv._stream(st.amplitudes.device))
+        plan.execute(st)
+    ms, _ = timed(gates, 5)
+    ms_s, _ = timed(lambda: sv.sample_indices(st.amplitudes, 100000, 0), 5)
+    # analytic check: |0> -> uniform 2^-n/2
+    amp = st.amplitudes[:4096].abs().cpu().numpy()
+    err = float(np.max(np.abs(amp - 2.0 ** (-n / 2))))
+    gs, gsp = qft_arrays(22)
+    t0 = time.perf_counter()
+    oracle.run_arrays(gs, gsp, 22, gs.shape[0], "fp32")
+    dt = time.perf_counter() - t0
+    ref_gates_per_s = gs.shape[0] / dt / 2 ** (n - 22)
+    S = (1 << n) * 8
+    return {"config": "c2 QFT 28q c64 + 1e5 shots", "gate_ms": ms, "sample_ms": ms_s, "gates": int(gt.shape[0]),
+            "gates_per_s": gt.shape[0] / ms * 1e3, "passes": plan.info["n_passes"],
+            "hbm_gbs": 2 * S * plan.info["n_passes"] / ms / 1e6, "max_abs_err_vs_uniform": err,
+            "cpu_ref_gates_per_s": ref_gates_per_s,
+            "cpu_ref": f"oracle port QFT22 fp32 {dt:.2f} s, per-gate time scaled x2^{n - 22}"}
+
+
+def c4(images):
+    m, nd = 24, 8
+    n = m + nd
+    rng = np.random.default_rng(0)
+    px = rng.integers(0, 256, (1 << m) * nd, dtype=np.uint8)
+    base = qc.prepare_angles(qc.ImageGray(8192, 16384, px), m, nd)
+    t0 = time.perf_counter()
+    angles = [torch.from_numpy(np.roll(base, 977 * i, axis=0)).cuda() for i in range(images)]  # distinct images
+    torch.cuda.synchronize()
+    upload_ms = (time.perf_counter() - t0) * 1e3 / images
+    st = sv.init_zero_state(n, "fp32", 1 << 40)
+    opts = sv.SimOptions("fp32", memory_budget=1 << 40)
+
+    def batch():
+        for a in angles:
+            qc.simulate(a, opts, state=st)
+    ms, _ = timed(batch, 2)
+    per_img = ms / images
+    gate_eq = m + 2 * nd * (1 << m)
+    # exact-mode decode of the last image's first 2^12 addresses is a cheap sanity check
+    rep_ok = bool(torch.isfinite(st.amplitudes[:1024]).all().item())
+    S = (1 << n) * 8
+    passes = 4  # 2 H passes (24 address qubits, 13-qubit tiles) + 2 UCRY passes (5 + 3 data qubits)
+    # reference algorithm on the gate-level circuit at m = 8 (2 x 8 x 256 gates), scaled x2^(n - 16) per gate
+    a_s = qc.prepare_angles(qc.ImageGray(32, 64, rng.integers(0, 256, 2048, dtype=np.uint8)), 8, nd)
+    gt, gp, ns = qc.build_qcrank_circuit(a_s, measure=False)
+    t0 = time.perf_counter()
+    oracle.run_arrays(gt, gp, ns, gt.shape[0], "fp32")
+    dt = time.perf_counter() - t0
+    ref_img_s = dt / gt.shape[0] * gate_eq * 2 ** (n - ns)
+    return {"config": f"c4 QCrank 24+8 c64, batch of {images} images", "ms_per_image": per_img,
+            "angle_upload_ms_per_image": upload_ms,
+            "images_per_s": 1e3 / per_img, "gate_equivalents_per_image": gate_eq,
+            "gate_equivalents_per_s": gate_eq / per_img * 1e3, "hbm_gbs": 2 * S * passes / per_img / 1e6,
+            "finite": rep_ok, "cpu_ref_s_per_image": ref_img_s,
+            "cpu_ref": f"oracle port of the gate-level QCrank circuit at m=8 ({gt.shape[0]} gates, {dt:.1f} s), "
+                       f"per-gate time scaled to 2^{n} amplitudes and {gate_eq} gates"}
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", choices=["c1", "c2", "c4"])
+    ap.add_argument("--images", type=int, default=4)
+    a = ap.parse_args()
+    out = {"c1": c1, "c2": c2}.get(a.config, lambda: c4(a.images))()
+    print(json.dumps(out), flush=True)
