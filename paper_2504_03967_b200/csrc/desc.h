@@ -71,12 +71,10 @@ struct CoefCap<double> {
 //   fam 3 RDW, 4 RDV  + pair index (T, C)   the W / V forms of RD
 //   fam 5 PHW  + tri index (T > C)   PH with W = e_T + e_C
 //   fam 6 PH2  + tri index (T > C)   x e on logical |11> of slot bits (T, C); coef: e
-//   OC_XF      F ^= payload where the predicate holds
-//   OC_CXM     payload T | C << 4: move slot p -> p ^ (p_C) e_T (materialises part of
+//   OC_XF      (= oc_xf(RB)) F ^= payload where the predicate holds
+//   OC_CXM     (= oc_cxm(RB)) payload T | C << 4: move slot p -> p ^ (p_C) e_T (materialises part of
 //              L), F_T ^= F_C.
 enum OpFam { F_RD = 0, F_CD, F_PH, F_RDW, F_RDV, F_PHW, F_PH2 };
-constexpr uint32_t OC_XF = 0xfe;
-constexpr uint32_t OC_CXM = 0xff;
 constexpr uint32_t kNoPred = 0xff;
 
 QG_HD constexpr int oc_base(int fam, int rb) {
@@ -85,6 +83,9 @@ QG_HD constexpr int oc_base(int fam, int rb) {
                                        : 3 * rb + 2 * rb * (rb - 1) + (fam - F_PHW) * rb * (rb - 1) / 2);
 }
 QG_HD constexpr int oc_std(int fam, int rb, int t) { return oc_base(fam, rb) + t; }
+// OC_XF / OC_CXM follow the families, so every code is a jump-table index
+QG_HD constexpr uint32_t oc_xf(int rb) { return (uint32_t)(3 * rb + 3 * rb * (rb - 1)); }
+QG_HD constexpr uint32_t oc_cxm(int rb) { return oc_xf(rb) + 1; }
 QG_HD constexpr int oc_pair(int fam, int rb, int t, int c) {
     return oc_base(fam, rb) + t * (rb - 1) + (c < t ? c : c - 1);
 }

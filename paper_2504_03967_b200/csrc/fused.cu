@@ -335,14 +335,17 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
     {
         const uint32_t code = w & 0xffu;
         if constexpr (RB == 5) {
-            const uint32_t idx = code == OC_XF ? QGJ_N_5 : (code == OC_CXM ? QGJ_N_5 + 1 : code);
+            static_assert(QGJ_N_5 == oc_xf(5), "jt_lists.h out of date");
+            const uint32_t idx = code;
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_5 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
         } else if constexpr (RB == 4) {
-            const uint32_t idx = code == OC_XF ? QGJ_N_4 : (code == OC_CXM ? QGJ_N_4 + 1 : code);
+            static_assert(QGJ_N_4 == oc_xf(4), "jt_lists.h out of date");
+            const uint32_t idx = code;
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_4 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
         } else {
             static_assert(RB == 3, "jump tables exist for RB = 3, 4, 5");
-            const uint32_t idx = code == OC_XF ? QGJ_N_3 : (code == OC_CXM ? QGJ_N_3 + 1 : code);
+            static_assert(QGJ_N_3 == oc_xf(3), "jt_lists.h out of date");
+            const uint32_t idx = code;
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_3 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
         }
     }
@@ -405,13 +408,13 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
 #undef QG_PAIRT
 #undef QG_PAIR
 #undef QG_OKP
-        case OC_XF: {
+        case oc_xf(RB): {
             QGJ_ENTER("QGJ_XF");
             const uint32_t pi = (w >> 8) & 0xffu;
             if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (w >> 16) & 31u;
             break;
         }
-        case OC_CXM: {
+        case oc_cxm(RB): {
             QGJ_ENTER("QGJ_CXM");
             run_cxm<RB>(a, w, F);
             break;
@@ -696,6 +699,7 @@ cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uin
             case 1: return launch_fused_t<float, 4, 3>(P, psi, rank_bits, st);
             case 2: return launch_fused_t<float, 4, 2>(P, psi, rank_bits, st);
             case 4: return launch_fused_t<float, 5, 3, 1>(P, psi, rank_bits, st);
+            case 5: return launch_fused_t<float, 5, 4, 1>(P, psi, rank_bits, st);
             default: return launch_fused_t<float, 3, 0>(P, psi, rank_bits, st);
         }
     }

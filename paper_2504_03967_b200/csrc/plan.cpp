@@ -124,7 +124,7 @@ static int validate(const int32_t* gt, const double* gp, int64_t n_gates, int n,
 // auto choice = first entry with >= 8 qubits outside the tile; kernel_cfg (1 + id)
 // forces one (tuning)
 // (ids must match launch_fused in fused.cu; array index = id)
-static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}, {4, 5, 3}};
+static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}, {4, 5, 3}, {5, 5, 4}};
 static const KernelCfg kCfgC128[] = {{0, 4, 3}, {1, 3, 2}, {2, 3, 0}};
 // auto preference order (ids)
 static const int kAutoC64[] = {4, 1, 2, 3};
@@ -132,7 +132,7 @@ static const int kAutoC128[] = {0, 1, 2};
 
 static bool pick_cfg(int dtype, int n_local, int force_k, int force_cfg, KernelCfg& out) {
     const KernelCfg* cfgs = dtype == QG_DTYPE_C64 ? kCfgC64 : kCfgC128;
-    const int n_all = dtype == QG_DTYPE_C64 ? 5 : 3;
+    const int n_all = dtype == QG_DTYPE_C64 ? 6 : 3;
     const int* order = dtype == QG_DTYPE_C64 ? kAutoC64 : kAutoC128;
     const int nc = dtype == QG_DTYPE_C64 ? 4 : 3;
     if (force_cfg > 0) {
@@ -719,8 +719,8 @@ static uint32_t op_code(const HostOp& o, int rb) {
             return oc_std(F_CD, rb, o.t);  // complex ops only in the standard form
         case A_PH: return o.c < 0 ? oc_std(F_PH, rb, o.t) : oc_tri(F_PHW, rb, o.t, o.c);
         case A_PH2: return oc_tri(F_PH2, rb, o.t, o.c);
-        case A_CXM: return OC_CXM;
-        default: return OC_XF;
+        case A_CXM: return oc_cxm(rb);
+        default: return oc_xf(rb);
     }
 }
 
@@ -756,9 +756,9 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
         for (const HostOp& o : h.ops) {
             uint32_t w;
             if (o.kind == A_XF) {
-                w = op_word(OC_XF, pred_index(o.cmask), (uint32_t)o.t);
+                w = op_word(oc_xf(hp.cfg.rb), pred_index(o.cmask), (uint32_t)o.t);
             } else if (o.kind == A_CXM) {
-                w = op_word(OC_CXM, kNoPred, (uint32_t)(o.t | (o.c << 4)));
+                w = op_word(oc_cxm(hp.cfg.rb), kNoPred, (uint32_t)(o.t | (o.c << 4)));
             } else if (o.kind == A_PH) {
                 w = op_word(op_code(o, hp.cfg.rb), (uint32_t)o.ph.size(), (uint32_t)nph);
                 for (const auto& x : o.ph) {
