@@ -190,6 +190,10 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
                             }
                             continue;
                         }
+                        if (o.kind == qg::A_XF) {  // one row per list entry
+                            for (const auto& x : o.xf) row((int64_t)s, o.kind, (int64_t)x.second, -1, x.first, 0, m);
+                            continue;
+                        }
                         row((int64_t)s, o.kind, t, c, o.cmask, o.qmask, m);
                     }
                     for (const auto& o : st.tph) row((int64_t)s, qg::A_TPH, -1, -1, o.cmask, o.qmask, o.m);

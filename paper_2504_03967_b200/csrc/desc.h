@@ -37,6 +37,7 @@ constexpr int kMaxOps = 640;    // op words per pass
 constexpr int kMaxPred = 48;    // thread predicates (global-index masks) per pass
 constexpr int kMaxTph = 128;    // thread-phase entries per pass
 constexpr int kMaxPhe = 320;    // PH list entries per pass
+constexpr int kMaxXfe = 256;    // XF list entries per pass
 constexpr int kLaneBits = 5;
 constexpr int kMaxRegBits = 5;
 constexpr int kMaxWarpBits = 4;
@@ -71,9 +72,11 @@ struct CoefCap<double> {
 //   fam 3 RDW, 4 RDV  + pair index (T, C)   the W / V forms of RD
 //   fam 5 PHW  + tri index (T > C)   PH with W = e_T + e_C
 //   fam 6 PH2  + tri index (T > C)   x e on logical |11> of slot bits (T, C); coef: e
-//   OC_XF      (= oc_xf(RB)) F ^= payload where the predicate holds
-//   OC_CXM     (= oc_cxm(RB)) payload T | C << 4: move slot p -> p ^ (p_C) e_T (materialises part of
-//              L), F_T ^= F_C.
+//   OC_XF      (= oc_xf(RB)) a list of X gates under thread-level controls: for each
+//              entry (xfe[]: predicate index | v << 8) F ^= v where the predicate
+//              holds; word bits 8-15 = entry count, 16-31 = first entry
+//   fam 7 CXM  + pair index (T, C) (after OC_XF): move slot p -> p ^ (p_C) e_T
+//              (materialises part of L), F_T ^= F_C
 enum OpFam { F_RD = 0, F_CD, F_PH, F_RDW, F_RDV, F_PHW, F_PH2 };
 constexpr uint32_t kNoPred = 0xff;
 
@@ -83,9 +86,11 @@ QG_HD constexpr int oc_base(int fam, int rb) {
                                        : 3 * rb + 2 * rb * (rb - 1) + (fam - F_PHW) * rb * (rb - 1) / 2);
 }
 QG_HD constexpr int oc_std(int fam, int rb, int t) { return oc_base(fam, rb) + t; }
-// OC_XF / OC_CXM follow the families, so every code is a jump-table index
+// OC_XF and the CXM family follow, so every code is a jump-table index
 QG_HD constexpr uint32_t oc_xf(int rb) { return (uint32_t)(3 * rb + 3 * rb * (rb - 1)); }
-QG_HD constexpr uint32_t oc_cxm(int rb) { return oc_xf(rb) + 1; }
+QG_HD constexpr uint32_t oc_cxm(int rb, int t, int c) {
+    return oc_xf(rb) + 1 + (uint32_t)(t * (rb - 1) + (c < t ? c : c - 1));
+}
 QG_HD constexpr int oc_pair(int fam, int rb, int t, int c) {
     return oc_base(fam, rb) + t * (rb - 1) + (c < t ? c : c - 1);
 }
@@ -141,6 +146,7 @@ struct PassDesc {
     uint32_t ops[kMaxOps + 1];  // + 1: the kernel prefetches one word past a stage's list
     Entry<Real> tph[kMaxTph];
     PhEnt<Real> ph[kMaxPhe];
+    uint32_t xfe[kMaxXfe];      // OC_XF list entries: predicate index | flip vector << 8
     Real coef[CoefCap<Real>::value];
 };
 

@@ -265,28 +265,6 @@ __device__ __forceinline__ void op_ph(T2 (&a)[1 << RB], T2 e, uint32_t F) {
     }
 }
 
-// materialising register CX (OC_CXM): kept out of run_op's jump table — a body
-// that permutes registers in the same loop as the others makes the register
-// allocator copy the whole amplitude array at the loop head of every op
-template <int RB, typename T2>
-__device__ __forceinline__ void run_cxm(T2 (&a)[1 << RB], uint32_t w, uint32_t& F) {
-    const uint32_t tc = (w >> 16) & 0xffu;
-    switch (tc) {
-#define QG_CXM(T, C)                                                                     \
-    case T | (C << 4):                                                                   \
-        if constexpr (T < RB && C < RB && T != C) {                                      \
-            r_cx<RB, T, C>(a);                                                           \
-            F ^= ((F >> C) & 1u) << T;                                                   \
-        }                                                                                \
-        break;
-#define QG_CXMT(T) QG_CXM(T, 0) QG_CXM(T, 1) QG_CXM(T, 2) QG_CXM(T, 3) QG_CXM(T, 4)
-        QG_CXMT(0) QG_CXMT(1) QG_CXMT(2) QG_CXMT(3) QG_CXMT(4)
-#undef QG_CXMT
-#undef QG_CXM
-        default: break;
-    }
-}
-
 // the thread's phase of an OC_PH word: product of its list entries whose
 // predicate holds (e.g. all the CR1 gates of a QFT row sharing one register target)
 template <typename T2, typename Real>
@@ -403,6 +381,18 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
             else r_cphase_flip<RB, T, C>(a, e, ft, fc);                                  \
         }                                                                                \
         break;
+#define QG_CXM(T, C)                                                                     \
+    case QG_LAB(QG_OKP(T, C), oc_cxm(RB, T, C), 700 + 5 * T + C):                        \
+        if constexpr (QG_OKP(T, C)) {                                                    \
+            QGJ_ENTER("QGJ_CXM_" #T "_" #C);                                             \
+            r_cx<RB, T, C>(a);                                                           \
+            F ^= ((F >> C) & 1u) << T;                                                   \
+        }                                                                                \
+        break;
+#define QG_CXMT(T) QG_CXM(T, 0) QG_CXM(T, 1) QG_CXM(T, 2) QG_CXM(T, 3) QG_CXM(T, 4)
+        QG_CXMT(0) QG_CXMT(1) QG_CXMT(2) QG_CXMT(3) QG_CXMT(4)
+#undef QG_CXMT
+#undef QG_CXM
 #define QG_PAIRT(T) QG_PAIR(T, 0) QG_PAIR(T, 1) QG_PAIR(T, 2) QG_PAIR(T, 3) QG_PAIR(T, 4)
         QG_PAIRT(0) QG_PAIRT(1) QG_PAIRT(2) QG_PAIRT(3) QG_PAIRT(4)
 #undef QG_PAIRT
@@ -410,13 +400,12 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
 #undef QG_OKP
         case oc_xf(RB): {
             QGJ_ENTER("QGJ_XF");
-            const uint32_t pi = (w >> 8) & 0xffu;
-            if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (w >> 16) & 31u;
-            break;
-        }
-        case oc_cxm(RB): {
-            QGJ_ENTER("QGJ_CXM");
-            run_cxm<RB>(a, w, F);
+            const int n = (w >> 8) & 0xffu, b = w >> 16;
+            for (int k = 0; k < n; ++k) {
+                const uint32_t e = P.xfe[b + k];
+                const uint32_t pi = e & 0xffu;
+                if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (e >> 8) & 31u;
+            }
             break;
         }
         default: __builtin_unreachable();
@@ -700,6 +689,7 @@ cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uin
             case 2: return launch_fused_t<float, 4, 2>(P, psi, rank_bits, st);
             case 4: return launch_fused_t<float, 5, 3, 1>(P, psi, rank_bits, st);
             case 5: return launch_fused_t<float, 5, 4, 1>(P, psi, rank_bits, st);
+            case 6: return launch_fused_t<float, 5, 2, 1>(P, psi, rank_bits, st);
             default: return launch_fused_t<float, 3, 0>(P, psi, rank_bits, st);
         }
     }

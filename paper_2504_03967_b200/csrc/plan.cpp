@@ -124,7 +124,7 @@ static int validate(const int32_t* gt, const double* gp, int64_t n_gates, int n,
 // auto choice = first entry with >= 8 qubits outside the tile; kernel_cfg (1 + id)
 // forces one (tuning)
 // (ids must match launch_fused in fused.cu; array index = id)
-static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}, {4, 5, 3}, {5, 5, 4}};
+static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}, {4, 5, 3}, {5, 5, 4}, {6, 5, 2}};
 static const KernelCfg kCfgC128[] = {{0, 4, 3}, {1, 3, 2}, {2, 3, 0}};
 // auto preference order (ids)
 static const int kAutoC64[] = {4, 1, 2, 3};
@@ -132,7 +132,7 @@ static const int kAutoC128[] = {0, 1, 2};
 
 static bool pick_cfg(int dtype, int n_local, int force_k, int force_cfg, KernelCfg& out) {
     const KernelCfg* cfgs = dtype == QG_DTYPE_C64 ? kCfgC64 : kCfgC128;
-    const int n_all = dtype == QG_DTYPE_C64 ? 6 : 3;
+    const int n_all = dtype == QG_DTYPE_C64 ? 7 : 3;
     const int* order = dtype == QG_DTYPE_C64 ? kAutoC64 : kAutoC128;
     const int nc = dtype == QG_DTYPE_C64 ? 4 : 3;
     if (force_cfg > 0) {
@@ -373,7 +373,23 @@ struct Emitter {
         for (int r = 0; r < rb; ++r) if ((row[r] >> b) & 1u) v |= 1u << r;
         return v;
     }
+    // X gates under thread-level controls (F ^= v where pred) commute with every op
+    // that does not read the F bits they flip: queue them and emit one OC_XF list op
+    // before the first reader (or at the stage end) instead of one op each
+    std::vector<std::pair<uint64_t, uint32_t>> xq;
+    uint32_t xq_mask = 0;
+    void flush_xf() {
+        if (xq.empty()) return;
+        HostOp o{};
+        o.kind = A_XF; o.t = (int)xq[0].second; o.c = -1; o.cmask = xq[0].first; o.tq = o.cq = -1;
+        o.xf = xq;
+        hs.ops.push_back(o);
+        xq.clear();
+        xq_mask = 0;
+    }
     void push(int kind, int t, int c, uint64_t cmask = 0) {
+        const uint32_t reads = (t >= 0 ? 1u << t : 0u) | (c >= 0 ? 1u << c : 0u);
+        if (reads & xq_mask) flush_xf();
         HostOp o{};
         o.kind = kind; o.t = t; o.c = c; o.cmask = cmask;
         o.tq = (kind != A_XF && t >= 0) ? qphys(t) : -1;
@@ -517,10 +533,9 @@ struct Emitter {
                     for (int r = 0; r < rb; ++r)  // L <- L * CX(c -> t)
                         if ((row[r] >> rt) & 1u) row[r] ^= 1u << rc;
                 } else {
-                    const uint32_t v = col(rt);
-                    push(A_XF, (int)v, -1, 1ull << g.c);
-                    hs.ops.back().tq = g.t;
-                    hs.ops.back().cq = g.c;
+                    const uint32_t v = col(rt);  // slot vector now; stays valid past later lazy CX
+                    xq.emplace_back(1ull << g.c, v);
+                    xq_mask |= v;
                 }
                 break;
             }
@@ -552,6 +567,7 @@ struct Emitter {
     void finish() {
         for (size_t b = 0; b < pend.size(); ++b) flush((int)b);
         for (size_t b = 0; b < pph.size(); ++b) flush_ph((int)b);
+        flush_xf();
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         hs.out_vec.assign(rb, 0);
@@ -681,7 +697,7 @@ static int n_coef(const HostOp& o) {
 }
 
 // resource needs of a pass (descriptor capacity is checked by the scheduler)
-struct PassSize { int ops = 0, coef = 0, tph = 0, pred = 0, phe = 0; };
+struct PassSize { int ops = 0, coef = 0, tph = 0, pred = 0, phe = 0, xfe = 0; };
 static PassSize pass_size(const HostPass& hp) {
     PassSize z;
     std::vector<uint64_t> preds;
@@ -691,9 +707,9 @@ static PassSize pass_size(const HostPass& hp) {
         for (const HostOp& o : h.ops) {
             z.coef += n_coef(o);
             z.phe += (int)o.ph.size();
-            if (o.kind == A_XF && o.cmask &&
-                std::find(preds.begin(), preds.end(), o.cmask) == preds.end())
-                preds.push_back(o.cmask);
+            z.xfe += (int)o.xf.size();
+            for (const auto& x : o.xf)
+                if (x.first && std::find(preds.begin(), preds.end(), x.first) == preds.end()) preds.push_back(x.first);
         }
     }
     z.pred = (int)preds.size();
@@ -705,7 +721,7 @@ static bool fits_t(const HostPass& hp) {
     const PassSize z = pass_size(hp);
     // one thread-phase slot is kept free for the plan's global phase
     return z.ops <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph && z.pred <= kMaxPred &&
-           z.phe <= kMaxPhe;
+           z.phe <= kMaxPhe && z.xfe <= kMaxXfe;
 }
 static bool fits(int dtype, const HostPass& hp) {
     return dtype == QG_DTYPE_C64 ? fits_t<float>(hp) : fits_t<double>(hp);
@@ -719,7 +735,7 @@ static uint32_t op_code(const HostOp& o, int rb) {
             return oc_std(F_CD, rb, o.t);  // complex ops only in the standard form
         case A_PH: return o.c < 0 ? oc_std(F_PH, rb, o.t) : oc_tri(F_PHW, rb, o.t, o.c);
         case A_PH2: return oc_tri(F_PH2, rb, o.t, o.c);
-        case A_CXM: return oc_cxm(rb);
+        case A_CXM: return oc_cxm(rb, o.t, o.c);
         default: return oc_xf(rb);
     }
 }
@@ -741,7 +757,7 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
             if (std::find(hp.tile_q.begin(), hp.tile_q.end(), q) == hp.tile_q.end()) d.comp_q[nc0++] = (uint8_t)q;
     }
     fill_stage(dtype, hp, hp.io, d.stg[0]);
-    int no = 0, nc = 0, nt = 0, np = 0, nph = 0;
+    int no = 0, nc = 0, nt = 0, np = 0, nph = 0, nxf = 0;
     auto pred_index = [&](uint64_t m) -> uint32_t {
         if (!m) return kNoPred;
         for (int i = 0; i < np; ++i) if (d.pred[i] == m) return (uint32_t)i;
@@ -756,9 +772,10 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
         for (const HostOp& o : h.ops) {
             uint32_t w;
             if (o.kind == A_XF) {
-                w = op_word(oc_xf(hp.cfg.rb), pred_index(o.cmask), (uint32_t)o.t);
+                w = op_word(oc_xf(hp.cfg.rb), (uint32_t)o.xf.size(), (uint32_t)nxf);
+                for (const auto& x : o.xf) d.xfe[nxf++] = pred_index(x.first) | (x.second << 8);
             } else if (o.kind == A_CXM) {
-                w = op_word(oc_cxm(hp.cfg.rb), kNoPred, (uint32_t)(o.t | (o.c << 4)));
+                w = op_word(oc_cxm(hp.cfg.rb, o.t, o.c), kNoPred, 0);
             } else if (o.kind == A_PH) {
                 w = op_word(op_code(o, hp.cfg.rb), (uint32_t)o.ph.size(), (uint32_t)nph);
                 for (const auto& x : o.ph) {

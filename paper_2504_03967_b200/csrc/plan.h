@@ -49,6 +49,7 @@ struct HostOp {
     uint64_t cmask, qmask;  // thread predicate (all bits 1) / thread-phase select bit
     double m[8];    // A_RD: m00 m01 m10 m11; A_CD: 2x2 complex; A_PH2: e; A_TPH: v0, v1
     std::vector<std::pair<uint64_t, std::pair<double, double>>> ph;  // A_PH: (predicate, e) factors
+    std::vector<std::pair<uint64_t, uint32_t>> xf;                    // A_XF: (predicate, flip vector) list
 };
 
 struct HostStage {
