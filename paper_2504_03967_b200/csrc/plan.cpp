@@ -915,7 +915,7 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
     }
     plan.cfg = cfg;
     const int max_stages = opts.max_stages > 0 ? std::min(opts.max_stages, kMaxStages) : kMaxStages;
-    const double max_cost = opts.max_cost > 0 ? (double)opts.max_cost : 250.0;
+    const double max_cost = opts.max_cost > 0 ? (double)opts.max_cost : 350.0;
     const int c_low = n_local >= 20 ? kLaneBits : 0;  // small states live in L2: no coalescing constraint
 
     std::vector<int> phys(n), inv(n);  // logical -> physical, physical -> logical
