@@ -172,8 +172,9 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
                     row((int64_t)s, 200, (int64_t)st.reg_tile.size(), packed, 0, 0, hdr);
                     for (const auto& o : st.ops) {
                         double m[8] = {0};
-                        if (o.kind == qg::A_RD) {  // real 2x2 in complex layout
-                            m[0] = o.m[0]; m[2] = o.m[1]; m[4] = o.m[2]; m[6] = o.m[3];
+                        if (o.kind == qg::A_RD) {  // the three shears as one real 2x2, complex layout
+                            const double a = o.m[0], b = o.m[1];
+                            m[0] = 1 + a * b; m[2] = 2 * a + a * a * b; m[4] = b; m[6] = 1 + a * b;
                         } else {
                             std::memcpy(m, o.m, sizeof(m));
                         }

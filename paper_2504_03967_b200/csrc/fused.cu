@@ -141,18 +141,27 @@ __device__ __forceinline__ void p_dense(T2 (&a)[1 << RB], const Real* __restrict
     }
 }
 
-// real 2x2 (H, RY and their products): half the work of the complex case
+// rotation by shears on pairs {i, i ^ V} (x = the parity(W & i) = 0 member):
+// x += a y; y += b x; x += a y — every FMA updates its own register in place
 template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
-__device__ __forceinline__ void p_rdense(T2 (&a)[1 << RB], const Real* __restrict__ m) {
-    const Real m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
+__device__ __forceinline__ void p_rot(T2 (&a)[1 << RB], Real sa, Real sb) {
 #pragma unroll
     for (int i = 0; i < (1 << RB); ++i) {
         if (parity_c(W & (uint32_t)i)) continue;
         const int j = i ^ (int)V;
-        const T2 x = a[i], y = a[j];
-        const T2 ty = r_mul(y, m01), tx = r_mul(x, m10);
-        a[i] = r_fma(ty, x, m00);
-        a[j] = r_fma(tx, y, m11);
+        a[i] = r_fma(a[i], a[j], sa);
+    }
+#pragma unroll
+    for (int i = 0; i < (1 << RB); ++i) {
+        if (parity_c(W & (uint32_t)i)) continue;
+        const int j = i ^ (int)V;
+        a[j] = r_fma(a[j], a[i], sb);
+    }
+#pragma unroll
+    for (int i = 0; i < (1 << RB); ++i) {
+        if (parity_c(W & (uint32_t)i)) continue;
+        const int j = i ^ (int)V;
+        a[i] = r_fma(a[i], a[j], sa);
     }
 }
 
@@ -229,13 +238,13 @@ __device__ __forceinline__ bool pred_ok(uint64_t tb, uint64_t m) { return (tb & 
 
 // pair-op bodies: flip-select the coefficients (X U X when the thread's roles
 // are swapped), then run the compile-time body
+// rotation R(psi) as three in-place shears (planner: Emitter::rotation); a thread
+// whose roles are swapped sees X R X = R(-psi): both shear coefficients negate
 template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
 __device__ __forceinline__ void op_rd(T2 (&a)[1 << RB], const Real* m, uint32_t F) {
     const bool f = parity_c(W & F);
-    Real c[4];
-    c[0] = sel(f, m[3], m[0]); c[1] = sel(f, m[2], m[1]);
-    c[2] = sel(f, m[1], m[2]); c[3] = sel(f, m[0], m[3]);
-    p_rdense<RB, V, W>(a, c);
+    const Real sa = sel(f, -m[0], m[0]), sb = sel(f, -m[1], m[1]);
+    p_rot<RB, V, W>(a, sa, sb);
 }
 template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
 __device__ __forceinline__ void op_cd(T2 (&a)[1 << RB], const Real* m, uint32_t F) {

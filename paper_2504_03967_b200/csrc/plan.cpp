@@ -451,28 +451,53 @@ struct Emitter {
     }
     // 2x2 on logical b: pairs along V = L e_b, roles by W = row b of L^-1; the kernel
     // has bodies for V = W = e_T, (V = e_T, W = e_T + e_C) and (V = e_T + e_C, W = e_T)
+    // Real orthogonal 2x2 (H, RY and their products) as a rotation R(psi) run as
+    // three in-place shears (Paeth: x += a y; y += b x; x += a y with a = -tan(psi/2),
+    // b = sin psi): 3 FMAs per pair instead of 4.  det -1: M = Z R(psi), the Z is
+    // queued as a phase (usually merging with later phases on the qubit); psi is
+    // folded into [-pi/2, pi/2] with R(psi + pi) = -R(psi) (sign -> global phase).
+    bool rotation(const M2& m, double& a, double& bb, bool& refl) {
+        const double m00 = m.a00.real(), m01 = m.a01.real(), m10 = m.a10.real(), m11 = m.a11.real();
+        const double det = m00 * m11 - m01 * m10;
+        refl = det < 0;
+        // R = Z M when det = -1 (row 1 negated)
+        const double r00 = m00, r01 = m01, r10 = refl ? -m10 : m10, r11 = refl ? -m11 : m11;
+        double psi = std::atan2(r10, r00);
+        const double c = std::cos(psi), s = std::sin(psi);
+        const double e = std::fabs(c - r00) + std::fabs(s - r10) + std::fabs(-s - r01) + std::fabs(c - r11);
+        if (e > 1e-12) return false;  // not orthogonal (never for products of H / RY)
+        if (psi > M_PI / 2) { psi -= M_PI; gphase = -gphase; }
+        else if (psi < -M_PI / 2) { psi += M_PI; gphase = -gphase; }
+        a = -std::tan(psi / 2);
+        bb = std::sin(psi);
+        return true;
+    }
     void emit_dense(int b, const M2& m) {
         flush_ph(b);
+        double ra = 0, rb_ = 0;
+        bool refl = false;
+        const bool rot = m_real(m) && rotation(m, ra, rb_, refl);
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         uint32_t v = col(b), w = inv[b];
         int t = -1, c = -1;
         if (unit(v) >= 0 && v == w) {
             t = unit(v);
-        } else if (unit(v) >= 0 && two(w) && (w & v) && m_real(m)) {  // (no complex W/V bodies)
+        } else if (unit(v) >= 0 && two(w) && (w & v) && rot) {  // (no complex W/V bodies)
             t = unit(v); c = unit(w & ~v);
-        } else if (unit(w) >= 0 && two(v) && (w & v) && m_real(m)) {
+        } else if (unit(w) >= 0 && two(v) && (w & v) && rot) {
             t = unit(w); c = unit(v & ~w);
         } else {
             materialise();
             t = b; v = w = 1u << b;
         }
-        push(m_real(m) ? A_RD : A_CD, t, c);
+        push(rot ? A_RD : A_CD, t, c);
         HostOp& o = hs.ops.back();
         o.form = c < 0 ? 0 : (v == (1u << t) ? 1 : 2);
-        if (m_real(m)) {
-            double* d = o.m;
-            d[0] = m.a00.real(); d[1] = m.a01.real(); d[2] = m.a10.real(); d[3] = m.a11.real();
+        if (rot) {
+            o.m[0] = ra;
+            o.m[1] = rb_;
+            if (refl) pph[b].emplace_back(0, cd(-1, 0));  // Z after the rotation
         } else {
             put(o.m, m);
         }
@@ -689,7 +714,7 @@ static void put_entry(Entry<Real>& e, const HostOp& o) {
 
 static int n_coef(const HostOp& o) {
     switch (o.kind) {
-        case A_RD: return 4;
+        case A_RD: return 2;
         case A_CD: return 8;
         case A_PH2: return 2;
         default: return 0;
