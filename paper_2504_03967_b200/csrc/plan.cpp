@@ -345,13 +345,15 @@ struct Emitter {
     std::vector<int> reg_of;  // physical qubit -> logical register bit or -1
     uint32_t row[kMaxRegBits];  // L as rows over logical bits
     std::vector<std::vector<M2>> pend;  // per logical bit: factors in application order
-    // per logical bit: pending phases on its |1> (predicate, e), applied as ONE
-    // OC_PH op; they commute with everything but non-diagonal actions on the bit
-    std::vector<std::vector<std::pair<uint64_t, cd>>> pph;
+    // pending phases in SLOT coordinates, grouped by role vector W (one or two slot
+    // bits): entries (predicate, e) applied as ONE OC_PH op.  Lazy register CX gates
+    // move no data, so a queued phase survives them; a group is emitted only before
+    // an op that does not commute with it (pair vector or flip vector v with
+    // parity(W & v) = 1, or a CXM move) or at the stage end.
+    std::vector<std::pair<uint32_t, std::vector<std::pair<uint64_t, cd>>>> sq;
     int n_cxm = 0;
     Emitter(HostStage& h, const std::vector<int>& tq, int n, int rb_, cd& gp)
-        : hs(h), tile_q(tq), rb(rb_), gphase(gp), reg_of(n, -1), pend(h.reg_tile.size()),
-          pph(h.reg_tile.size()) {
+        : hs(h), tile_q(tq), rb(rb_), gphase(gp), reg_of(n, -1), pend(h.reg_tile.size()) {
         for (size_t b = 0; b < hs.reg_tile.size(); ++b) reg_of[tile_q[hs.reg_tile[b]]] = (int)b;
         for (int r = 0; r < kMaxRegBits; ++r) row[r] = 1u << r;
     }
@@ -397,6 +399,7 @@ struct Emitter {
         hs.ops.push_back(o);
     }
     void materialise() {  // emit CXM row operations reducing L to the identity
+        flush_phases(~0u);  // CXM moves data: queued phases go first
         for (int j = 0; j < rb; ++j) {
             if (!((row[j] >> j) & 1u)) {
                 int i = j + 1;
@@ -422,28 +425,41 @@ struct Emitter {
         if (t < 0) { materialise(); t = b; }
         return t;
     }
+    static bool odd(uint32_t x) { return __builtin_popcount(x) & 1; }
     // phase e on logical |1> of b (where the thread predicate cmask holds): queued
+    // under its slot role vector W = row b of L^-1
     void emit_phase(int b, cd e, uint64_t cmask) {
         if (e == cd(1)) return;
-        pph[b].emplace_back(cmask, e);
-    }
-    // one OC_PH op for b's queued phases; role vector W = row b of L^-1 (1 or 2 slot bits)
-    void flush_ph(int b) {
-        if (pph[b].empty()) return;
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         uint32_t w = inv[b];
         if (unit(w) < 0 && !two(w)) { materialise(); w = 1u << b; }
+        for (auto& g : sq)
+            if (g.first == w) { g.second.emplace_back(cmask, e); return; }
+        sq.push_back({w, {{cmask, e}}});
+    }
+    void emit_group(const std::pair<uint32_t, std::vector<std::pair<uint64_t, cd>>>& g) {
+        const uint32_t w = g.first;
         if (unit(w) >= 0) push(A_PH, unit(w), -1);
         else push(A_PH, 31 - __builtin_clz(w), __builtin_ctz(w));  // W form, T > C
         HostOp& o = hs.ops.back();
-        // merge the unconditional factors into one
-        cd e0(1, 0);
-        for (const auto& x : pph[b]) if (!x.first) e0 *= x.second;
+        cd e0(1, 0);  // the unconditional factors merged into entry 0
+        for (const auto& x : g.second) if (!x.first) e0 *= x.second;
         o.ph.push_back({0, {e0.real(), e0.imag()}});
-        for (const auto& x : pph[b])
+        for (const auto& x : g.second)
             if (x.first) o.ph.push_back({x.first, {x.second.real(), x.second.imag()}});
-        pph[b].clear();
+    }
+    // emit the queued groups that do not commute with an op on slot vector v
+    // (v = ~0: all of them), in queue order
+    void flush_phases(uint32_t v) {
+        std::vector<std::pair<uint32_t, std::vector<std::pair<uint64_t, cd>>>> keep;
+        auto groups = std::move(sq);
+        sq.clear();
+        for (auto& g : groups) {
+            if (v == ~0u || odd(g.first & v)) emit_group(g);
+            else keep.push_back(std::move(g));
+        }
+        sq = std::move(keep);
     }
     void emit_diag(int b, const M2& m) {  // diag(d0, d1) = d0 * diag(1, d1 / d0)
         if (m.a00 != cd(1)) gphase *= m.a00;
@@ -473,7 +489,6 @@ struct Emitter {
         return true;
     }
     void emit_dense(int b, const M2& m) {
-        flush_ph(b);
         double ra = 0, rb_ = 0;
         bool refl = false;
         const bool rot = m_real(m) && rotation(m, ra, rb_, refl);
@@ -491,13 +506,14 @@ struct Emitter {
             materialise();
             t = b; v = w = 1u << b;
         }
+        flush_phases(v);  // phases acting on these pairs' members differently go first
         push(rot ? A_RD : A_CD, t, c);
         HostOp& o = hs.ops.back();
         o.form = c < 0 ? 0 : (v == (1u << t) ? 1 : 2);
         if (rot) {
             o.m[0] = ra;
             o.m[1] = rb_;
-            if (refl) pph[b].emplace_back(0, cd(-1, 0));  // Z after the rotation
+            if (refl) emit_phase(b, cd(-1, 0), 0);  // Z after the rotation
         } else {
             put(o.m, m);
         }
@@ -540,7 +556,6 @@ struct Emitter {
         const int rt = reg_of[g.t];
         switch (g.kind) {
             case K_H: case K_RX: case K_RY:
-                if (!pph[rt].empty()) { flush(rt); flush_ph(rt); }  // queued phases act first
                 pend[rt].push_back(gate_matrix(g.kind, g.p));
                 break;
             case K_RZ: {
@@ -551,7 +566,6 @@ struct Emitter {
             }
             case K_CX: {
                 flush(rt);
-                flush_ph(rt);
                 const int rc = reg_of[g.c];
                 if (rc >= 0) {
                     flush_nondiag(rc);
@@ -559,6 +573,7 @@ struct Emitter {
                         if ((row[r] >> rt) & 1u) row[r] ^= 1u << rc;
                 } else {
                     const uint32_t v = col(rt);  // slot vector now; stays valid past later lazy CX
+                    flush_phases(v);
                     xq.emplace_back(1ull << g.c, v);
                     xq_mask |= v;
                 }
@@ -591,7 +606,7 @@ struct Emitter {
     }
     void finish() {
         for (size_t b = 0; b < pend.size(); ++b) flush((int)b);
-        for (size_t b = 0; b < pph.size(); ++b) flush_ph((int)b);
+        flush_phases(~0u);
         flush_xf();
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
