@@ -570,6 +570,22 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
                 a[gray_c(j)] = __ldcs(psi + g);
             }
         }
+        {  // warm L2 with this CTA's next tile while this one computes: each of the
+           // first R lanes prefetches one 32-amplitude run (2-4 lines, no registers held)
+            const uint64_t nt = tile + gridDim.x;
+            if (nt < P.n_tiles && lane < R) {
+                const StageDesc& S = P.stg[li];
+                uint64_t g = tbase[nt & 255] | tbase[256 + ((nt >> 8) & 255)] | tbase[512 + ((nt >> 16) & 255)] |
+                             tbase[768 + ((nt >> 24) & 255)] | tmg[li * kMapG + 32 + warp];
+#pragma unroll
+                for (int b = 0; b < RB; ++b)
+                    if ((lane >> b) & 1) g |= 1ull << S.reg_q[b];
+                const char* p = reinterpret_cast<const char*>(psi + g);
+#pragma unroll
+                for (int l = 0; l < (int)(32 * sizeof(T2)) / 128; ++l)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128 * l));
+            }
+        }
         int cur = li;
         uint32_t F = 0;  // register flip mask (see run_round)
         for (int s = 1; s <= ns; ++s) {
