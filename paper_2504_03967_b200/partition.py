@@ -86,29 +86,43 @@ def remap_local(shards: list[torch.Tensor], n_local: int, global_pos, local_pos)
             t[j * blk:(j + 1) * blk].copy_(old[peer][own * blk:(own + 1) * blk])
 
 
+REMAP_CHUNK_BYTES = 1 << 30  # per peer and round: bounds the staging memory (37 q / 8 ranks = 128 GiB shards)
+
+
 def remap_dist(shard: torch.Tensor, n_local: int, global_pos, local_pos, rank: int, group=None,
-               staging: torch.Tensor | None = None) -> int:
-    """torch.distributed remap of this rank's shard; returns the number of sends."""
+               staging: torch.Tensor | None = None, chunk_bytes: int = REMAP_CHUNK_BYTES) -> int:
+    """torch.distributed remap of this rank's shard; returns the number of sends.
+
+    Block j of this shard goes to the rank whose swapped bits equal j and comes
+    back from it (an all-to-all within the group of 2^s ranks sharing the other
+    rank bits).  The exchange runs in rounds of at most `chunk_bytes` per peer
+    through a staging buffer of (2^s - 1) chunks, so a 128 GiB shard needs
+    ~7 GiB of staging, not another 112 GiB."""
     import torch.distributed as dist
 
     s = len(global_pos)
     blk = 1 << (n_local - s)
     own, peers = remap_peers(rank, n_local, global_pos, local_pos)
-    need = len(peers) * blk
+    if not peers:
+        return 0
+    chunk = max(1, min(blk, chunk_bytes // shard.element_size()))
+    need = len(peers) * chunk
     if staging is None or staging.numel() < need or staging.dtype != shard.dtype:
         staging = torch.empty(need, dtype=shard.dtype, device=shard.device)
+
     def wire(t: torch.Tensor) -> torch.Tensor:  # complex blocks travel as (re, im) pairs
         return torch.view_as_real(t) if t.is_complex() else t
 
-    ops = []
-    for k, (j, peer) in enumerate(peers):
-        ops.append(dist.P2POp(dist.isend, wire(shard[j * blk:(j + 1) * blk]), peer, group=group))
-        ops.append(dist.P2POp(dist.irecv, wire(staging[k * blk:(k + 1) * blk]), peer, group=group))
-    if ops:
+    for off in range(0, blk, chunk):
+        n = min(chunk, blk - off)
+        ops = []
+        for k, (j, peer) in enumerate(peers):
+            ops.append(dist.P2POp(dist.isend, wire(shard[j * blk + off:j * blk + off + n]), peer, group=group))
+            ops.append(dist.P2POp(dist.irecv, wire(staging[k * chunk:k * chunk + n]), peer, group=group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-    for k, (j, _) in enumerate(peers):
-        shard[j * blk:(j + 1) * blk].copy_(staging[k * blk:(k + 1) * blk])
+        for k, (j, _) in enumerate(peers):
+            shard[j * blk + off:j * blk + off + n].copy_(staging[k * chunk:k * chunk + n])
     return len(peers)
 
 

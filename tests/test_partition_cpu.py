@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, remaps, full, out):
+def _worker(rank, world, port, n, remaps, full, out, chunk_bytes=pt.REMAP_CHUNK_BYTES):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -29,18 +29,18 @@ def _worker(rank, world, port, n, remaps, full, out):
     shard = full[rank << n_local:(rank + 1) << n_local].clone()
     sends = 0
     for gpos, lpos in remaps:
-        sends += pt.remap_dist(shard, n_local, gpos, lpos, rank)
+        sends += pt.remap_dist(shard, n_local, gpos, lpos, rank, chunk_bytes=chunk_bytes)
     out[rank] = (shard.numpy().copy(), sends)
     dist.destroy_process_group()
 
 
-def _run(world, n, remaps):
+def _run(world, n, remaps, chunk_bytes=pt.REMAP_CHUNK_BYTES):
     g = torch.Generator().manual_seed(7)
     full = torch.complex(torch.randn(1 << n, generator=g, dtype=torch.float64),
                          torch.randn(1 << n, generator=g, dtype=torch.float64))
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), n, remaps, full, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n, remaps, full, out, chunk_bytes), nprocs=world, join=True)
     n_local = n - (world.bit_length() - 1)
     shards = [full[r << n_local:(r + 1) << n_local].clone() for r in range(world)]
     for gpos, lpos in remaps:
@@ -48,12 +48,13 @@ def _run(world, n, remaps):
     return [out[r] for r in range(world)], shards
 
 
-@pytest.mark.parametrize("world,n,remaps", [
-    (2, 6, [([5], [4])]),
-    (4, 7, [([6], [4]), ([5, 6], [3, 4]), ([5], [4])]),
+@pytest.mark.parametrize("world,n,remaps,chunk_bytes", [
+    (2, 6, [([5], [4])], pt.REMAP_CHUNK_BYTES),
+    (4, 7, [([6], [4]), ([5, 6], [3, 4]), ([5], [4])], pt.REMAP_CHUNK_BYTES),
+    (4, 7, [([5, 6], [3, 4]), ([6], [4])], 48),   # several exchange rounds per block (3 x 16 B chunks)
 ])
-def test_gloo_remap_equals_local(world, n, remaps):
-    got, ref = _run(world, n, remaps)
+def test_gloo_remap_equals_local(world, n, remaps, chunk_bytes):
+    got, ref = _run(world, n, remaps, chunk_bytes)
     for r in range(world):
         assert np.array_equal(got[r][0], ref[r].numpy())
         assert got[r][1] == sum((1 << len(gp)) - 1 for gp, _ in remaps)
