@@ -137,6 +137,8 @@ struct PassDesc {
     int32_t k;             // tile qubits
     int32_t load_direct;   // 1: load with stage 0 mapping; 0: load with stg[0] (io) then transpose
     int32_t store_direct;  // 1: store from the last stage; 0: transpose to io then store
+    int32_t tile_lo32;     // 1: every tile qubit < 32 (32-bit in-tile addressing)
+    int32_t pad0;
     uint64_t n_tiles;      // 2^(n_local - k)
     uint8_t tile_q[kMaxTile];  // sorted physical positions of the tile bits
     uint8_t comp_q[48];        // local positions outside the tile, ascending (tile id bits)

@@ -561,13 +561,25 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
     for (uint64_t tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
         const uint64_t base = tbase[tile & 255] | tbase[256 + ((tile >> 8) & 255)] |
                               tbase[512 + ((tile >> 16) & 255)] | tbase[768 + ((tile >> 24) & 255)];
-        {  // global load, Gray-code order over the register index
+        // the tile's amplitudes: pt[o], pt = psi + (the tile-id bits), o = the tile
+        // bits; when every tile bit is below 32 (P.tile_lo32) the per-amplitude
+        // address walk is 32-bit (1 LOP3 + 1 IMAD.WIDE instead of 64-bit XOR + LEA pair)
+        T2* __restrict__ pt = psi + base;
+        if (P.tile_lo32) {  // global load, Gray-code order over the register index
             const StageDesc& S = P.stg[li];
-            uint64_t g = base | tgb(li);
+            uint32_t o = (uint32_t)tgb(li);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                if (j) o ^= 1u << S.reg_q[ctz_c(j)];
+                a[gray_c(j)] = __ldcs(pt + o);
+            }
+        } else {
+            const StageDesc& S = P.stg[li];
+            uint64_t g = tgb(li);
 #pragma unroll
             for (int j = 0; j < R; ++j) {
                 if (j) g ^= 1ull << S.reg_q[ctz_c(j)];
-                a[gray_c(j)] = __ldcs(psi + g);
+                a[gray_c(j)] = __ldcs(pt + g);
             }
         }
         {  // warm L2 with this CTA's next tile while this one computes: each of the
@@ -626,19 +638,33 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 :
             if (NBUF == 2) buf ^= buf_bytes;
             F = 0;
         }
-        {  // global store through the output mapping (deferred CX + flips folded in)
+        if (P.tile_lo32) {  // global store through the output mapping (CX map + flips folded in)
+            const StageDesc& S = P.stg[si];
+            uint32_t og[RB];
+#pragma unroll
+            for (int b = 0; b < RB; ++b) og[b] = (uint32_t)S.out_g[b];
+            uint32_t o = (uint32_t)tgb(si);
+#pragma unroll
+            for (int b = 0; b < RB; ++b)
+                if ((F >> b) & 1u) o ^= og[b];
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                if (j) o ^= og[ctz_c(j)];
+                __stcs(pt + o, a[gray_c(j)]);
+            }
+        } else {
             const StageDesc& S = P.stg[si];
             uint64_t og[RB];
 #pragma unroll
             for (int b = 0; b < RB; ++b) og[b] = S.out_g[b];
-            uint64_t g = base | tgb(si);
+            uint64_t g = tgb(si);
 #pragma unroll
             for (int b = 0; b < RB; ++b)
                 if ((F >> b) & 1u) g ^= og[b];
 #pragma unroll
             for (int j = 0; j < R; ++j) {
                 if (j) g ^= og[ctz_c(j)];
-                __stcs(psi + g, a[gray_c(j)]);
+                __stcs(pt + g, a[gray_c(j)]);
             }
         }
     }

@@ -791,6 +791,7 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
     d.store_direct = hp.store_direct;
     d.n_tiles = 1ull << (n_local - d.k);
     for (int i = 0; i < d.k; ++i) d.tile_q[i] = (uint8_t)hp.tile_q[i];
+    d.tile_lo32 = hp.tile_q.empty() || hp.tile_q.back() < 32 ? 1 : 0;  // tile_q is sorted
     {
         int nc0 = 0;
         for (int q = 0; q < n_local; ++q)
