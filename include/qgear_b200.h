@@ -122,7 +122,7 @@ int qg_plan_get_final_map(const qg_plan* plan, int32_t* phys_of_logical);
  *   where slot bit c = 1), 4 PH2 (phase on |11> of slot bits t, c), 5 XF (flip
  *   vector t where cmask holds), 6 TPH (thread phase v0 / v1 by qmask, where cmask
  *   holds), 100/101 single-gate kernel (GateOp kind 0/1), 200 stage header
- *   (t = register bits, c = packed out vectors 5 bits each, mats row = physical
+ *   (t = register bits, c = packed out vectors 6 bits each, mats row = physical
  *   qubit of each register bit).
  * Call with NULL buffers to get the counts. */
 int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* mats, int64_t* n_mats);

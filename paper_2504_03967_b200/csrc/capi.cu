@@ -167,7 +167,7 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
                     int64_t packed = 0;
                     for (size_t b = 0; b < st.reg_tile.size(); ++b) {
                         hdr[b] = hp.tile_q[st.reg_tile[b]];
-                        packed |= (int64_t)st.out_vec[b] << (5 * b);
+                        packed |= (int64_t)st.out_vec[b] << (6 * b);
                     }
                     row((int64_t)s, 200, (int64_t)st.reg_tile.size(), packed, 0, 0, hdr);
                     for (const auto& o : st.ops) {

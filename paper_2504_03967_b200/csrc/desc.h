@@ -39,7 +39,7 @@ constexpr int kMaxTph = 128;    // thread-phase entries per pass
 constexpr int kMaxPhe = 320;    // PH list entries per pass
 constexpr int kMaxXfe = 256;    // XF list entries per pass
 constexpr int kLaneBits = 5;
-constexpr int kMaxRegBits = 5;
+constexpr int kMaxRegBits = 6;
 constexpr int kMaxWarpBits = 4;
 constexpr int kMaxTile = 16;
 template <typename Real>

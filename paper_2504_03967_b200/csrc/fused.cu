@@ -109,9 +109,10 @@ __device__ __forceinline__ T2 cmul(T2 a, T2 b) {
     return c_mul(a, b.x, b.y);
 }
 
-__host__ __device__ constexpr int ctz_c(int x) {  // x in 1..31 (unrolled loop constant)
-    return (x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : (x & 8) ? 3 : 4;
+__host__ __device__ constexpr int ctz_c(int x) {  // x in 1..63 (unrolled loop constant)
+    return (x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : (x & 8) ? 3 : (x & 16) ? 4 : 5;
 }
+static_assert(ctz_c(32) == 5 && ctz_c(48) == 4 && ctz_c(8) == 3, "ctz_c");
 __host__ __device__ constexpr int gray_c(int x) { return x ^ (x >> 1); }
 
 // ----------------------------------------------------------------- register ops
@@ -321,7 +322,11 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
 #ifdef QG_JT
     {
         const uint32_t code = w & 0xffu;
-        if constexpr (RB == 5) {
+        if constexpr (RB == 6) {
+            static_assert(QGJ_N_6 == oc_xf(6), "jt_lists.h out of date");
+            const uint32_t idx = code;
+            asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_6 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
+        } else if constexpr (RB == 5) {
             static_assert(QGJ_N_5 == oc_xf(5), "jt_lists.h out of date");
             const uint32_t idx = code;
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_5 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
@@ -330,7 +335,7 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
             const uint32_t idx = code;
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_4 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
         } else {
-            static_assert(RB == 3, "jump tables exist for RB = 3, 4, 5");
+            static_assert(RB == 3, "jump tables exist for RB = 3, 4, 5, 6");
             static_assert(QGJ_N_3 == oc_xf(3), "jt_lists.h out of date");
             const uint32_t idx = code;
             asm volatile("{\n\tQGJ_TBL: .branchtargets " QGJ_LIST_3 ";\n\tbrx.idx %0, QGJ_TBL;\n\t}" ::"r"(idx));
@@ -357,29 +362,29 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
             op_ph<RB, 1u << T, T2, Real>(a, ph_product<T2>(P, w, tb), F);                \
         }                                                                                \
         break;
-        QG_STD(0) QG_STD(1) QG_STD(2) QG_STD(3) QG_STD(4)
+        QG_STD(0) QG_STD(1) QG_STD(2) QG_STD(3) QG_STD(4) QG_STD(5)
 #undef QG_STD
 #define QG_OKP(T, C) (T < RB && C < RB && T != C)
 #define QG_PAIR(T, C)                                                                    \
-    case QG_LAB(QG_OKP(T, C), oc_pair(F_RDW, RB, T, C), 100 + 5 * T + C):                \
+    case QG_LAB(QG_OKP(T, C), oc_pair(F_RDW, RB, T, C), 100 + 6 * T + C):                \
         if constexpr (QG_OKP(T, C)) {                                                    \
             QGJ_ENTER("QGJ_RDW_" #T "_" #C);                                             \
             op_rd<RB, 1u << T, (1u << T) | (1u << C)>(a, P.coef + (w >> 16), F);         \
         }                                                                                \
         break;                                                                           \
-    case QG_LAB(QG_OKP(T, C), oc_pair(F_RDV, RB, T, C), 200 + 5 * T + C):                \
+    case QG_LAB(QG_OKP(T, C), oc_pair(F_RDV, RB, T, C), 200 + 6 * T + C):                \
         if constexpr (QG_OKP(T, C)) {                                                    \
             QGJ_ENTER("QGJ_RDV_" #T "_" #C);                                             \
             op_rd<RB, (1u << T) | (1u << C), 1u << T>(a, P.coef + (w >> 16), F);         \
         }                                                                                \
         break;                                                                           \
-    case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PHW, RB, T, C), 500 + 5 * T + C):        \
+    case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PHW, RB, T, C), 500 + 6 * T + C):        \
         if constexpr (QG_OKP(T, C) && C < T) {                                           \
             QGJ_ENTER("QGJ_PHW_" #T "_" #C);                                             \
             op_ph<RB, (1u << T) | (1u << C), T2, Real>(a, ph_product<T2>(P, w, tb), F);  \
         }                                                                                \
         break;                                                                           \
-    case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PH2, RB, T, C), 600 + 5 * T + C):        \
+    case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PH2, RB, T, C), 600 + 6 * T + C):        \
         if constexpr (QG_OKP(T, C) && C < T) {                                           \
             QGJ_ENTER("QGJ_PH2_" #T "_" #C);                                             \
             const Real* m = P.coef + (w >> 16);                                          \
@@ -391,19 +396,19 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
         }                                                                                \
         break;
 #define QG_CXM(T, C)                                                                     \
-    case QG_LAB(QG_OKP(T, C), oc_cxm(RB, T, C), 700 + 5 * T + C):                        \
+    case QG_LAB(QG_OKP(T, C), oc_cxm(RB, T, C), 700 + 6 * T + C):                        \
         if constexpr (QG_OKP(T, C)) {                                                    \
             QGJ_ENTER("QGJ_CXM_" #T "_" #C);                                             \
             r_cx<RB, T, C>(a);                                                           \
             F ^= ((F >> C) & 1u) << T;                                                   \
         }                                                                                \
         break;
-#define QG_CXMT(T) QG_CXM(T, 0) QG_CXM(T, 1) QG_CXM(T, 2) QG_CXM(T, 3) QG_CXM(T, 4)
-        QG_CXMT(0) QG_CXMT(1) QG_CXMT(2) QG_CXMT(3) QG_CXMT(4)
+#define QG_CXMT(T) QG_CXM(T, 0) QG_CXM(T, 1) QG_CXM(T, 2) QG_CXM(T, 3) QG_CXM(T, 4) QG_CXM(T, 5)
+        QG_CXMT(0) QG_CXMT(1) QG_CXMT(2) QG_CXMT(3) QG_CXMT(4) QG_CXMT(5)
 #undef QG_CXMT
 #undef QG_CXM
-#define QG_PAIRT(T) QG_PAIR(T, 0) QG_PAIR(T, 1) QG_PAIR(T, 2) QG_PAIR(T, 3) QG_PAIR(T, 4)
-        QG_PAIRT(0) QG_PAIRT(1) QG_PAIRT(2) QG_PAIRT(3) QG_PAIRT(4)
+#define QG_PAIRT(T) QG_PAIR(T, 0) QG_PAIR(T, 1) QG_PAIR(T, 2) QG_PAIR(T, 3) QG_PAIR(T, 4) QG_PAIR(T, 5)
+        QG_PAIRT(0) QG_PAIRT(1) QG_PAIRT(2) QG_PAIRT(3) QG_PAIRT(4) QG_PAIRT(5)
 #undef QG_PAIRT
 #undef QG_PAIR
 #undef QG_OKP
@@ -413,7 +418,7 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
             for (int k = 0; k < n; ++k) {
                 const uint32_t e = P.xfe[b + k];
                 const uint32_t pi = e & 0xffu;
-                if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (e >> 8) & 31u;
+                if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (e >> 8) & 63u;
             }
             break;
         }
@@ -506,7 +511,7 @@ __host__ __device__ constexpr size_t tables_bytes() {
 // NBUF = 1: one buffer, a second barrier before it is rewritten (half the SMEM,
 // so two CTAs fit on an SM)
 template <typename Real, int RB, int WB, int NBUF>
-__global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8) ? 1 : 2)
+__global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB >= 6) ? 1 : 2)
     fused_pass_kernel(const __grid_constant__ PassDesc<Real> P, typename V2<Real>::T* __restrict__ psi,
                       uint64_t rank_bits) {
     using T2 = typename V2<Real>::T;
@@ -741,6 +746,7 @@ cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uin
             case 4: return launch_fused_t<float, 5, 3, 1>(P, psi, rank_bits, st);
             case 5: return launch_fused_t<float, 5, 4, 1>(P, psi, rank_bits, st);
             case 6: return launch_fused_t<float, 5, 2, 1>(P, psi, rank_bits, st);
+            case 7: return launch_fused_t<float, 6, 3, 1>(P, psi, rank_bits, st);
             default: return launch_fused_t<float, 3, 0>(P, psi, rank_bits, st);
         }
     }

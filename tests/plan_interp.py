@@ -60,7 +60,7 @@ class _Stage:
     def _par(x):
         x = np.asarray(x, dtype=np.int64)
         r = np.zeros_like(x)
-        for b in range(6):
+        for b in range(8):
             r ^= (x >> b) & 1
         return r
 
@@ -137,7 +137,7 @@ def run_program(plan, dtype=np.complex128) -> np.ndarray:
             last_pass = p
         if kind == STAGE:
             reg_q = [int(m[b]) for b in range(t)]
-            out_vec = [(c >> (5 * j)) & 31 for j in range(t)]
+            out_vec = [(c >> (6 * j)) & 63 for j in range(t)]
             st = _Stage(psi, n, reg_q, out_vec, dtype)
             continue
         cx = lambda k: complex(m[2 * k], m[2 * k + 1])  # noqa: E731

@@ -274,3 +274,15 @@ def test_sampler_edge_cases():
     sv.apply_1q(st, GateKind.H, 16)
     t = sv.sample_counts(st, 50000, 1)
     assert set(t.indices.tolist()) <= {0, 1 << 16}
+
+# every fused-kernel instantiation (kernel_cfg = 1 + id; c64: 8 configs incl. the
+# 32/64-amplitude-per-thread ones, c128: 3) against the oracle on a mixed circuit
+@pytest.mark.parametrize("precision,cfg", [("fp32", c) for c in range(1, 9)] + [("fp64", c) for c in range(1, 4)])
+def test_every_kernel_config_vs_oracle(precision, cfg):
+    n = 17
+    gt, gp = mixed(n, 500, 30 + cfg)
+    ref = oracle.run_arrays(gt, gp, n, gt.shape[0], "fp64")
+    plan = sv.CompiledCircuit(gt, gp, n, precision, kernel_cfg=cfg)
+    st = sv.init_zero_state(n, precision)
+    plan.execute(st)
+    assert rel_l2(st.to_numpy(), ref) < (1e-12 if precision == "fp64" else 1e-5)
