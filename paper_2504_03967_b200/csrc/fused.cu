@@ -7,9 +7,14 @@
 //   tile   = 2^k amplitudes sharing all index bits outside the pass's tile
 //            qubits (desc.tile_q); the 5 lowest tile bits are the lane bits of
 //            the io mapping, so global loads/stores are >= 256 B contiguous.
-//   thread = 2^RB amplitudes in registers; a register stage applies every op
-//            whose target is a register bit with straight-line FMA code
-//            (switch over the runtime bit -> compile-time-unrolled body).
+//   thread = 2^RB amplitudes in registers ("slots"); a register stage runs its
+//            op list (desc.h): each 32-bit op word is dispatched through a PTX
+//            jump table to a body whose slot bits are compile-time constants,
+//            so the slot array is only indexed by constants (straight-line
+//            packed-f32x2 FMA code).
+//   lazy CX = register CX gates never touch data: the planner tracks the GF(2)
+//            map L (slot p holds logical index L^-1 (p ^ F)) and the transpose /
+//            store addresses apply it at the stage end.
 //   stage switch = one SMEM round trip with a linear XOR swizzle
 //            (conflict-free lanes chosen by the planner).
 //   controls / diagonal phases on non-register qubits = per-thread predicates
@@ -77,7 +82,6 @@ __device__ __forceinline__ float2 c_mul(float2 x, float mr, float mi) {
 __device__ __forceinline__ float2 c_fma(float2 acc, float2 x, float mr, float mi) {
     return upk(fma2(pk(-x.y, x.x), pk(mi, mi), fma2(pk(x.x, x.y), pk(mr, mr), pk(acc.x, acc.y))));
 }
-__device__ __forceinline__ float2 r_mul(float2 x, float r) { return upk(mul2(pk(x.x, x.y), pk(r, r))); }
 __device__ __forceinline__ float2 r_fma(float2 acc, float2 x, float r) {
     return upk(fma2(pk(x.x, x.y), pk(r, r), pk(acc.x, acc.y)));
 }
@@ -92,11 +96,6 @@ __device__ __forceinline__ double2 c_fma(double2 acc, double2 x, double mr, doub
     acc.x += mr * x.x - mi * x.y;
     acc.y += mr * x.y + mi * x.x;
     return acc;
-}
-__device__ __forceinline__ double2 r_mul(double2 x, double r) {
-    x.x *= r;
-    x.y *= r;
-    return x;
 }
 __device__ __forceinline__ double2 r_fma(double2 acc, double2 x, double r) {
     acc.x += r * x.x;
@@ -442,26 +441,6 @@ __device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<R
 }
 
 // ----------------------------------------------------------------- mappings
-template <int WB>
-__device__ __forceinline__ uint64_t thread_gbits(const StageDesc& S, int lane, int warp) {
-    uint64_t g = 0;
-#pragma unroll
-    for (int l = 0; l < kLaneBits; ++l) g |= (uint64_t)((lane >> l) & 1) << S.lane_q[l];
-#pragma unroll
-    for (int w = 0; w < WB; ++w) g |= (uint64_t)((warp >> w) & 1) << S.warp_q[w];
-    return g;
-}
-
-template <int WB>
-__device__ __forceinline__ uint32_t thread_soff(const StageDesc& S, int lane, int warp) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int l = 0; l < kLaneBits; ++l) s ^= ((lane >> l) & 1) ? (uint32_t)S.lane_s[l] : 0u;
-#pragma unroll
-    for (int w = 0; w < WB; ++w) s ^= ((warp >> w) & 1) ? (uint32_t)S.warp_s[w] : 0u;
-    return s;
-}
-
 // SMEM offsets are kept in BYTES (swizzled amplitude index * sizeof(T2)) so an
 // access is one LOP3 (xor) + STS/LDS [reg + smem_base] with no scaling.
 template <int RB, typename T2>
