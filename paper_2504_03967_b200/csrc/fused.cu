@@ -733,6 +733,7 @@ cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uin
     switch (cfg_id) {
         case 0: return launch_fused_t<double, 4, 3>(P, psi, rank_bits, st);
         case 1: return launch_fused_t<double, 3, 2>(P, psi, rank_bits, st);
+        case 3: return launch_fused_t<double, 5, 3, 1>(P, psi, rank_bits, st);
         default: return launch_fused_t<double, 3, 0>(P, psi, rank_bits, st);
     }
 }

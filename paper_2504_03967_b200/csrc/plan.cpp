@@ -126,16 +126,16 @@ static int validate(const int32_t* gt, const double* gp, int64_t n_gates, int n,
 // (ids must match launch_fused in fused.cu; array index = id)
 static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}, {4, 5, 3}, {5, 5, 4}, {6, 5, 2},
                                     {7, 6, 3}};
-static const KernelCfg kCfgC128[] = {{0, 4, 3}, {1, 3, 2}, {2, 3, 0}};
+static const KernelCfg kCfgC128[] = {{0, 4, 3}, {1, 3, 2}, {2, 3, 0}, {3, 5, 3}};
 // auto preference order (ids)
 static const int kAutoC64[] = {4, 1, 2, 3};
-static const int kAutoC128[] = {0, 1, 2};
+static const int kAutoC128[] = {3, 0, 1, 2};
 
 static bool pick_cfg(int dtype, int n_local, int force_k, int force_cfg, KernelCfg& out) {
     const KernelCfg* cfgs = dtype == QG_DTYPE_C64 ? kCfgC64 : kCfgC128;
-    const int n_all = dtype == QG_DTYPE_C64 ? 8 : 3;
+    const int n_all = dtype == QG_DTYPE_C64 ? 8 : 4;
     const int* order = dtype == QG_DTYPE_C64 ? kAutoC64 : kAutoC128;
-    const int nc = dtype == QG_DTYPE_C64 ? 4 : 3;
+    const int nc = 4;  // auto candidates per dtype
     if (force_cfg > 0) {
         if (force_cfg > n_all || cfgs[force_cfg - 1].k() > n_local) return false;
         out = cfgs[force_cfg - 1];

@@ -16,7 +16,7 @@ from paper_2504_03967_b200 import errors as E
 from paper_2504_03967_b200 import statevec as sv
 from paper_2504_03967_b200.generators import QftSpec, RandomSpec, build_qft, generate_random_gate_list
 from paper_2504_03967_b200.generators import qft_arrays, random_arrays
-from paper_2504_03967_b200.ir import CircType, CircuitTensor, GateKind
+from paper_2504_03967_b200.ir import CircType, CircuitTensor, GateKind, GateRecord
 
 pytestmark = pytest.mark.gpu
 
@@ -276,8 +276,8 @@ def test_sampler_edge_cases():
     assert set(t.indices.tolist()) <= {0, 1 << 16}
 
 # every fused-kernel instantiation (kernel_cfg = 1 + id; c64: 8 configs incl. the
-# 32/64-amplitude-per-thread ones, c128: 3) against the oracle on a mixed circuit
-@pytest.mark.parametrize("precision,cfg", [("fp32", c) for c in range(1, 9)] + [("fp64", c) for c in range(1, 4)])
+# 32/64-amplitude-per-thread ones, c128: 4) against the oracle on a mixed circuit
+@pytest.mark.parametrize("precision,cfg", [("fp32", c) for c in range(1, 9)] + [("fp64", c) for c in range(1, 5)])
 def test_every_kernel_config_vs_oracle(precision, cfg):
     n = 17
     gt, gp = mixed(n, 500, 30 + cfg)
@@ -286,3 +286,24 @@ def test_every_kernel_config_vs_oracle(precision, cfg):
     st = sv.init_zero_state(n, precision)
     plan.execute(st)
     assert rel_l2(st.to_numpy(), ref) < (1e-12 if precision == "fp64" else 1e-5)
+
+
+# tiny states (below every fused tile: the single-gate kernel path) and edge inputs
+@pytest.mark.parametrize("n", range(1, 10))
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_small_states_vs_oracle(n, precision):
+    gt, gp = mixed(n, 60, 200 + n)
+    ref = oracle.run_arrays(gt, gp, n, gt.shape[0], "fp64")
+    st, counts = sv.run_circuit(circuit(gt, gp, n), sv.SimOptions(precision=precision, shots=256, rng_seed=1))
+    assert rel_l2(st.to_numpy(), ref) <= TOL[precision]
+    assert counts.total == 256 and all(len(k) == n for k in counts.counts)
+
+
+def test_empty_and_measure_only_circuits():
+    for gates in ([], [GateRecord.measure(0), GateRecord.measure(2)]):
+        c = CircuitTensor.from_gates(CircType.IMPORTED, 3, gates)
+        st, counts = sv.run_circuit(c, sv.SimOptions("fp64", shots=10))
+        ref = np.zeros(8, dtype=np.complex128)
+        ref[0] = 1
+        assert np.array_equal(st.to_numpy(), ref)
+        assert counts.counts == {"000": 10}

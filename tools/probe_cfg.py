@@ -26,8 +26,9 @@ for n in ns:
         gt, gp = random_arrays(RandomSpec(n, 1000, 0)) if kind == "random" else qft_arrays(n)
         ref = None
         for kw in specs:
-            plan, st, ms = run(gt, gp, n, "fp32", **kw)
-            S = (1 << n) * 8
+            prec = os.environ.get("QG_PREC", "fp32")
+            plan, st, ms = run(gt, gp, n, prec, **kw)
+            S = (1 << n) * (8 if prec == "fp32" else 16)
             out = dict(kind=kind, n=n, kw=kw, passes=plan.info["n_passes"], stages=plan.info["n_stages"],
                        cxm=plan.info["n_cxm"], ms=round(ms, 3), ms_per_pass=round(ms / plan.info["n_passes"], 4),
                        gbs=round(2 * S * plan.info["n_passes"] / ms / 1e6, 1), gates_per_s=round(gt.shape[0] / ms * 1e3))
