@@ -130,6 +130,11 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
 /* ---- execution ------------------------------------------------------------ */
 /* init_zero_state (statevec.py:81-94) for one shard: amplitude 0 = 1 on rank 0 */
 int qg_state_init_zero(void* state, int32_t n_local, int32_t dtype, int32_t rank, void* stream);
+/* H on every qubit of qubit_mask (global positions) applied to |0...0>, in one
+ * write pass: amplitude 2^(-popcount(mask)/2) where the global index has no bit
+ * outside the mask (QCrank's address-register preparation, qcrank.simulate) */
+int qg_state_init_uniform(void* state, int32_t n_local, int32_t dtype, uint64_t qubit_mask, int32_t rank,
+                          void* stream);
 /* run one segment of the plan (all passes on one device): replaces statevec.py:207-208
  * (and the per-worker loop partition.py:265-274 for the LOCAL part) */
 int qg_plan_execute_segment(const qg_plan* plan, int64_t segment, void* state, int32_t rank,

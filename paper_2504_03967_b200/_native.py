@@ -58,6 +58,7 @@ _SIGS = {
     "qg_plan_get_final_map": (C.c_int, [_P, _P]),
     "qg_plan_export": (C.c_int, [_P, _P, C.POINTER(C.c_int64), _P, C.POINTER(C.c_int64)]),
     "qg_state_init_zero": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P]),
+    "qg_state_init_uniform": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, _P]),
     "qg_plan_execute_segment": (C.c_int, [_P, C.c_int64, _P, C.c_int32, _P, C.c_int32, C.POINTER(ExecStats)]),
     "qg_plan_execute": (C.c_int, [_P, _P, _P, C.c_int32, C.POINTER(ExecStats)]),
     "qg_apply_matrix": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P]),

@@ -223,6 +223,14 @@ int qg_state_init_zero(void* state, int32_t n_local, int32_t dtype, int32_t rank
     return QG_OK;
 }
 
+int qg_state_init_uniform(void* state, int32_t n_local, int32_t dtype, uint64_t qubit_mask, int32_t rank,
+                          void* stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (!state || n_local < 0 || n_local > 40 || rank < 0) return fail(QG_E_INVALID_ARG, "bad state / n_local / rank");
+    QG_CUDA(qg::launch_init_uniform(state, n_local, dtype, rank, qubit_mask, (cudaStream_t)stream), "init_uniform");
+    return QG_OK;
+}
+
 int qg_plan_execute_segment(const qg_plan* plan, int64_t segment, void* state, int32_t rank, void* stream,
                             int32_t timed, qg_exec_stats* stats) {
     if (!plan || !state) return fail(QG_E_INVALID_ARG, "NULL argument");

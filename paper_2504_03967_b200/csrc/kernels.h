@@ -22,6 +22,7 @@ int64_t ucry_workspace_bytes(int m, int n_t, int dtype);
 cudaError_t launch_ucry(int dtype, void* psi, const UcryOp& op, const double* alpha_dev, void* ws, cudaStream_t st);
 
 cudaError_t launch_init_zero(void* psi, int n_local, int dtype, int rank, cudaStream_t st);
+cudaError_t launch_init_uniform(void* psi, int n_local, int dtype, int rank, uint64_t mask, cudaStream_t st);
 // partial fp64 sums of |a|^2: grid-stride, one double per CTA into `partial`, then
 // a single-CTA finish into partial[n_parts]
 cudaError_t launch_norm(const void* psi, int64_t n_amps, int dtype, double* partial, int n_parts, cudaStream_t st);

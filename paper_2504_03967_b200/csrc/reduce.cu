@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <cub/cub.cuh>
+#include <cmath>
 
 #include "kernels.h"
 
@@ -58,6 +59,31 @@ cudaError_t launch_init_zero(void* psi, int n_local, int dtype, int rank, cudaSt
         if (dtype == 0) set_one<<<1, 1, 0, st>>>(static_cast<float2*>(psi));
         else set_one<<<1, 1, 0, st>>>(static_cast<double2*>(psi));
     }
+    return cudaGetLastError();
+}
+
+// H on every qubit of `mask` applied to |0...0>: 2^(-|mask|/2) where the global
+// index has no bit outside mask, 0 elsewhere (one write pass)
+template <typename T2>
+__global__ void set_uniform(T2* __restrict__ psi, uint64_t n, uint64_t rank_bits, uint64_t mask, double v) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        T2 a;
+        a.x = ((rank_bits | i) & ~mask) ? 0 : v;
+        a.y = 0;
+        psi[i] = a;
+    }
+}
+
+cudaError_t launch_init_uniform(void* psi, int n_local, int dtype, int rank, uint64_t mask, cudaStream_t st) {
+    const uint64_t n = 1ull << n_local;
+    const double v = std::pow(2.0, -0.5 * __builtin_popcountll(mask));
+    const uint64_t rank_bits = (uint64_t)rank << n_local;
+    const int threads = 256;
+    uint64_t blocks = (n + threads - 1) / threads;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    if (dtype == 0) set_uniform<<<(unsigned)blocks, threads, 0, st>>>(static_cast<float2*>(psi), n, rank_bits, mask, v);
+    else set_uniform<<<(unsigned)blocks, threads, 0, st>>>(static_cast<double2*>(psi), n, rank_bits, mask, v);
     return cudaGetLastError();
 }
 

@@ -313,13 +313,22 @@ def run_gates(gate_type: np.ndarray, gate_param: np.ndarray, n_qubits: int, opti
     gp = np.asarray(gate_param, dtype=np.float64).reshape(-1)
     nb = sv._trailing_split_arrays(gt[:, 0])
     sv._check_budget(n_qubits, options.precision, options.memory_budget)
-    items = collapse_ucry(gt[:nb], gp[:nb], min_addr)
+    lead, lead_mask = 0, 0
+    while lead < nb and gt[lead, 0] == GateKind.H and not (lead_mask >> int(gt[lead, 2])) & 1:
+        lead_mask |= 1 << int(gt[lead, 2])
+        lead += 1
+    if lead < 4:  # not worth a special case
+        lead, lead_mask = 0, 0
+    items = collapse_ucry(gt[lead:nb], gp[lead:nb], min_addr)
     plans = []
     for it in items:  # plan everything first: gate errors raise before any device work
         if it[0] == "gates":
             plans.append(sv.CompiledCircuit(it[1], it[2], n_qubits, options.precision, 0, options.fuse,
                                             options.tile_qubits, options.max_stages, options.max_cost))
     state = sv.init_zero_state(n_qubits, options.precision, options.memory_budget, options.device)
+    if lead_mask:  # leading H layer on distinct qubits, applied to |0...0>: uniform superposition
+        N.call("qg_state_init_uniform", C.c_void_p(state.amplitudes.data_ptr()), n_qubits,
+               sv._QG_DTYPE[options.precision], C.c_uint64(lead_mask), 0, sv._stream(state.amplitudes.device))
     pi, k = 0, 0
     while k < len(items):
         if items[k][0] == "gates":
@@ -342,8 +351,9 @@ def run_gates(gate_type: np.ndarray, gate_param: np.ndarray, n_qubits: int, opti
 
 def simulate(angles: np.ndarray, options: sv.SimOptions | None = None, state: sv.StateVector | None = None):
     """Run the QCrank circuit of an AngleTensor without materialising its gate
-    arrays: H on the address register (fused pass) then the data register's
-    uniformly controlled RYs (qg_apply_ucry, 5 data qubits per pass) — the same
+    arrays: the H layer on |0...0> is the uniform superposition of the address
+    register (qg_state_init_uniform, one write pass), then the data register's
+    uniformly controlled RYs (qg_apply_ucry, 5 data qubits per pass) — the
     kernels run_gates uses after collapse_ucry.  `state` (optional) is a reusable
     buffer of the right size (batched images)."""
     options = options or sv.SimOptions()
@@ -353,15 +363,11 @@ def simulate(angles: np.ndarray, options: sv.SimOptions | None = None, state: sv
     nd = angles.shape[1]
     n = m + nd
     sv._check_budget(n, options.precision, options.memory_budget)
-    h_t = np.array([[int(GateKind.H), -1, q] for q in range(m)], dtype=np.int32).reshape(-1, 3)
-    plan = sv.CompiledCircuit(h_t, np.zeros(m), n, options.precision, 0, options.fuse, options.tile_qubits,
-                              options.max_stages, options.max_cost)
     if state is None:
         state = sv.init_zero_state(n, options.precision, options.memory_budget, options.device)
-    else:
-        N.call("qg_state_init_zero", C.c_void_p(state.amplitudes.data_ptr()), n, sv._QG_DTYPE[options.precision],
-               0, sv._stream(state.amplitudes.device))
-    plan.execute(state)
+    # H on the address register applied to |0...0>: the uniform superposition, one write pass
+    N.call("qg_state_init_uniform", C.c_void_p(state.amplitudes.data_ptr()), n, sv._QG_DTYPE[options.precision],
+           C.c_uint64((1 << m) - 1), 0, sv._stream(state.amplitudes.device))
     apply_ucry(state, list(range(m)), list(range(m, n)), angles)
     counts = None
     if options.shots > 0:

@@ -105,7 +105,7 @@ def c4(images):
     # exact-mode decode of the last image's first 2^12 addresses is a cheap sanity check
     rep_ok = bool(torch.isfinite(st.amplitudes[:1024]).all().item())
     S = (1 << n) * 8
-    passes = 4  # 2 H passes (24 address qubits, 13-qubit tiles) + 2 UCRY passes (5 + 3 data qubits)
+    bytes_per_image = 5 * S  # uniform-superposition init (write S) + 2 UCRY passes (5 + 3 data qubits, 2S each)
     # reference algorithm on the gate-level circuit at m = 8 (2 x 8 x 256 gates), scaled x2^(n - 16) per gate
     a_s = qc.prepare_angles(qc.ImageGray(32, 64, rng.integers(0, 256, 2048, dtype=np.uint8)), 8, nd)
     gt, gp, ns = qc.build_qcrank_circuit(a_s, measure=False)
@@ -116,7 +116,7 @@ def c4(images):
     return {"config": f"c4 QCrank 24+8 c64, batch of {images} images", "ms_per_image": per_img,
             "angle_upload_ms_per_image": upload_ms,
             "images_per_s": 1e3 / per_img, "gate_equivalents_per_image": gate_eq,
-            "gate_equivalents_per_s": gate_eq / per_img * 1e3, "hbm_gbs": 2 * S * passes / per_img / 1e6,
+            "gate_equivalents_per_s": gate_eq / per_img * 1e3, "hbm_gbs": bytes_per_image / per_img / 1e6,
             "finite": rep_ok, "cpu_ref_s_per_image": ref_img_s,
             "cpu_ref": f"oracle port of the gate-level QCrank circuit at m=8 ({gt.shape[0]} gates, {dt:.1f} s), "
                        f"per-gate time scaled to 2^{n} amplitudes and {gate_eq} gates"}
