@@ -50,20 +50,23 @@ def _newest_input() -> float:
 
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-    extra = []
-    if src == "fused.cu":
-        ptx = os.path.join(BUILD, "fused.ptx")
-        r = subprocess.run([NVCC, *ARCH, *FLAGS, "-ptx", os.path.join(CSRC, src), "-o", ptx],
-                           capture_output=True, text=True)
-        if r.returncode != 0 or not jump_table_ok(open(ptx).read()):
-            sys.stderr.write("fused.cu: PTX jump-table check failed; building the compare-tree dispatch\n")
-            extra = ["-DQG_NO_JT"]
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-warn-spills"]
+    keep = os.path.join(BUILD, "keep_" + os.path.splitext(src)[0])
+    if src == "fused.cu":  # keep the PTX of this very compilation for the jump-table check
+        os.makedirs(keep, exist_ok=True)
+        cmd += ["-keep", "-keep-dir", keep]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    if src == "fused.cu":
+        ptx = os.path.join(keep, "fused.ptx")
+        if not os.path.exists(ptx) or not jump_table_ok(open(ptx).read()):
+            sys.stderr.write("fused.cu: PTX jump-table check failed; building the compare-tree dispatch\n")
+            r = subprocess.run(cmd + ["-DQG_NO_JT"], capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     if r.stderr.strip():
         sys.stderr.write(r.stderr)
     return obj
