@@ -14,7 +14,7 @@ import re
 from .errors import raise_for_status
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libqgear_b200.so")
+LIB_PATH = os.environ.get("QG_LIB_PATH") or os.path.join(_PKG, "libqgear_b200.so")  # override: dev variants
 HEADER_PATH = os.path.join(os.path.dirname(_PKG), "include", "qgear_b200.h")
 
 DTYPE_C64 = 0
