@@ -417,6 +417,64 @@ struct Emitter {
                 }
         }
     }
+    static void inverse_of(const uint32_t* rows, int rb, uint32_t* inv) {
+        uint32_t a[kMaxRegBits];
+        for (int r = 0; r < rb; ++r) { a[r] = rows[r]; inv[r] = 1u << r; }
+        for (int j = 0; j < rb; ++j) {
+            int p = j;
+            while (!((a[p] >> j) & 1u)) ++p;
+            std::swap(a[p], a[j]); std::swap(inv[p], inv[j]);
+            for (int r = 0; r < rb; ++r)
+                if (r != j && ((a[r] >> j) & 1u)) { a[r] ^= a[j]; inv[r] ^= inv[j]; }
+        }
+    }
+    // Fewest OC_CXM moves (<= 2, searched) that leave logical bit b in a form the
+    // kernel has a body for (dense: V = W unit / W form / V form; phase: W with one
+    // or two bits); applies them and returns true.  Full materialisation costs
+    // rank(L - I) moves, usually 3.
+    bool reduce_for(int b, bool dense) {
+        auto form_ok = [&](const uint32_t* rows) {
+            uint32_t inv[kMaxRegBits] = {};
+            inverse_of(rows, rb, inv);
+            const uint32_t w = inv[b];
+            if (!dense) return unit(w) >= 0 || two(w);
+            uint32_t v = 0;
+            for (int r = 0; r < rb; ++r) if ((rows[r] >> b) & 1u) v |= 1u << r;
+            return (unit(v) >= 0 && v == w) || (unit(v) >= 0 && two(w) && (w & v)) ||
+                   (unit(w) >= 0 && two(v) && (w & v));
+        };
+        uint32_t r1[kMaxRegBits], r2[kMaxRegBits];
+        int best[4] = {-1, -1, -1, -1};
+        for (int t1 = 0; t1 < rb && best[0] < 0; ++t1)
+            for (int c1 = 0; c1 < rb && best[0] < 0; ++c1) {
+                if (t1 == c1) continue;
+                std::memcpy(r1, row, sizeof(r1));
+                r1[t1] ^= r1[c1];
+                if (form_ok(r1)) { best[0] = t1; best[1] = c1; }
+            }
+        if (best[0] < 0)
+            for (int t1 = 0; t1 < rb && best[0] < 0; ++t1)
+                for (int c1 = 0; c1 < rb && best[0] < 0; ++c1) {
+                    if (t1 == c1) continue;
+                    std::memcpy(r1, row, sizeof(r1));
+                    r1[t1] ^= r1[c1];
+                    for (int t2 = 0; t2 < rb && best[0] < 0; ++t2)
+                        for (int c2 = 0; c2 < rb && best[0] < 0; ++c2) {
+                            if (t2 == c2) continue;
+                            std::memcpy(r2, r1, sizeof(r2));
+                            r2[t2] ^= r2[c2];
+                            if (form_ok(r2)) { best[0] = t1; best[1] = c1; best[2] = t2; best[3] = c2; }
+                        }
+                }
+        if (best[0] < 0) return false;
+        flush_phases(~0u);  // CXM moves data: queued phases go first
+        for (int k = 0; k < 4 && best[k] >= 0; k += 2) {
+            row[best[k]] ^= row[best[k + 1]];
+            push(A_CXM, best[k], best[k + 1]);
+            ++n_cxm;
+        }
+        return true;
+    }
     static int unit(uint32_t v) { return (v && !(v & (v - 1))) ? __builtin_ctz(v) : -1; }
     static bool two(uint32_t v) { return v && unit(v) < 0 && unit(v & (v - 1)) >= 0; }
     int slot_w(int b) {  // slot bit whose value is logical bit b (materialising if needed)
@@ -434,7 +492,10 @@ struct Emitter {
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         uint32_t w = inv[b];
-        if (unit(w) < 0 && !two(w)) { materialise(); w = 1u << b; }
+        if (unit(w) < 0 && !two(w)) {
+            if (reduce_for(b, false)) { inverse(inv); w = inv[b]; }
+            else { materialise(); w = 1u << b; }
+        }
         for (auto& g : sq)
             if (g.first == w) { g.second.emplace_back(cmask, e); return; }
         sq.push_back({w, {{cmask, e}}});
@@ -496,6 +557,13 @@ struct Emitter {
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         uint32_t v = col(b), w = inv[b];
+        const bool supported = (unit(v) >= 0 && v == w) || (rot && unit(v) >= 0 && two(w) && (w & v)) ||
+                               (rot && unit(w) >= 0 && two(v) && (w & v));
+        if (!supported && rot && reduce_for(b, true)) {
+            inverse(inv);
+            v = col(b);
+            w = inv[b];
+        }
         int t = -1, c = -1;
         if (unit(v) >= 0 && v == w) {
             t = unit(v);
