@@ -6,16 +6,19 @@ Public API mirrors the reference package (/root/reference/pkg/src/qgear):
   statevec    init_zero_state, run_circuit, run_circuit_timed, sample_counts, exact_probabilities,
               apply_matrix_array / swap_target_pairs_array / phase_pairs_array, ...
   partition   execute_distributed (sharded over torch.distributed ranks or in-process shards)
+  batch       run_circuit_set(_distributed): CircuitSet batches, plan reuse via qg_plan_rebind
+  qcrank      QCrank image encoding / decoding, one-pass UCRY execution
+  container   QGIR1 circuit-set files: native parse / write, zero-copy array views
 The compute runs in libqgear_b200.so (hand-written sm_100a CUDA); see DESIGN.md.
 """
 
 from . import errors, generators, ir  # noqa: F401
 
-__all__ = ["errors", "generators", "ir", "statevec", "partition"]
+__all__ = ["errors", "generators", "ir", "statevec", "partition", "batch", "qcrank", "container"]
 
 
-def __getattr__(name):  # torch-dependent modules load lazily
-    if name in ("statevec", "partition"):
+def __getattr__(name):  # torch- / library-dependent modules load lazily
+    if name in ("statevec", "partition", "batch", "qcrank", "container"):
         import importlib
 
         return importlib.import_module(f".{name}", __name__)
