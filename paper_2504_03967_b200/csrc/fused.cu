@@ -549,6 +549,9 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB 
         // bits; when every tile bit is below 32 (P.tile_lo32) the per-amplitude
         // address walk is 32-bit (1 LOP3 + 1 IMAD.WIDE instead of 64-bit XOR + LEA pair)
         T2* __restrict__ pt = psi + base;
+        // opaque to the compiler, so psi + base + o is not re-associated into a
+        // 64-bit add + LEA pair per amplitude: one IMAD.WIDE.U32 (o * 8 + pt) each
+        asm("mov.b64 %0, %0;" : "+l"(pt));
         if (P.tile_lo32) {  // global load, Gray-code order over the register index
             const StageDesc& S = P.stg[li];
             uint32_t o = (uint32_t)tgb(li);
