@@ -77,6 +77,7 @@ struct CoefCap<double> {
 //              holds; word bits 8-15 = entry count, 16-31 = first entry
 //   fam 7 CXM  + pair index (T, C) (after OC_XF): move slot p -> p ^ (p_C) e_T
 //              (materialises part of L), F_T ^= F_C
+//   OC_END     (= oc_end(RB)) terminates a stage's op list
 enum OpFam { F_RD = 0, F_CD, F_PH, F_RDW, F_RDV, F_PHW, F_PH2 };
 constexpr uint32_t kNoPred = 0xff;
 
@@ -91,6 +92,8 @@ QG_HD constexpr uint32_t oc_xf(int rb) { return (uint32_t)(3 * rb + 3 * rb * (rb
 QG_HD constexpr uint32_t oc_cxm(int rb, int t, int c) {
     return oc_xf(rb) + 1 + (uint32_t)(t * (rb - 1) + (c < t ? c : c - 1));
 }
+// ends every stage's op list
+QG_HD constexpr uint32_t oc_end(int rb) { return oc_xf(rb) + 1 + (uint32_t)(rb * (rb - 1)); }
 QG_HD constexpr int oc_pair(int fam, int rb, int t, int c) {
     return oc_base(fam, rb) + t * (rb - 1) + (c < t ? c : c - 1);
 }

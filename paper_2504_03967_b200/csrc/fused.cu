@@ -316,8 +316,16 @@ __device__ __forceinline__ T2 ph_product(const PassDesc<Real>& P, uint32_t w, ui
 #endif
 #define QG_LAB(ok, code, junk) ((ok) ? (code) : 1000 + (junk))
 template <int RB, typename T2, typename Real>
-__device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P, uint32_t w, uint64_t tb,
-                                       uint32_t& F) {
+__device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<Real>& P, int o, uint64_t tb,
+                                              uint32_t& F) {
+    // op words are read through a running byte offset (no per-op index math) and
+    // one word ahead; the list ends with an OC_END word (no per-op bound check)
+    const char* opb = reinterpret_cast<const char*>(P.ops);
+    uint32_t ob = (uint32_t)o * 4u;
+    uint32_t w = *reinterpret_cast<const uint32_t*>(opb + ob);
+  for (;;) {
+    ob += 4u;
+    const uint32_t wn = *reinterpret_cast<const uint32_t*>(opb + ob);
 #ifdef QG_JT
     {
         const uint32_t code = w & 0xffu;
@@ -421,24 +429,17 @@ __device__ __forceinline__ void run_op(T2 (&a)[1 << RB], const PassDesc<Real>& P
             }
             break;
         }
+        case oc_end(RB): {
+            QGJ_ENTER("QGJ_END");
+            return;
+        }
         default: __builtin_unreachable();
     }
+    w = wn;
+  }
 }
 #undef QG_LAB
 #undef QGJ_ENTER
-
-// a stage's op list; the next op word is fetched before the current op runs
-// (the descriptor has slack after the last word, so the read is in bounds)
-template <int RB, typename T2, typename Real>
-__device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<Real>& P, int o, const int end,
-                                              uint64_t tb, uint32_t& F) {
-    uint32_t w = P.ops[o];
-    for (; o < end; ++o) {
-        const uint32_t wn = P.ops[o + 1];
-        run_op<RB>(a, P, w, tb, F);
-        w = wn;
-    }
-}
 
 // ----------------------------------------------------------------- mappings
 // SMEM offsets are kept in BYTES (swizzled amplitude index * sizeof(T2)) so an
@@ -599,7 +600,7 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB 
                 F = 0;
             }
             const uint64_t tb = base | rank_bits | tgb(s);
-            run_stage_ops<RB>(a, P, S.op_begin, S.op_end, tb, F);
+            run_stage_ops<RB>(a, P, S.op_begin, tb, F);
             if (S.tph_end > S.tph_begin) {  // thread-level phases commute with the whole stage
                 T2 ph;
                 ph.x = Real(1);

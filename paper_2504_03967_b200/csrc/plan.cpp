@@ -829,7 +829,7 @@ template <typename Real>
 static bool fits_t(const HostPass& hp) {
     const PassSize z = pass_size(hp);
     // one thread-phase slot is kept free for the plan's global phase
-    return z.ops <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph && z.pred <= kMaxPred &&
+    return z.ops + (int)hp.stages.size() <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph && z.pred <= kMaxPred &&
            z.phe <= kMaxPhe && z.xfe <= kMaxXfe;
 }
 static bool fits(int dtype, const HostPass& hp) {
@@ -900,6 +900,7 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
             }
             d.ops[no++] = w;
         }
+        d.ops[no++] = op_word(oc_end(hp.cfg.rb), 0, 0);
         sd.op_end = (uint16_t)no;
         sd.tph_begin = (uint16_t)nt;
         for (const HostOp& o : h.tph) put_entry(d.tph[nt++], o);
