@@ -124,13 +124,13 @@ struct StageDesc {
     uint8_t lane_q[kLaneBits];
     uint8_t warp_q[kMaxWarpBits];
     uint8_t pad[2];
-    uint16_t reg_s[kMaxRegBits];   // input mapping: SMEM offset of each register bit
+    uint32_t reg_s[kMaxRegBits];   // input mapping: SMEM byte offset of each register bit
     uint16_t lane_s[kLaneBits];
     uint16_t warp_s[kMaxWarpBits];
     // output mapping (transpose out / global store): for slot bit j the tile-index
     // vector of L^-1 e_j (the stage's register CX gates, GF(2)-linear), as SMEM
     // offsets and as global index masks
-    uint16_t out_s[kMaxRegBits];
+    uint32_t out_s[kMaxRegBits];   // (SMEM byte offsets)
     uint64_t out_g[kMaxRegBits];
 };
 

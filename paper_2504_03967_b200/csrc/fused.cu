@@ -447,10 +447,9 @@ __device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<R
 template <int RB, typename T2>
 __device__ __forceinline__ void smem_put(char* sm, const StageDesc& S, uint32_t so, const T2 (&a)[1 << RB],
                                          uint32_t F) {
-    constexpr int sh = sizeof(T2) == 8 ? 3 : 4;
     uint32_t rs[RB];
 #pragma unroll
-    for (int b = 0; b < RB; ++b) rs[b] = (uint32_t)S.out_s[b] << sh;
+    for (int b = 0; b < RB; ++b) rs[b] = S.out_s[b];
 #pragma unroll
     for (int b = 0; b < RB; ++b)
         if ((F >> b) & 1u) so ^= rs[b];
@@ -463,10 +462,9 @@ __device__ __forceinline__ void smem_put(char* sm, const StageDesc& S, uint32_t 
 
 template <int RB, typename T2>
 __device__ __forceinline__ void smem_get(const char* sm, const StageDesc& S, uint32_t so, T2 (&a)[1 << RB]) {
-    constexpr int sh = sizeof(T2) == 8 ? 3 : 4;
     uint32_t rs[RB];
 #pragma unroll
-    for (int b = 0; b < RB; ++b) rs[b] = (uint32_t)S.reg_s[b] << sh;
+    for (int b = 0; b < RB; ++b) rs[b] = S.reg_s[b];
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) {
         if (j) so ^= rs[ctz_c(j)];

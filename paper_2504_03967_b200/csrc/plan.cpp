@@ -765,7 +765,7 @@ static void fill_stage(int dtype, const HostPass& hp, const HostStage& h, StageD
     std::memset(&d, 0, sizeof(d));
     for (size_t b = 0; b < h.reg_tile.size(); ++b) {
         d.reg_q[b] = (uint8_t)hp.tile_q[h.reg_tile[b]];
-        d.reg_s[b] = (uint16_t)swz(dtype, 1 << h.reg_tile[b]);
+        d.reg_s[b] = (uint32_t)swz(dtype, 1 << h.reg_tile[b]) * (dtype == QG_DTYPE_C64 ? 8u : 16u);
     }
     for (size_t b = 0; b < h.lane_tile.size(); ++b) {
         d.lane_q[b] = (uint8_t)hp.tile_q[h.lane_tile[b]];
@@ -784,7 +784,7 @@ static void fill_stage(int dtype, const HostPass& hp, const HostStage& h, StageD
                 tidx |= 1 << h.reg_tile[r];
                 g |= 1ull << hp.tile_q[h.reg_tile[r]];
             }
-        d.out_s[b] = (uint16_t)swz(dtype, tidx);
+        d.out_s[b] = (uint32_t)swz(dtype, tidx) * (dtype == QG_DTYPE_C64 ? 8u : 16u);
         d.out_g[b] = g;
     }
 }
