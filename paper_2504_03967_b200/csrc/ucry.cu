@@ -9,10 +9,11 @@
 // Gray order recovers alpha) and runs it here as one HBM pass for up to
 // kMaxUcryTargets data qubits at once:
 //
-//   thread = one address a (and one combination of the remaining qubits);
-//   it holds the 2^T amplitudes of its T target qubits in registers, applies
-//   RY(alpha[a][d]) for every target d (cos/sin from a per-address table built
-//   once in fp64 and cast, like statevec.py:117), and writes them back.
+//   thread = one address a: it reads its cos/sin for every target once (a
+//   per-address table built in fp64 and cast, like statevec.py:117), then for
+//   each combination of the remaining qubits holds the 2^T amplitudes of its
+//   T target qubits in registers, applies RY(alpha[a][d]) for every target d,
+//   and writes them back.
 //
 // Traffic = read + write of the state once (+ the table, 2^m * T * 2 reals).
 #include <cuda_runtime.h>
@@ -63,44 +64,51 @@ __global__ void __launch_bounds__(256) ucry_kernel(typename U2<Real>::T* __restr
                                                    const typename U2<Real>::T* __restrict__ table) {
     using C2 = typename U2<Real>::T;
     const uint64_t n_addr = 1ull << op.m;
-    const uint64_t n_threads = n_addr << op.n_rest;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_threads;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t a = g & (n_addr - 1);
-        const uint64_t r = g >> op.m;
-        const uint64_t base = (op.addr_contig ? (a << op.addr_pos[0]) : deposit(a, op.addr_pos, op.m)) |
-                              deposit(r, op.rest_pos, op.n_rest);
-        C2 v[1 << T];
-#pragma unroll
-        for (int x = 0; x < (1 << T); ++x) {
-            uint64_t i = base;
-#pragma unroll
-            for (int k = 0; k < T; ++k) i |= (uint64_t)((x >> k) & 1) << op.tgt_pos[k];
-            v[x] = psi[i];
-        }
+    const uint64_t n_rest = 1ull << op.n_rest;
+    // thread = one address a: its cos/sin for every target are read once and
+    // reused for all 2^n_rest combinations of the remaining qubits
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_addr;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        Real c[T], s[T];
 #pragma unroll
         for (int k = 0; k < T; ++k) {
             const C2 cs = table[(uint64_t)k * n_addr + a];
-            const Real c = cs.x, s = cs.y;
+            c[k] = cs.x;
+            s[k] = cs.y;
+        }
+        const uint64_t abits = op.addr_contig ? (a << op.addr_pos[0]) : deposit(a, op.addr_pos, op.m);
+        for (uint64_t r = 0; r < n_rest; ++r) {
+            const uint64_t base = abits | deposit(r, op.rest_pos, op.n_rest);
+            C2 v[1 << T];
 #pragma unroll
             for (int x = 0; x < (1 << T); ++x) {
-                if (x & (1 << k)) continue;
-                const C2 p = v[x], q = v[x | (1 << k)];
-                C2 u, w;  // RY = [[c, -s], [s, c]] (statevec.py:104)
-                u.x = c * p.x - s * q.x;
-                u.y = c * p.y - s * q.y;
-                w.x = s * p.x + c * q.x;
-                w.y = s * p.y + c * q.y;
-                v[x] = u;
-                v[x | (1 << k)] = w;
+                uint64_t i = base;
+#pragma unroll
+                for (int k = 0; k < T; ++k) i |= (uint64_t)((x >> k) & 1) << op.tgt_pos[k];
+                v[x] = psi[i];
             }
-        }
 #pragma unroll
-        for (int x = 0; x < (1 << T); ++x) {
-            uint64_t i = base;
+            for (int k = 0; k < T; ++k) {
 #pragma unroll
-            for (int k = 0; k < T; ++k) i |= (uint64_t)((x >> k) & 1) << op.tgt_pos[k];
-            psi[i] = v[x];
+                for (int x = 0; x < (1 << T); ++x) {
+                    if (x & (1 << k)) continue;
+                    const C2 p = v[x], q = v[x | (1 << k)];
+                    C2 u, w;  // RY = [[c, -s], [s, c]] (statevec.py:104)
+                    u.x = c[k] * p.x - s[k] * q.x;
+                    u.y = c[k] * p.y - s[k] * q.y;
+                    w.x = s[k] * p.x + c[k] * q.x;
+                    w.y = s[k] * p.y + c[k] * q.y;
+                    v[x] = u;
+                    v[x | (1 << k)] = w;
+                }
+            }
+#pragma unroll
+            for (int x = 0; x < (1 << T); ++x) {
+                uint64_t i = base;
+#pragma unroll
+                for (int k = 0; k < T; ++k) i |= (uint64_t)((x >> k) & 1) << op.tgt_pos[k];
+                psi[i] = v[x];
+            }
         }
     }
 }
@@ -117,8 +125,7 @@ cudaError_t launch_t(void* psi, const UcryOp& op, const double* alpha, void* ws,
         if (blocks > 148 * 32) blocks = 148 * 32;
         ucry_table<Real><<<(unsigned)blocks, threads, 0, st>>>(alpha, n_addr, op.n_t, table);
     }
-    const uint64_t n_threads = (uint64_t)n_addr << op.n_rest;
-    uint64_t blocks = (n_threads + 255) / 256;
+    uint64_t blocks = ((uint64_t)n_addr + 255) / 256;
     if (blocks > 148ull * 8) blocks = 148ull * 8;
     C2* s = static_cast<C2*>(psi);
     switch (op.n_t) {
