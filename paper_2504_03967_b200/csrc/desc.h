@@ -34,7 +34,6 @@ namespace qg {
 
 constexpr int kMaxStages = 8;
 constexpr int kMaxOps = 640;    // op words per pass
-constexpr int kMaxPred = 48;    // thread predicates (global-index masks) per pass
 constexpr int kMaxTph = 128;    // thread-phase entries per pass
 constexpr int kMaxPhe = 320;    // PH list entries per pass
 constexpr int kMaxXfe = 256;    // XF list entries per pass
@@ -73,8 +72,9 @@ struct CoefCap<double> {
 //   fam 5 PHW  + tri index (T > C)   PH with W = e_T + e_C
 //   fam 6 PH2  + tri index (T > C)   x e on logical |11> of slot bits (T, C); coef: e
 //   OC_XF      (= oc_xf(RB)) a list of X gates under thread-level controls: for each
-//              entry (xfe[]: predicate index | v << 8) F ^= v where the predicate
-//              holds; word bits 8-15 = entry count, 16-31 = first entry
+//              entry (xfe[]: control bit position | v << 8) F ^= v where that bit of
+//              the thread's global index is 1; word bits 8-15 = entry count, 16-31 =
+//              first entry
 //   fam 7 CXM  + pair index (T, C) (after OC_XF): move slot p -> p ^ (p_C) e_T
 //              (materialises part of L), F_T ^= F_C
 //   OC_END     (= oc_end(RB)) terminates a stage's op list
@@ -110,10 +110,12 @@ struct Entry {
     Real v[4];           // v0 = (v[0], v[1]), v1 = (v[2], v[3])
 };
 
-// one factor of an OC_PH phase: e where every bit of cmask is 1 in the thread's index
+// one factor of an OC_PH phase: e where bit `pos` of the thread's global index
+// is 1 (every predicate on this path is a single control qubit)
 template <typename Real>
 struct PhEnt {
-    uint64_t cmask;
+    uint32_t pos;
+    uint32_t pad;
     Real e[2];
 };
 
@@ -147,11 +149,10 @@ struct PassDesc {
     uint8_t comp_q[48];        // local positions outside the tile, ascending (tile id bits)
     // stg[0] = coalesced io mapping (lanes = tile bits 0..4); stg[1 + s] = compute stage s
     StageDesc stg[kMaxStages + 1];
-    uint64_t pred[kMaxPred];
     uint32_t ops[kMaxOps + 1];  // + 1: the kernel prefetches one word past a stage's list
     Entry<Real> tph[kMaxTph];
     PhEnt<Real> ph[kMaxPhe];
-    uint32_t xfe[kMaxXfe];      // OC_XF list entries: predicate index | flip vector << 8
+    uint32_t xfe[kMaxXfe];      // OC_XF list entries: control bit position | flip vector << 8
     Real coef[CoefCap<Real>::value];
 };
 

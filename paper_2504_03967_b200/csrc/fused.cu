@@ -284,12 +284,11 @@ __device__ __forceinline__ T2 ph_product(const PassDesc<Real>& P, uint32_t w, ui
     e.y = P.ph[b].e[1];
     for (int k = 1; k < n; ++k) {
         const PhEnt<Real>& E = P.ph[b + k];
-        if (pred_ok(tb, E.cmask)) {
-            T2 v;
-            v.x = E.e[0];
-            v.y = E.e[1];
-            e = cmul(e, v);
-        }
+        const bool on = (tb >> E.pos) & 1u;
+        T2 v;
+        v.x = on ? E.e[0] : Real(1);
+        v.y = on ? E.e[1] : Real(0);
+        e = cmul(e, v);
     }
     return e;
 }
@@ -424,8 +423,8 @@ __device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<R
             const int n = (w >> 8) & 0xffu, b = w >> 16;
             for (int k = 0; k < n; ++k) {
                 const uint32_t e = P.xfe[b + k];
-                const uint32_t pi = e & 0xffu;
-                if (pi == kNoPred || pred_ok(tb, P.pred[pi])) F ^= (e >> 8) & 63u;
+                const uint32_t on = (uint32_t)(tb >> (e & 63u)) & 1u;
+                F ^= (e >> 8) & (0u - on);
             }
             break;
         }

@@ -22,6 +22,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <cassert>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -383,6 +384,7 @@ struct Emitter {
     uint32_t xq_mask = 0;
     void flush_xf() {
         if (xq.empty()) return;
+        for (const auto& x : xq) assert(x.first && !(x.first & (x.first - 1)));  // one control bit
         HostOp o{};
         o.kind = A_XF; o.t = (int)xq[0].second; o.c = -1; o.cmask = xq[0].first; o.tq = o.cq = -1;
         o.xf = xq;
@@ -806,10 +808,9 @@ static int n_coef(const HostOp& o) {
 }
 
 // resource needs of a pass (descriptor capacity is checked by the scheduler)
-struct PassSize { int ops = 0, coef = 0, tph = 0, pred = 0, phe = 0, xfe = 0; };
+struct PassSize { int ops = 0, coef = 0, tph = 0, phe = 0, xfe = 0; };
 static PassSize pass_size(const HostPass& hp) {
     PassSize z;
-    std::vector<uint64_t> preds;
     for (const HostStage& h : hp.stages) {
         z.ops += (int)h.ops.size();
         z.tph += (int)h.tph.size();
@@ -817,11 +818,8 @@ static PassSize pass_size(const HostPass& hp) {
             z.coef += n_coef(o);
             z.phe += (int)o.ph.size();
             z.xfe += (int)o.xf.size();
-            for (const auto& x : o.xf)
-                if (x.first && std::find(preds.begin(), preds.end(), x.first) == preds.end()) preds.push_back(x.first);
         }
     }
-    z.pred = (int)preds.size();
     return z;
 }
 
@@ -829,7 +827,7 @@ template <typename Real>
 static bool fits_t(const HostPass& hp) {
     const PassSize z = pass_size(hp);
     // one thread-phase slot is kept free for the plan's global phase
-    return z.ops + (int)hp.stages.size() <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph && z.pred <= kMaxPred &&
+    return z.ops + (int)hp.stages.size() <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph &&
            z.phe <= kMaxPhe && z.xfe <= kMaxXfe;
 }
 static bool fits(int dtype, const HostPass& hp) {
@@ -867,13 +865,7 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
             if (std::find(hp.tile_q.begin(), hp.tile_q.end(), q) == hp.tile_q.end()) d.comp_q[nc0++] = (uint8_t)q;
     }
     fill_stage(dtype, hp, hp.io, d.stg[0]);
-    int no = 0, nc = 0, nt = 0, np = 0, nph = 0, nxf = 0;
-    auto pred_index = [&](uint64_t m) -> uint32_t {
-        if (!m) return kNoPred;
-        for (int i = 0; i < np; ++i) if (d.pred[i] == m) return (uint32_t)i;
-        d.pred[np] = m;
-        return (uint32_t)np++;
-    };
+    int no = 0, nc = 0, nt = 0, nph = 0, nxf = 0;
     for (int s = 0; s < d.n_stages; ++s) {
         const HostStage& h = hp.stages[s];
         StageDesc& sd = d.stg[1 + s];
@@ -883,13 +875,13 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
             uint32_t w;
             if (o.kind == A_XF) {
                 w = op_word(oc_xf(hp.cfg.rb), (uint32_t)o.xf.size(), (uint32_t)nxf);
-                for (const auto& x : o.xf) d.xfe[nxf++] = pred_index(x.first) | (x.second << 8);
+                for (const auto& x : o.xf) d.xfe[nxf++] = (uint32_t)__builtin_ctzll(x.first) | (x.second << 8);
             } else if (o.kind == A_CXM) {
                 w = op_word(oc_cxm(hp.cfg.rb, o.t, o.c), kNoPred, 0);
             } else if (o.kind == A_PH) {
                 w = op_word(op_code(o, hp.cfg.rb), (uint32_t)o.ph.size(), (uint32_t)nph);
                 for (const auto& x : o.ph) {
-                    d.ph[nph].cmask = x.first;
+                    d.ph[nph].pos = x.first ? (uint32_t)__builtin_ctzll(x.first) : 0u;
                     d.ph[nph].e[0] = (Real)x.second.first;
                     d.ph[nph].e[1] = (Real)x.second.second;
                     ++nph;
