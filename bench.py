@@ -61,6 +61,22 @@ def cpu_sample(n_qubits_target: int, sample_qubits: int, sample_blocks: int, see
     return 1.0 / sec_per_gate_target, dt, gt.shape[0]
 
 
+def host_info() -> dict:
+    """The host the CPU arm ran on (cpu_count, affinity, CPU model)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "model": model,
+            "threads": "1: statevec.run_circuit is single-threaded numpy; the reference's threaded executor "
+                       "(partition.execute_distributed) is fp64-only (partition.py:300-301), not this c64 config"}
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -133,7 +149,8 @@ def run_reference(args, rank: int):
            "dtype": "c64", "data": "synthetic (reference generator stream, PCG64 seed 0)", "impl": "reference",
            "config": {"workload": f"random CX-block, {args.qubits} qubits, {args.blocks} blocks, complex64",
                       "n_qubits": args.qubits, "blocks": args.blocks, "gates": 3 * args.blocks},
-           "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "port", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "port", "sample": sample,
+                            "host": host_info()},
            "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -265,7 +282,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         cpu = {"value": v, "unit": "gates/s", "cores": 1, "kind": "port",
                "sample": (f"oracle port of statevec.run_circuit (numpy fp32, 1 core), RandomSpec("
                           f"{args.cpu_sample_qubits}, {args.cpu_sample_blocks}, seed 0) = {g_s} gates in {dt:.2f} s, "
-                          f"per-gate time scaled x2^{n - args.cpu_sample_qubits} to {n} qubits")}
+                          f"per-gate time scaled x2^{n - args.cpu_sample_qubits} to {n} qubits"),
+               "host": host_info()}
     out = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
