@@ -8,7 +8,7 @@
 // Sampler (two-level inverse-CDF, no full-length prefix array):
 //   1. chunk_sums:  one HBM read of the state; fp64 sums per 256-amp sub-block
 //                   and per 16384-amp chunk (sub-block sums kept in workspace).
-//   2. chunk_scan:  exclusive prefix of the chunk sums (single CTA) -> total.
+//   2. scan:        CUB exclusive prefix of the chunk sums (+ one 0) -> total.
 //   3. draw:        per shot, u*total -> binary search over chunk prefixes ->
 //                   linear walk over <= 64 sub-block sums -> <= 256 amplitudes.
 //   4. CUB radix sort of the outcome indices + run-length encode -> (index, count).
@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cub/cub.cuh>
 #include <cmath>
 
@@ -174,10 +175,12 @@ static SLayout layout(int64_t n_amps, int64_t shots) {
                                    (int)ns, 0, bits_for(n_amps));
     cub::DeviceRunLengthEncode::Encode(nullptr, rle_b, (const int64_t*)nullptr, (int64_t*)nullptr, (int64_t*)nullptr,
                                        (int64_t*)nullptr, (int)ns);
-    L.cub_bytes = sort_b > rle_b ? sort_b : rle_b;
+    size_t scan_b = 0;  // exclusive scan of the n_ch + 1 chunk sums (the last one 0 -> the total)
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (const double*)nullptr, (double*)nullptr, (int)(L.n_ch + 1));
+    L.cub_bytes = std::max(std::max(sort_b, rle_b), scan_b);
     size_t o = 0;
     L.off_sub = o; o += align256(L.n_sub * 8);
-    L.off_bsum = o; o += align256(L.n_ch * 8);
+    L.off_bsum = o; o += align256((L.n_ch + 1) * 8);
     L.off_bpre = o; o += align256((L.n_ch + 1) * 8);
     L.off_draw = o; o += align256(ns * 8);
     L.off_sorted = o; o += align256(ns * 8);
@@ -200,6 +203,23 @@ const int64_t* sample_nunique_ptr(const void* ws, int64_t n_amps, int64_t shots)
 }
 
 // ----------------------------------------------------------------- sampler kernels
+// 16-byte vector of amplitudes and its probability mass
+template <typename T2>
+struct Vec16;
+template <>
+struct Vec16<float2> {
+    using T = float4;  // two complex64 amplitudes
+    __device__ static double prob(float4 v) {
+        const double a = v.x, b = v.y, c = v.z, d = v.w;
+        return (a * a + b * b) + (c * c + d * d);
+    }
+};
+template <>
+struct Vec16<double2> {
+    using T = double2;  // one complex128 amplitude
+    __device__ static double prob(double2 v) { return v.x * v.x + v.y * v.y; }
+};
+
 // one CTA (256 threads = 8 warps) per chunk; warp w sums sub-blocks w, w+8, ...
 template <typename T2>
 __global__ void chunk_sums(const T2* __restrict__ psi, int64_t sb, int64_t ch, double* __restrict__ sub,
@@ -211,7 +231,20 @@ __global__ void chunk_sums(const T2* __restrict__ psi, int64_t sb, int64_t ch, d
     for (int64_t j = w; j < nsb; j += 8) {
         const T2* p = psi + c * ch + j * sb;
         double acc = 0;
-        for (int64_t i = l; i < sb; i += 32) acc += prob(p[i]);
+        if (sb == kSub) {
+            // lane l owns amplitudes [8l, 8l + 8) of the sub-block: every 16-byte
+            // load is issued before the first use (the scalar loop kept one in flight)
+            using V = typename Vec16<T2>::T;
+            constexpr int kA = 16 / (int)sizeof(T2);  // amplitudes per vector
+            const V* pv = reinterpret_cast<const V*>(p) + l * (8 / kA);
+            V v[8 / kA];
+#pragma unroll
+            for (int k = 0; k < 8 / kA; ++k) v[k] = __ldcs(pv + k);
+#pragma unroll
+            for (int k = 0; k < 8 / kA; ++k) acc += Vec16<T2>::prob(v[k]);
+        } else {
+            for (int64_t i = l; i < sb; i += 32) acc += prob(p[i]);
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (l == 0) sub[c * nsb + j] = acc;
@@ -224,31 +257,8 @@ __global__ void chunk_sums(const T2* __restrict__ psi, int64_t sb, int64_t ch, d
         double t = 0;
         for (int i = 0; i < 8; ++i) t += ws[i];
         bsum[c] = t;
+        if (c == 0) bsum[gridDim.x] = 0.0;  // the scan's extra element
     }
-}
-
-// exclusive prefix of n doubles with one CTA of 1024 threads; out[n] = total
-__global__ void chunk_scan(const double* __restrict__ in, int64_t n, double* __restrict__ out) {
-    __shared__ double part[1024];
-    const int t = threadIdx.x;
-    const int64_t per = (n + 1023) / 1024;
-    const int64_t b = t * per, e = (b + per < n) ? b + per : n;
-    double s = 0;
-    for (int64_t i = b; i < e; ++i) s += in[i];
-    part[t] = s;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan
-        const double v = t >= off ? part[t - off] : 0.0;
-        __syncthreads();
-        part[t] += v;
-        __syncthreads();
-    }
-    double run = t ? part[t - 1] : 0.0;
-    for (int64_t i = b; i < e; ++i) {
-        out[i] = run;
-        run += in[i];
-    }
-    if (t == 1023) out[n] = part[1023];
 }
 
 __device__ __forceinline__ uint32_t mulhilo(uint32_t a, uint32_t b, uint32_t& hi) {
@@ -328,7 +338,9 @@ cudaError_t sample_prefix(const void* psi, int64_t n_amps, int dtype, void* ws, 
     double* bpre = reinterpret_cast<double*>(w + L.off_bpre);
     if (dtype == 0) chunk_sums<<<(unsigned)L.n_ch, 256, 0, st>>>(static_cast<const float2*>(psi), L.sb, L.ch, sub, bsum);
     else chunk_sums<<<(unsigned)L.n_ch, 256, 0, st>>>(static_cast<const double2*>(psi), L.sb, L.ch, sub, bsum);
-    chunk_scan<<<1, 1024, 0, st>>>(bsum, L.n_ch, bpre);
+    size_t tb = L.cub_bytes;  // bsum[n_ch] = 0 (chunk_sums), so bpre[n_ch] = the total
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(w + L.off_cub, tb, bsum, bpre, (int)(L.n_ch + 1), st);
+    if (e != cudaSuccess) return e;
     (void)total_dev;
     return cudaGetLastError();
 }
