@@ -11,10 +11,13 @@
 //   2. scan:        CUB exclusive prefix of the chunk sums (+ one 0) -> total.
 //   3. draw:        per shot, u*total -> binary search over chunk prefixes ->
 //                   linear walk over <= 64 sub-block sums -> <= 256 amplitudes.
-//   4. CUB radix sort of the outcome indices + run-length encode -> (index, count).
-// Uniforms come from a counter-based Philox4x32-10 stream (seed, shot) or from
-// the caller (numpy's default_rng(seed).random(shots) reproduces the reference's
-// Generator.choice draws exactly up to fp64 rounding of the cdf).
+//   4. (caller uniforms only) CUB radix sort of the outcomes; run-length encode
+//      -> (index, count).
+// Uniforms come from a counter-based Philox4x32-10 stream (seed, shot) turned into
+// ascending order statistics (exponential spacings: no sort of the outcomes), or
+// from the caller (numpy's default_rng(seed).random(shots) reproduces the
+// reference's Generator.choice draws exactly up to fp64 rounding of the cdf;
+// those outcomes are radix-sorted before the run-length encode).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -151,7 +154,7 @@ constexpr int64_t kChunk = 16384;  // amplitudes per chunk (64 sub-blocks)
 
 struct SLayout {
     int64_t sb, ch, n_sub, n_ch;
-    size_t off_sub, off_bsum, off_bpre, off_draw, off_sorted, off_runs, off_cub, total;
+    size_t off_sub, off_bsum, off_bpre, off_draw, off_sorted, off_exp, off_runs, off_cub, total;
     size_t cub_bytes;
 };
 
@@ -177,13 +180,16 @@ static SLayout layout(int64_t n_amps, int64_t shots) {
                                        (int64_t*)nullptr, (int)ns);
     size_t scan_b = 0;  // exclusive scan of the n_ch + 1 chunk sums (the last one 0 -> the total)
     cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (const double*)nullptr, (double*)nullptr, (int)(L.n_ch + 1));
-    L.cub_bytes = std::max(std::max(sort_b, rle_b), scan_b);
+    size_t cum_b = 0;  // inclusive scan of shots + 1 exponential spacings (sorted uniforms)
+    cub::DeviceScan::InclusiveSum(nullptr, cum_b, (const double*)nullptr, (double*)nullptr, (int)(ns + 1));
+    L.cub_bytes = std::max(std::max(sort_b, rle_b), std::max(scan_b, cum_b));
     size_t o = 0;
     L.off_sub = o; o += align256(L.n_sub * 8);
     L.off_bsum = o; o += align256((L.n_ch + 1) * 8);
     L.off_bpre = o; o += align256((L.n_ch + 1) * 8);
     L.off_draw = o; o += align256(ns * 8);
-    L.off_sorted = o; o += align256(ns * 8);
+    L.off_sorted = o; o += align256((ns + 1) * 8);
+    L.off_exp = o; o += align256((ns + 1) * 8);
     L.off_runs = o; o += align256(8);
     L.off_cub = o; o += align256(L.cub_bytes);
     L.total = o;
@@ -287,13 +293,24 @@ __device__ __forceinline__ double philox_uniform(uint64_t seed, uint64_t ctr) {
     return (double)(x >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// Exp(1) variates from the Philox stream: their running sums S_1..S_{N+1} give the
+// order statistics of N uniforms as S_k / S_{N+1} (exactly distributed as sorted
+// uniforms), so the draws come out in index order and need no sort
+__global__ void expo_kernel(uint64_t seed, int64_t m, double* __restrict__ out) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m; s += (int64_t)gridDim.x * blockDim.x)
+        out[s] = -log1p(-philox_uniform(seed, (uint64_t)s));
+}
+
+// uni = caller uniforms (any order), or the running exponential sums with their
+// total at uni_total (ascending uniforms); out[s] = the outcome of draw s
 template <typename T2>
-__global__ void draw_kernel(const T2* __restrict__ psi, int64_t shots, uint64_t seed, const double* __restrict__ uni,
-                            const double* __restrict__ sub, const double* __restrict__ bpre, int64_t n_ch, int64_t sb,
-                            int64_t ch, unsigned long long* __restrict__ out) {
+__global__ void draw_kernel(const T2* __restrict__ psi, int64_t shots, const double* __restrict__ uni,
+                            const double* __restrict__ uni_total, const double* __restrict__ sub,
+                            const double* __restrict__ bpre, int64_t n_ch, int64_t sb, int64_t ch,
+                            unsigned long long* __restrict__ out) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= shots) return;
-    const double u = uni ? uni[s] : philox_uniform(seed, (uint64_t)s);
+    const double u = uni_total ? uni[s] / *uni_total : uni[s];
     const double tot = bpre[n_ch];
     const double target = u * tot;
     // first chunk c with bpre[c+1] > target  (searchsorted side='right')
@@ -355,19 +372,38 @@ cudaError_t sample_draw(const void* psi, int64_t n_amps, int dtype, int64_t shot
     auto* draws = reinterpret_cast<unsigned long long*>(w + L.off_draw);
     auto* sorted = reinterpret_cast<unsigned long long*>(w + L.off_sorted);
     const unsigned blocks = (unsigned)((shots + 255) / 256);
+    const double* uni = uniforms;
+    const double* uni_total = nullptr;
+    cudaError_t e;
+    size_t tb = L.cub_bytes;
+    if (!uniforms) {  // Philox stream as ascending uniforms (exponential spacings)
+        double* ex = reinterpret_cast<double*>(w + L.off_exp);
+        double* cum = reinterpret_cast<double*>(w + L.off_sorted);
+        const int64_t m = shots + 1;
+        const unsigned eb = (unsigned)std::min<int64_t>((m + 255) / 256, 148 * 16);
+        expo_kernel<<<eb, 256, 0, st>>>(seed, m, ex);
+        e = cub::DeviceScan::InclusiveSum(w + L.off_cub, tb, ex, cum, (int)m, st);
+        if (e != cudaSuccess) return e;
+        uni = cum;
+        uni_total = cum + shots;
+    }
     if (dtype == 0)
-        draw_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(psi), shots, seed, uniforms, sub, bpre, L.n_ch,
+        draw_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(psi), shots, uni, uni_total, sub, bpre, L.n_ch,
                                             L.sb, L.ch, draws);
     else
-        draw_kernel<<<blocks, 256, 0, st>>>(static_cast<const double2*>(psi), shots, seed, uniforms, sub, bpre,
+        draw_kernel<<<blocks, 256, 0, st>>>(static_cast<const double2*>(psi), shots, uni, uni_total, sub, bpre,
                                             L.n_ch, L.sb, L.ch, draws);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    size_t tb = L.cub_bytes;
-    e = cub::DeviceRadixSort::SortKeys(w + L.off_cub, tb, draws, sorted, (int)shots, 0, bits_for(n_amps), st);
-    if (e != cudaSuccess) return e;
+    const unsigned long long* keys = draws;  // ascending already for the Philox stream
+    if (uniforms) {
+        tb = L.cub_bytes;
+        e = cub::DeviceRadixSort::SortKeys(w + L.off_cub, tb, draws, sorted, (int)shots, 0, bits_for(n_amps), st);
+        if (e != cudaSuccess) return e;
+        keys = sorted;
+    }
     tb = L.cub_bytes;
-    e = cub::DeviceRunLengthEncode::Encode(w + L.off_cub, tb, reinterpret_cast<const int64_t*>(sorted), out_idx,
+    e = cub::DeviceRunLengthEncode::Encode(w + L.off_cub, tb, reinterpret_cast<const int64_t*>(keys), out_idx,
                                            out_cnt, n_unique_dev, (int)shots, st);
     return e;
 }
