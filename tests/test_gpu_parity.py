@@ -274,6 +274,17 @@ def test_sampler_edge_cases():
     sv.apply_1q(st, GateKind.H, 16)
     t = sv.sample_counts(st, 50000, 1)
     assert set(t.indices.tolist()) <= {0, 1 << 16}
+    # one shot; and the Philox path's ascending-order-statistics draws on a skewed
+    # distribution (p = sin^2(0.05) ~ 2.5e-3 on |1>): unique ascending outcomes, exact total
+    t = sv.sample_counts(st, 1, 9)
+    assert t.total == 1 and sum(t.values.tolist()) == 1
+    st = sv.init_zero_state(1, "fp32")
+    sv.apply_1q(st, GateKind.RY, 0, 0.1)
+    shots = 400_000
+    t = sv.sample_counts(st, shots, 11)
+    assert t.indices.tolist() == [0, 1] and sum(t.values.tolist()) == shots
+    p1 = math.sin(0.05) ** 2
+    assert abs(t.values[1] / shots - p1) <= 5 * math.sqrt(p1 * (1 - p1) / shots)
 
 # every fused-kernel instantiation (kernel_cfg = 1 + id; c64: 8 configs incl. the
 # 32/64-amplitude-per-thread ones, c128: 4) against the oracle on a mixed circuit
