@@ -36,6 +36,7 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxOps = 640;    // op words per pass
 constexpr int kMaxTph = 128;    // thread-phase entries per pass
 constexpr int kMaxPhe = 320;    // PH list entries per pass
+constexpr int kMaxUph = 64;     // PH ops per pass with tile-uniform factors
 constexpr int kMaxXfe = 256;    // XF list entries per pass
 constexpr int kLaneBits = 5;
 constexpr int kMaxRegBits = 6;
@@ -66,7 +67,8 @@ struct CoefCap<double> {
 //   fam 1 CD   + T            complex 2x2 (coef: 8 reals, row major)
 //   fam 2 PH   + T            x e where parity(W & p) ^ f = 1, W = e_T; the phase is
 //                             the product of a list of predicated entries (ph[]):
-//                             word bits 8-15 = entry count, 16-31 = first entry;
+//                             word bits 8-14 = entry count, 15 = tile-uniform slot,
+//                             16-31 = first entry;
 //                             entry 0 is unconditional (its cmask is ignored)
 //   fam 3 RDW, 4 RDV  + pair index (T, C)   the W / V forms of RD
 //   fam 5 PHW  + tri index (T > C)   PH with W = e_T + e_C
@@ -111,7 +113,11 @@ struct Entry {
 };
 
 // one factor of an OC_PH phase: e where bit `pos` of the thread's global index
-// is 1 (every predicate on this path is a single control qubit)
+// is 1 (every predicate on this path is a single control qubit).  Entry 0 of a
+// word's list is its unconditional factor; when word bit 15 is set its pad is the
+// word's tile-uniform slot: the product of the word's factors whose control is a tile-id or
+// rank bit (the same for every thread of a tile) is computed once per tile by one
+// thread (PassDesc::uph) and read from shared memory by the op.
 template <typename Real>
 struct PhEnt {
     uint32_t pos;
@@ -143,7 +149,7 @@ struct PassDesc {
     int32_t load_direct;   // 1: load with stage 0 mapping; 0: load with stg[0] (io) then transpose
     int32_t store_direct;  // 1: store from the last stage; 0: transpose to io then store
     int32_t tile_lo32;     // 1: every tile qubit < 32 (32-bit in-tile addressing)
-    int32_t pad0;
+    int32_t n_uph;         // tile-uniform phase slots (uph)
     uint64_t n_tiles;      // 2^(n_local - k)
     uint8_t tile_q[kMaxTile];  // sorted physical positions of the tile bits
     uint8_t comp_q[48];        // local positions outside the tile, ascending (tile id bits)
@@ -154,6 +160,8 @@ struct PassDesc {
     PhEnt<Real> ph[kMaxPhe];
     uint32_t xfe[kMaxXfe];      // OC_XF list entries: control bit position | flip vector << 8
     Real coef[CoefCap<Real>::value];
+    uint32_t uph[kMaxUph];      // tile-uniform slot: first ph entry | count << 16 (last: the
+                                // other fields keep their constant-bank offsets)
 };
 
 // single-gate (unfused) op on global index bits

@@ -276,12 +276,18 @@ __device__ __forceinline__ void op_ph(T2 (&a)[1 << RB], T2 e, uint32_t F) {
 
 // the thread's phase of an OC_PH word: product of its list entries whose
 // predicate holds (e.g. all the CR1 gates of a QFT row sharing one register target)
-template <typename T2, typename Real>
+template <bool UPH, typename T2, typename Real>
 __device__ __forceinline__ T2 ph_product(const PassDesc<Real>& P, uint32_t w, uint64_t tb) {
-    const int n = (w >> 8) & 0xffu, b = w >> 16;
-    T2 e;  // entry 0 is the unconditional factor (planner: flush_ph)
+    const int n = (w >> 8) & 0x7fu, b = w >> 16;
+    T2 e;  // entry 0 is the unconditional factor (planner: emit_group)
     e.x = P.ph[b].e[0];
     e.y = P.ph[b].e[1];
+    if constexpr (UPH) {  // passes with tile-uniform slots (the kernel variant that computes them)
+        if (w & 0x8000u) {  // the tile-uniform factors, computed at the tile start (slot in entry 0's pad)
+            extern __shared__ __align__(16) unsigned char smem_raw[];
+            e = cmul(e, reinterpret_cast<const T2*>(smem_raw)[P.ph[b].pad]);
+        }
+    }
     for (int k = 1; k < n; ++k) {
         const PhEnt<Real>& E = P.ph[b + k];
         const bool on = (tb >> E.pos) & 1u;
@@ -314,7 +320,7 @@ __device__ __forceinline__ T2 ph_product(const PassDesc<Real>& P, uint32_t w, ui
 #define QGJ_ENTER(name) ((void)0)
 #endif
 #define QG_LAB(ok, code, junk) ((ok) ? (code) : 1000 + (junk))
-template <int RB, typename T2, typename Real>
+template <int RB, bool UPH, typename T2, typename Real>
 __device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<Real>& P, int o, uint64_t tb,
                                               uint32_t& F) {
     // op words are read through a running byte offset (no per-op index math) and
@@ -365,7 +371,7 @@ __device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<R
     case QG_LAB(T < RB, oc_std(F_PH, RB, T), 16 + T):                                    \
         if constexpr (T < RB) {                                                          \
             QGJ_ENTER("QGJ_PH_" #T);                                                     \
-            op_ph<RB, 1u << T, T2, Real>(a, ph_product<T2>(P, w, tb), F);                \
+            op_ph<RB, 1u << T, T2, Real>(a, ph_product<UPH, T2>(P, w, tb), F);                \
         }                                                                                \
         break;
         QG_STD(0) QG_STD(1) QG_STD(2) QG_STD(3) QG_STD(4) QG_STD(5)
@@ -387,7 +393,7 @@ __device__ __forceinline__ void run_stage_ops(T2 (&a)[1 << RB], const PassDesc<R
     case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PHW, RB, T, C), 500 + 6 * T + C):        \
         if constexpr (QG_OKP(T, C) && C < T) {                                           \
             QGJ_ENTER("QGJ_PHW_" #T "_" #C);                                             \
-            op_ph<RB, (1u << T) | (1u << C), T2, Real>(a, ph_product<T2>(P, w, tb), F);  \
+            op_ph<RB, (1u << T) | (1u << C), T2, Real>(a, ph_product<UPH, T2>(P, w, tb), F);  \
         }                                                                                \
         break;                                                                           \
     case QG_LAB(QG_OKP(T, C) && C < T, oc_tri(F_PH2, RB, T, C), 600 + 6 * T + C):        \
@@ -480,14 +486,15 @@ __device__ __forceinline__ void smem_get(const char* sm, const StageDesc& S, uin
 // per stage a thread's index bits cost a few LDS instead of bit-deposit loops.
 constexpr int kMapG = 48;   // u64 entries per mapping (32 lanes + 16 warps)
 constexpr int kMapS = 48;   // u32 entries per mapping
-__host__ __device__ constexpr size_t tables_bytes() {
-    return 4 * 256 * 8 + (kMaxStages + 1) * (kMapG * 8 + kMapS * 4);
+constexpr size_t kUphBytes = kMaxUph * 16;  // tile-uniform phase slots (T2 each), at offset 0
+__host__ __device__ constexpr size_t tables_bytes() {  // + the tile-uniform phase slots
+    return 4 * 256 * 8 + (kMaxStages + 1) * (kMapG * 8 + kMapS * 4) + kUphBytes;
 }
 
 // NBUF = 2: transposes alternate two tile buffers (one barrier each);
 // NBUF = 1: one buffer, a second barrier before it is rewritten (half the SMEM,
 // so two CTAs fit on an SM)
-template <typename Real, int RB, int WB, int NBUF>
+template <typename Real, int RB, int WB, int NBUF, bool UPH>
 __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB >= 6) ? 1 : 2)
     fused_pass_kernel(const __grid_constant__ PassDesc<Real> P, typename V2<Real>::T* __restrict__ psi,
                       uint64_t rank_bits) {
@@ -496,10 +503,12 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB 
     constexpr int NT = 32 << WB;
     constexpr int sh = sizeof(T2) == 8 ? 3 : 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    char* sm = reinterpret_cast<char*>(smem_raw);
+    // [tile-uniform phase slots (UPH variant) | tile buffer(s) | index tables]; the
+    // slots sit at a fixed address so the PH bodies need no pointer register
+    char* sm = reinterpret_cast<char*>(smem_raw) + (UPH ? kUphBytes : 0);
     const int k = P.k;
     const uint32_t buf_bytes = (uint32_t)sizeof(T2) << k;
-    uint64_t* tbase = reinterpret_cast<uint64_t*>(smem_raw + NBUF * (size_t)buf_bytes);
+    uint64_t* tbase = reinterpret_cast<uint64_t*>(sm + NBUF * (size_t)buf_bytes);
     uint64_t* tmg = tbase + 4 * 256;
     uint32_t* tms = reinterpret_cast<uint32_t*>(tmg + (kMaxStages + 1) * kMapG);
     const int ns = P.n_stages;
@@ -583,6 +592,27 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB 
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128 * l));
             }
         }
+        if constexpr (UPH) {  // tile-uniform phase slots: one thread per slot (tile-id / rank bits)
+            const uint64_t ub = base | rank_bits;
+            __syncthreads();  // every thread is done with the previous tile's slots
+            for (int u = tid; u < P.n_uph; u += NT) {
+                const uint32_t d = P.uph[u];
+                T2 e;
+                e.x = Real(1);
+                e.y = Real(0);
+                for (uint32_t i = d & 0xffffu, end = (d & 0xffffu) + (d >> 16); i < end; ++i) {
+                    const PhEnt<Real>& E = P.ph[i];
+                    if ((ub >> E.pos) & 1u) {
+                        T2 v;
+                        v.x = E.e[0];
+                        v.y = E.e[1];
+                        e = cmul(e, v);
+                    }
+                }
+                reinterpret_cast<T2*>(smem_raw)[u] = e;
+            }
+            __syncthreads();
+        }
         int cur = li;
         uint32_t F = 0;  // register flip mask (see run_round)
         for (int s = 1; s <= ns; ++s) {
@@ -597,7 +627,7 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB 
                 F = 0;
             }
             const uint64_t tb = base | rank_bits | tgb(s);
-            run_stage_ops<RB>(a, P, S.op_begin, tb, F);
+            run_stage_ops<RB, UPH>(a, P, S.op_begin, tb, F);
             if (S.tph_end > S.tph_begin) {  // thread-level phases commute with the whole stage
                 T2 ph;
                 ph.x = Real(1);
@@ -693,12 +723,12 @@ __global__ void gate_kernel(typename V2<Real>::T* __restrict__ psi, int n_local,
 }
 
 // ----------------------------------------------------------------- launchers
-template <typename Real, int RB, int WB, int NBUF = 2>
-static cudaError_t launch_fused_t(const PassDesc<Real>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
+template <typename Real, int RB, int WB, int NBUF, bool UPH>
+static cudaError_t launch_fused_u(const PassDesc<Real>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
     constexpr int threads = 32 << WB;
     const int k = RB + kLaneBits + WB;
     const size_t smem = NBUF * ((size_t)1 << k) * sizeof(typename V2<Real>::T) + tables_bytes();
-    auto kern = fused_pass_kernel<Real, RB, WB, NBUF>;
+    auto kern = fused_pass_kernel<Real, RB, WB, NBUF, UPH>;
     static int max_blocks = -1;  // per instantiation: resident CTAs per SM x SMs
     if (max_blocks < 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -713,6 +743,14 @@ static cudaError_t launch_fused_t(const PassDesc<Real>& P, void* psi, uint64_t r
     const uint64_t grid = P.n_tiles < (uint64_t)max_blocks ? P.n_tiles : (uint64_t)max_blocks;
     kern<<<(unsigned)grid, threads, smem, st>>>(P, reinterpret_cast<typename V2<Real>::T*>(psi), rank_bits);
     return cudaGetLastError();
+}
+
+// passes without tile-uniform phase slots run the variant without their per-tile
+// prologue and per-op flag test
+template <typename Real, int RB, int WB, int NBUF = 2>
+static cudaError_t launch_fused_t(const PassDesc<Real>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
+    return P.n_uph ? launch_fused_u<Real, RB, WB, NBUF, true>(P, psi, rank_bits, st)
+                   : launch_fused_u<Real, RB, WB, NBUF, false>(P, psi, rank_bits, st);
 }
 
 cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uint64_t rank_bits, cudaStream_t st) {

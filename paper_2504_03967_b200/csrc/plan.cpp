@@ -808,7 +808,7 @@ static int n_coef(const HostOp& o) {
 }
 
 // resource needs of a pass (descriptor capacity is checked by the scheduler)
-struct PassSize { int ops = 0, coef = 0, tph = 0, phe = 0, xfe = 0; };
+struct PassSize { int ops = 0, coef = 0, tph = 0, phe = 0, xfe = 0, uph = 0; };
 static PassSize pass_size(const HostPass& hp) {
     PassSize z;
     for (const HostStage& h : hp.stages) {
@@ -818,6 +818,13 @@ static PassSize pass_size(const HostPass& hp) {
             z.coef += n_coef(o);
             z.phe += (int)o.ph.size();
             z.xfe += (int)o.xf.size();
+            if (o.kind == A_PH) {  // a tile-uniform slot when some control lies outside the tile
+                bool uni = false;
+                for (size_t i = 1; i < o.ph.size(); ++i)
+                    uni |= std::find(hp.tile_q.begin(), hp.tile_q.end(), __builtin_ctzll(o.ph[i].first)) ==
+                           hp.tile_q.end();
+                z.uph += uni;
+            }
         }
     }
     return z;
@@ -828,7 +835,7 @@ static bool fits_t(const HostPass& hp) {
     const PassSize z = pass_size(hp);
     // one thread-phase slot is kept free for the plan's global phase
     return z.ops + (int)hp.stages.size() <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph &&
-           z.phe <= kMaxPhe && z.xfe <= kMaxXfe;
+           z.phe <= kMaxPhe && z.xfe <= kMaxXfe && z.uph <= kMaxUph;
 }
 static bool fits(int dtype, const HostPass& hp) {
     return dtype == QG_DTYPE_C64 ? fits_t<float>(hp) : fits_t<double>(hp);
@@ -879,12 +886,31 @@ static bool build_desc(const HostPass& hp, int n_local, PassDesc<Real>& d, std::
             } else if (o.kind == A_CXM) {
                 w = op_word(oc_cxm(hp.cfg.rb, o.t, o.c), kNoPred, 0);
             } else if (o.kind == A_PH) {
-                w = op_word(op_code(o, hp.cfg.rb), (uint32_t)o.ph.size(), (uint32_t)nph);
-                for (const auto& x : o.ph) {
+                // entry 0, then the factors controlled by tile bits (per thread); the
+                // factors controlled by tile-id / rank bits go to a tile-uniform slot
+                // (word bits 8-14 = entry count, bit 15 = has a tile-uniform slot)
+                std::vector<size_t> thr, uni;
+                for (size_t i = 1; i < o.ph.size(); ++i) {
+                    const int pos = __builtin_ctzll(o.ph[i].first);
+                    (std::find(hp.tile_q.begin(), hp.tile_q.end(), pos) != hp.tile_q.end() ? thr : uni).push_back(i);
+                }
+                if (1 + thr.size() > 127) { err = "phase list too long"; return false; }
+                w = op_word(op_code(o, hp.cfg.rb), (uint32_t)(1 + thr.size()) | (uni.empty() ? 0u : 0x80u),
+                            (uint32_t)nph);
+                auto put = [&](const std::pair<uint64_t, std::pair<double, double>>& x) {
                     d.ph[nph].pos = x.first ? (uint32_t)__builtin_ctzll(x.first) : 0u;
+                    d.ph[nph].pad = 0;
                     d.ph[nph].e[0] = (Real)x.second.first;
                     d.ph[nph].e[1] = (Real)x.second.second;
                     ++nph;
+                };
+                const int e0 = nph;
+                put(o.ph[0]);
+                for (size_t i : thr) put(o.ph[i]);
+                if (!uni.empty()) {
+                    d.ph[e0].pad = (uint32_t)d.n_uph;
+                    d.uph[d.n_uph++] = (uint32_t)nph | ((uint32_t)uni.size() << 16);
+                    for (size_t i : uni) put(o.ph[i]);
                 }
             } else {
                 w = op_word(op_code(o, hp.cfg.rb), kNoPred, (uint32_t)nc);
