@@ -592,16 +592,17 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB 
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128 * l));
             }
         }
-        if constexpr (UPH) {  // tile-uniform phase slots: one thread per slot (tile-id / rank bits)
+        if constexpr (UPH) {  // tile-uniform phase slots (tile-id / rank bit factors): one warp
+                              // per slot, its lanes splitting the factors, then a product tree
             const uint64_t ub = base | rank_bits;
             __syncthreads();  // every thread is done with the previous tile's slots
-            for (int u = tid; u < P.n_uph; u += NT) {
+            for (int u = warp; u < P.n_uph; u += NT / 32) {
                 const uint32_t d = P.uph[u];
                 T2 e;
                 e.x = Real(1);
                 e.y = Real(0);
-                for (uint32_t i = d & 0xffffu, end = (d & 0xffffu) + (d >> 16); i < end; ++i) {
-                    const PhEnt<Real>& E = P.ph[i];
+                for (uint32_t i = lane; i < (d >> 16); i += 32) {
+                    const PhEnt<Real>& E = P.ph[(d & 0xffffu) + i];
                     if ((ub >> E.pos) & 1u) {
                         T2 v;
                         v.x = E.e[0];
@@ -609,7 +610,14 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB 
                         e = cmul(e, v);
                     }
                 }
-                reinterpret_cast<T2*>(smem_raw)[u] = e;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    T2 v;
+                    v.x = __shfl_xor_sync(0xffffffffu, e.x, o);
+                    v.y = __shfl_xor_sync(0xffffffffu, e.y, o);
+                    e = cmul(e, v);
+                }
+                if (lane == 0) reinterpret_cast<T2*>(smem_raw)[u] = e;
             }
             __syncthreads();
         }
