@@ -147,6 +147,12 @@ static bool pick_cfg(int dtype, int n_local, int force_k, int force_cfg, KernelC
             if (cfgs[order[i]].k() == force_k && force_k <= n_local) { out = cfgs[order[i]]; return true; }
         return false;
     }
+    // small states (measured on B200 with tools/probe_cfg.py, random CX-block circuits):
+    // mid-size tiles beat the >= 256-tile rule below (c64 16-19 q: k = 11, 0.76 vs
+    // 1.19 ms at 16 q; c128 16-17 q: k = 10, 0.85 vs 1.26 ms; c128 20 q: k = 13, 1.95 vs 2.13 ms)
+    if (dtype == QG_DTYPE_C64 && n_local >= 16 && n_local <= 19) { out = cfgs[2]; return true; }
+    if (dtype == QG_DTYPE_C128 && n_local >= 16 && n_local <= 17) { out = cfgs[1]; return true; }
+    if (dtype == QG_DTYPE_C128 && n_local == 20) { out = cfgs[3]; return true; }
     for (int i = 0; i < nc; ++i)
         if (n_local - cfgs[order[i]].k() >= 8) { out = cfgs[order[i]]; return true; }
     for (int i = 0; i < nc; ++i)
