@@ -48,8 +48,13 @@ def _newest_input() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def _compile(src: str) -> str:
+def _compile(src: str, force: bool = True) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+    if not force and os.path.exists(obj):  # incremental: every header counts as a dependency
+        deps = [os.path.join(CSRC, f) for f in [src] + HEADERS]
+        deps += [os.path.join(ROOT, "include", "qgear_b200.h"), os.path.abspath(__file__)]
+        if os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
+            return obj
     cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-warn-spills"]
@@ -77,7 +82,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
         return OUT
     os.makedirs(BUILD, exist_ok=True)
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(_compile, SOURCES))
+        objs = list(ex.map(lambda src: _compile(src, force), SOURCES))
     cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -31,6 +31,26 @@ int cuda_fail(cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(e_, where); \
     } while (0)
 
+// Every entry point that launches work on a state makes the state's device the
+// current one for the call (a stream of device d only takes launches while d is
+// current), restoring the caller's device on return.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const void* ptr) {
+        if (!ptr) return;
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) { cudaGetLastError(); return; }
+        if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return;
+        int cur = 0;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != a.device && cudaSetDevice(a.device) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 int check_dtype(int32_t dtype) {
     return (dtype == QG_DTYPE_C64 || dtype == QG_DTYPE_C128) ? QG_OK : fail(QG_E_INVALID_ARG, "dtype must be 0 (c64) or 1 (c128)");
 }
@@ -217,6 +237,7 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
 }
 
 int qg_state_init_zero(void* state, int32_t n_local, int32_t dtype, int32_t rank, void* stream) {
+    DeviceGuard dg_(state);
     if (int rc = check_dtype(dtype)) return rc;
     if (!state || n_local < 0 || n_local > 40) return fail(QG_E_INVALID_ARG, "bad state / n_local");
     QG_CUDA(qg::launch_init_zero(state, n_local, dtype, rank, (cudaStream_t)stream), "init_zero");
@@ -225,14 +246,17 @@ int qg_state_init_zero(void* state, int32_t n_local, int32_t dtype, int32_t rank
 
 int qg_state_init_uniform(void* state, int32_t n_local, int32_t dtype, uint64_t qubit_mask, int32_t rank,
                           void* stream) {
+    DeviceGuard dg_(state);
     if (int rc = check_dtype(dtype)) return rc;
     if (!state || n_local < 0 || n_local > 40 || rank < 0) return fail(QG_E_INVALID_ARG, "bad state / n_local / rank");
+    if (qubit_mask >> n_local) return fail(QG_E_INDEX_OUT_OF_RANGE, "H-layer qubit outside the shard's local qubits");
     QG_CUDA(qg::launch_init_uniform(state, n_local, dtype, rank, qubit_mask, (cudaStream_t)stream), "init_uniform");
     return QG_OK;
 }
 
 int qg_plan_execute_segment(const qg_plan* plan, int64_t segment, void* state, int32_t rank, void* stream,
                             int32_t timed, qg_exec_stats* stats) {
+    DeviceGuard dg_(state);
     if (!plan || !state) return fail(QG_E_INVALID_ARG, "NULL argument");
     if (segment < 0 || segment >= (int64_t)plan->segs.size()) return fail(QG_E_INVALID_ARG, "segment out of range");
     if (rank < 0 || rank >= (1 << plan->g)) return fail(QG_E_BAD_WORKER_COUNT, "rank out of range");
@@ -274,6 +298,7 @@ static int single_gate(void* state, int32_t n_local, int32_t dtype, const qg::Ga
 }
 
 int qg_apply_matrix(void* state, int32_t n_local, int32_t dtype, int32_t target, const double* u, void* stream) {
+    DeviceGuard dg_(state);
     if (target < 0 || target >= n_local)
         return fail(QG_E_INDEX_OUT_OF_RANGE, "target " + std::to_string(target) + " out of range for " +
                                                  std::to_string(n_local) + " qubits");
@@ -293,6 +318,7 @@ int64_t qg_ucry_workspace_bytes(int32_t m, int32_t n_targets, int32_t dtype) {
 int qg_apply_ucry(void* state, int32_t n_local, int32_t dtype, const int32_t* addr_qubits, int32_t m,
                   const int32_t* targets, int32_t n_targets, const double* alpha_dev, void* workspace,
                   int64_t workspace_bytes, void* stream) {
+    DeviceGuard dg_(state);
     if (int rc = check_dtype(dtype)) return rc;
     if (!state || !alpha_dev || !workspace || (m > 0 && !addr_qubits) || !targets)
         return fail(QG_E_INVALID_ARG, "NULL argument");
@@ -340,6 +366,7 @@ static int check_pair(int32_t n, int32_t c, int32_t t) {
 }
 
 int qg_apply_cx(void* state, int32_t n_local, int32_t dtype, int32_t control, int32_t target, void* stream) {
+    DeviceGuard dg_(state);
     if (int rc = check_pair(n_local, control, target)) return rc;
     qg::GateOp op{};
     op.kind = 0;
@@ -352,6 +379,7 @@ int qg_apply_cx(void* state, int32_t n_local, int32_t dtype, int32_t control, in
 
 int qg_apply_cr1(void* state, int32_t n_local, int32_t dtype, int32_t control, int32_t target, double lam,
                  void* stream) {
+    DeviceGuard dg_(state);
     if (int rc = check_pair(n_local, control, target)) return rc;
     qg::GateOp op{};
     op.kind = 0;
@@ -365,6 +393,7 @@ int qg_apply_cr1(void* state, int32_t n_local, int32_t dtype, int32_t control, i
 
 int qg_norm_sq(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
                double* out_host, void* stream) {
+    DeviceGuard dg_(state);
     if (int rc = check_dtype(dtype)) return rc;
     const int parts = qg::norm_parts();
     if (!state || !workspace || !out_host || n_amps < 1) return fail(QG_E_INVALID_ARG, "NULL argument");
@@ -378,6 +407,7 @@ int qg_norm_sq(const void* state, int64_t n_amps, int32_t dtype, void* workspace
 }
 
 int qg_probabilities(const void* state, int64_t n_amps, int32_t dtype, double* probs_dev, void* stream) {
+    DeviceGuard dg_(state);
     if (int rc = check_dtype(dtype)) return rc;
     if (!state || !probs_dev || n_amps < 1) return fail(QG_E_INVALID_ARG, "NULL argument");
     QG_CUDA(qg::launch_probs(state, n_amps, dtype, probs_dev, (cudaStream_t)stream), "probabilities");
@@ -393,6 +423,7 @@ int qg_sample(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, u
               const double* uniforms_dev, double norm_tol, void* workspace, int64_t workspace_bytes,
               int64_t* out_index_dev, int64_t* out_count_dev, int64_t* n_unique_host, double* norm_sq_host,
               void* stream) {
+    DeviceGuard dg_(state);
     if (int rc = check_dtype(dtype)) return rc;
     if (shots < 1) return fail(QG_E_INVALID_ARG, "shots must be >= 1, got " + std::to_string(shots));
     if (shots > (int64_t)INT32_MAX) return fail(QG_E_INVALID_ARG, "shots > 2^31-1 not supported by this sampler");

@@ -737,12 +737,19 @@ static cudaError_t launch_fused_u(const PassDesc<Real>& P, void* psi, uint64_t r
     const int k = RB + kLaneBits + WB;
     const size_t smem = NBUF * ((size_t)1 << k) * sizeof(typename V2<Real>::T) + tables_bytes();
     auto kern = fused_pass_kernel<Real, RB, WB, NBUF, UPH>;
-    static int max_blocks = -1;  // per instantiation: resident CTAs per SM x SMs
-    if (max_blocks < 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // per instantiation AND per device (the SMEM attribute is a per-device setting):
+    // resident CTAs per SM x SMs
+    constexpr int kDevs = 64;
+    static int max_blocks_dev[kDevs] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kDevs) return cudaErrorInvalidDevice;
+    int& max_blocks = max_blocks_dev[dev];
+    if (max_blocks <= 0) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0, occ = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, occ = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
         if (e != cudaSuccess) return e;

@@ -150,9 +150,15 @@ static bool pick_cfg(int dtype, int n_local, int force_k, int force_cfg, KernelC
     // small states (measured on B200 with tools/probe_cfg.py, random CX-block circuits):
     // mid-size tiles beat the >= 256-tile rule below (c64 16-19 q: k = 11, 0.76 vs
     // 1.19 ms at 16 q; c128 16-17 q: k = 10, 0.85 vs 1.26 ms; c128 20 q: k = 13, 1.95 vs 2.13 ms)
-    if (dtype == QG_DTYPE_C64 && n_local >= 16 && n_local <= 19) { out = cfgs[2]; return true; }
-    if (dtype == QG_DTYPE_C128 && n_local >= 16 && n_local <= 17) { out = cfgs[1]; return true; }
-    if (dtype == QG_DTYPE_C128 && n_local == 20) { out = cfgs[3]; return true; }
+    // (picked by tile size, so reordering the tables cannot change the choice)
+    auto by_k = [&](int k) {
+        for (int i = 0; i < nc; ++i)
+            if (cfgs[order[i]].k() == k) { out = cfgs[order[i]]; return true; }
+        return false;
+    };
+    if (dtype == QG_DTYPE_C64 && n_local >= 16 && n_local <= 19 && by_k(11)) return true;
+    if (dtype == QG_DTYPE_C128 && n_local >= 16 && n_local <= 17 && by_k(10)) return true;
+    if (dtype == QG_DTYPE_C128 && n_local == 20 && by_k(13)) return true;
     for (int i = 0; i < nc; ++i)
         if (n_local - cfgs[order[i]].k() >= 8) { out = cfgs[order[i]]; return true; }
     for (int i = 0; i < nc; ++i)
@@ -1105,7 +1111,12 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
             if (is_diag(g)) continue;
             const int p = phys[g.t];
             if (p >= n_local && std::find(need.begin(), need.end(), p) == need.end()) need.push_back(p);
-            if ((int)need.size() == plan.g) break;
+            // at most min(g, n_local) qubits per remap: they swap with the top local positions
+            if ((int)need.size() == std::min(plan.g, n_local)) break;
+        }
+        if (n_local == 0) {  // no local position to swap a global target into
+            err = "workers = 2^n_qubits leaves no local qubit for a non-diagonal gate";
+            return QG_E_BAD_WORKER_COUNT;
         }
         if (need.empty()) { err = "planner made no progress"; return QG_E_PROTOCOL; }
         qg_remap rm{};

@@ -36,7 +36,7 @@ import torch
 
 from . import _native as N
 from . import statevec as sv
-from .errors import LengthMismatchError, PlanTooSmallError
+from .errors import IndexOutOfRangeError, LengthMismatchError, PlanTooSmallError
 from .ir import CircType, GateKind
 
 SHOTS_PER_ADDRESS = 3000
@@ -314,8 +314,13 @@ def run_gates(gate_type: np.ndarray, gate_param: np.ndarray, n_qubits: int, opti
     nb = sv._trailing_split_arrays(gt[:, 0])
     sv._check_budget(n_qubits, options.precision, options.memory_budget)
     lead, lead_mask = 0, 0
-    while lead < nb and gt[lead, 0] == GateKind.H and not (lead_mask >> int(gt[lead, 2])) & 1:
-        lead_mask |= 1 << int(gt[lead, 2])
+    while lead < nb and gt[lead, 0] == GateKind.H:
+        q = int(gt[lead, 2])
+        if not 0 <= q < n_qubits:  # the reference's _check_record order: range before anything else
+            raise IndexOutOfRangeError(f"gate {lead}: target {q} outside [0, {n_qubits})")
+        if (lead_mask >> q) & 1:
+            break
+        lead_mask |= 1 << q
         lead += 1
     if lead < 4:  # not worth a special case
         lead, lead_mask = 0, 0

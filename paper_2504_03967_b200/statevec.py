@@ -85,7 +85,14 @@ class StateVector:
 
 @dataclass
 class SimOptions:
-    """statevec.py:56-61, plus B200 knobs (defaults keep reference behaviour)."""
+    """statevec.py:56-61, plus B200 knobs.
+
+    The reference fields keep their meaning and defaults.  One default differs in
+    effect: ``sampler="philox"`` draws the shots from a device Philox stream, so
+    counts are deterministic per ``rng_seed`` but NOT the reference's PCG64
+    counts; ``sampler="numpy"`` reproduces the reference's
+    ``default_rng(seed).choice`` stream (statevec.py:229-232) exactly, up to
+    cumulative-sum rounding ties."""
 
     precision: str = "fp64"
     shots: int = 0

@@ -131,3 +131,31 @@ def test_empty_circuit_plan():
     assert plan.info["n_passes"] == 0
     got = run_program(plan)
     assert got[0] == 1 and np.count_nonzero(got) == 1
+
+
+@pytest.mark.parametrize("n,log2_ranks", [(3, 2), (5, 4), (6, 4), (4, 3), (2, 1)])
+def test_small_states_with_many_ranks(n, log2_ranks):
+    """remaps must never reach below local position 0 when 2^g > 2^(n/2)."""
+    gt, gp = random_arrays(RandomSpec(n, 40, 5))
+    ref = oracle.run_arrays(gt, gp, n, gt.shape[0], "fp64")
+    for fuse in (True, False):
+        plan = CompiledCircuit(gt, gp, n, "fp64", log2_ranks=log2_ranks, fuse=fuse)
+        for rm in plan.remaps:
+            assert all(0 <= p < plan.n_local for p in rm[1])
+        assert rel_l2(run_program(plan), ref) < 1e-12
+
+
+def test_all_qubits_global_needs_a_local_qubit():
+    gt, gp = random_arrays(RandomSpec(3, 5, 5))
+    assert isinstance(_plan_error(gt, gp, 3, log2_ranks=3), E.BadWorkerCountError)
+    # diagonal-only circuits need no remap and run with every qubit global
+    gt = np.array([[3, -1, 0], [5, 0, 1]], dtype=np.int32)
+    plan = CompiledCircuit(gt, np.array([0.3, 0.7]), 2, "fp64", log2_ranks=2)
+    assert plan.info["n_remaps"] == 0
+
+
+@pytest.mark.parametrize("precision,n,k", [("fp32", 16, 11), ("fp32", 19, 11), ("fp64", 16, 10), ("fp64", 17, 10),
+                                           ("fp64", 20, 13)])
+def test_small_state_tile_choice(precision, n, k):
+    gt, gp = random_arrays(RandomSpec(n, 20, 0))
+    assert CompiledCircuit(gt, gp, n, precision).info["tile_qubits"] == k
