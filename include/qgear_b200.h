@@ -63,7 +63,9 @@ typedef struct {
     int32_t max_stages;       /* 0 = auto; register stages per pass (SMEM transposes + 1) */
     int32_t max_cost;         /* 0 = auto; per-amplitude instruction budget of one pass */
     int32_t kernel_cfg;       /* 0 = auto; else 1 + id of the fused-kernel configuration (tuning) */
-    int32_t reserved[5];
+    int32_t jit;              /* circuit-specialised pass kernels (complex64): 0 = auto (large shards),
+                                 1 = on, -1 = off (the op-stream interpreter runs every pass) */
+    int32_t reserved[4];
 } qg_plan_opts;
 
 typedef struct {
@@ -102,6 +104,25 @@ typedef struct {
 int qg_plan_create(const int32_t* gate_type, const double* gate_param, int64_t n_gates,
                    int32_t n_qubits, const qg_plan_opts* opts, qg_plan** out);
 int qg_plan_destroy(qg_plan* plan);
+
+/* Circuit-specialised pass kernels (jit != -1): each fused pass of a complex64
+ * plan is emitted as straight-line PTX and compiled on host threads right after
+ * qg_plan_create returns; execution waits per pass, so compilation overlaps the
+ * first passes.  Status of that compilation (wait = 1 blocks until done). */
+typedef struct {
+    int64_t n_passes;         /* fused passes in the plan */
+    int64_t n_jit;            /* compiled (these run the specialised kernel) */
+    int64_t n_fallback;       /* not covered by the emitter: the interpreter runs them */
+    int64_t n_pending;
+    double compile_ms_sum;    /* emit + compile time summed over passes */
+    double compile_ms_wall;   /* plan creation -> last pass compiled */
+    int32_t threads;
+    int32_t enabled;
+} qg_jit_status;
+int qg_plan_jit_status(const qg_plan* plan, int32_t wait, qg_jit_status* out);
+/* the PTX emitted for fused pass `pass_index` (running index over the plan's fused
+ * passes); *len = bytes needed (excluding NUL); writes at most cap bytes */
+int qg_plan_pass_ptx(const qg_plan* plan, int64_t pass_index, char* buf, int64_t cap, int64_t* len);
 /* batched parameter sets (CircuitSet circuits that share one gate structure):
  * new gate_param (n_gates >= the plan's body gates, same order as at create)
  * for the same gate_type; re-emits each pass from its stored schedule (no

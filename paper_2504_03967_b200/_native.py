@@ -24,7 +24,13 @@ DTYPE_C128 = 1
 class PlanOpts(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("log2_ranks", C.c_int32), ("fuse", C.c_int32),
                 ("tile_qubits", C.c_int32), ("max_stages", C.c_int32), ("max_cost", C.c_int32),
-                ("kernel_cfg", C.c_int32), ("reserved", C.c_int32 * 5)]
+                ("kernel_cfg", C.c_int32), ("jit", C.c_int32), ("reserved", C.c_int32 * 4)]
+
+
+class JitStatus(C.Structure):
+    _fields_ = [("n_passes", C.c_int64), ("n_jit", C.c_int64), ("n_fallback", C.c_int64), ("n_pending", C.c_int64),
+                ("compile_ms_sum", C.c_double), ("compile_ms_wall", C.c_double), ("threads", C.c_int32),
+                ("enabled", C.c_int32)]
 
 
 class Qgir1Info(C.Structure):

@@ -78,7 +78,7 @@ def run_circuit_set(circuit_set: CircuitSet, options: sv.SimOptions | None = Non
             planned = key not in plans
             if planned:
                 plans[key] = sv.CompiledCircuit(gt, gp, n, options.precision, 0, options.fuse,
-                                                options.tile_qubits, options.max_stages, options.max_cost)
+                                                options.tile_qubits, options.max_stages, options.max_cost, jit=options.jit)
             else:
                 plans[key].rebind(gp[:nb])
             plan = plans[key]

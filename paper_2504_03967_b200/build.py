@@ -17,8 +17,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
-SOURCES = ["plan.cpp", "container.cpp", "capi.cu", "fused.cu", "reduce.cu", "ucry.cu"]
-HEADERS = ["desc.h", "kernels.h", "plan.h", "jt_lists.h"]
+SOURCES = ["plan.cpp", "container.cpp", "capi.cu", "fused.cu", "reduce.cu", "ucry.cu", "jit.cpp"]
+HEADERS = ["desc.h", "kernels.h", "plan.h", "jt_lists.h", "jit.h"]
 
 
 def jump_table_ok(ptx: str) -> bool:
@@ -48,11 +48,23 @@ def _newest_input() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
+def _deps(path: str, seen=None) -> list:
+    """path + every local header it includes (recursively, quoted includes only)."""
+    seen = [] if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.append(path)
+    for line in open(path, errors="replace"):
+        m = re.match(r'\s*#\s*include\s+"([^"]+)"', line)
+        if m:
+            _deps(os.path.normpath(os.path.join(os.path.dirname(path), m.group(1))), seen)
+    return seen
+
+
 def _compile(src: str, force: bool = True) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-    if not force and os.path.exists(obj):  # incremental: every header counts as a dependency
-        deps = [os.path.join(CSRC, f) for f in [src] + HEADERS]
-        deps += [os.path.join(ROOT, "include", "qgear_b200.h"), os.path.abspath(__file__)]
+    if not force and os.path.exists(obj):  # incremental: the source's own #include closure
+        deps = _deps(os.path.join(CSRC, src)) + [os.path.abspath(__file__)]
         if os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
             return obj
     cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
@@ -83,7 +95,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
     os.makedirs(BUILD, exist_ok=True)
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda src: _compile(src, force), SOURCES))
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-cudart", "static"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-cudart", "static",
+           "-L/usr/local/cuda/lib64", "-lnvptxcompiler_static", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/qgear_b200.h"
+#include "jit.h"
 #include "kernels.h"
 #include "plan.h"
 
@@ -51,6 +52,24 @@ struct DeviceGuard {
     DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
+// fused-kernel configurations the JIT emitter covers (must match launch_fused:
+// complex64 ids >= 4 are the single-buffered ones)
+int jit_nbuf(const qg_plan& p) { return p.cfg.id >= 4 ? 1 : 2; }
+
+bool jit_wanted(const qg_plan& p, int mode) {
+    if (mode < 0 || p.dtype != QG_DTYPE_C64 || p.d32.empty() || jit_nbuf(p) != 1) return false;
+    if (mode > 0) return true;
+    // auto: shards large enough that a pass takes milliseconds (compilation,
+    // ~0.2 s of one host core per pass, overlaps the execution of earlier passes)
+    return p.n_local >= 30;
+}
+
+void jit_launch(qg_plan& p, int mode) {
+    if (!jit_wanted(p, mode)) return;
+    p.jit_threads = qg::jit_default_threads();
+    p.jit = qg::jit_start(p.d32, p.cfg.rb, p.cfg.wb, jit_nbuf(p), p.jit_threads);
+}
+
 int check_dtype(int32_t dtype) {
     return (dtype == QG_DTYPE_C64 || dtype == QG_DTYPE_C128) ? QG_OK : fail(QG_E_INVALID_ARG, "dtype must be 0 (c64) or 1 (c128)");
 }
@@ -62,7 +81,10 @@ int run_segment(const qg_plan* plan, int64_t seg, void* state, int32_t rank, cud
     const int64_t shard_bytes = ((int64_t)1 << plan->n_local) * (plan->dtype == QG_DTYPE_C64 ? 8 : 16);
     for (size_t p = 0; p < passes.size(); ++p) {
         cudaError_t e;
-        if (idx[p] >= 0) {
+        qg::JitKernel* jk = (idx[p] >= 0 && plan->jit) ? plan->jit->wait(idx[p]) : nullptr;
+        if (jk) {
+            e = qg::launch_jit(*jk, plan->d32[idx[p]], state, rank_bits, st);
+        } else if (idx[p] >= 0) {
             const void* d = plan->dtype == QG_DTYPE_C64 ? (const void*)&plan->d32[idx[p]] : (const void*)&plan->d64[idx[p]];
             e = qg::launch_fused(plan->dtype, plan->cfg.id, d, state, rank_bits, st);
         } else {
@@ -105,6 +127,8 @@ int qg_plan_create(const int32_t* gate_type, const double* gate_param, int64_t n
         delete p;
         return fail(rc, err);
     }
+    p->jit_mode = o.jit;
+    jit_launch(*p, o.jit);
     *out = p;
     return QG_OK;
 }
@@ -113,13 +137,52 @@ int qg_plan_rebind(qg_plan* plan, const double* gate_param, int64_t n_gates) {
     if (!plan) return fail(QG_E_INVALID_ARG, "plan is NULL");
     std::string err;
     int rc;
+    if (plan->jit) {  // the compile workers read the descriptors being rebuilt
+        plan->jit->join(true);
+        plan->jit.reset();
+    }
     try {
         rc = qg::rebind_plan(*plan, gate_param, n_gates, err);
     } catch (const std::bad_alloc&) {
         rc = QG_E_OUT_OF_MEMORY;
         err = "out of host memory while rebinding";
     }
+    if (rc == QG_OK) jit_launch(*plan, plan->jit_mode);
     return rc == QG_OK ? QG_OK : fail(rc, err);
+}
+
+int qg_plan_jit_status(const qg_plan* plan, int32_t wait, qg_jit_status* out) {
+    if (!plan || !out) return fail(QG_E_INVALID_ARG, "NULL argument");
+    std::memset(out, 0, sizeof *out);
+    out->n_passes = (int64_t)plan->d32.size();
+    if (!plan->jit) return QG_OK;
+    qg::JitState& J = *plan->jit;
+    if (wait) J.join();
+    out->enabled = 1;
+    out->threads = plan->jit_threads;
+    out->n_jit = J.n_ok.load();
+    out->n_fallback = J.n_fallback.load();
+    out->n_pending = out->n_passes - out->n_jit - out->n_fallback;
+    out->compile_ms_sum = J.compile_us.load() / 1000.0;
+    {
+        std::lock_guard<std::mutex> lk(J.mu);
+        out->compile_ms_wall = J.wall_us / 1000.0;
+    }
+    return QG_OK;
+}
+
+int qg_plan_pass_ptx(const qg_plan* plan, int64_t pass_index, char* buf, int64_t cap, int64_t* len) {
+    if (!plan || !len) return fail(QG_E_INVALID_ARG, "NULL argument");
+    if (plan->dtype != QG_DTYPE_C64) return fail(QG_E_INVALID_ARG, "the pass emitter covers complex64 plans");
+    if (pass_index < 0 || pass_index >= (int64_t)plan->d32.size()) return fail(QG_E_INVALID_ARG, "pass_index out of range");
+    const std::string ptx = qg::jit_ptx_c64(plan->d32[pass_index], plan->cfg.rb, plan->cfg.wb, jit_nbuf(*plan), "qg_jit_pass");
+    *len = (int64_t)ptx.size();
+    if (buf && cap > 0) {
+        const int64_t n = std::min<int64_t>(cap - 1, (int64_t)ptx.size());
+        std::memcpy(buf, ptx.data(), (size_t)n);
+        buf[n] = 0;
+    }
+    return QG_OK;
 }
 
 int qg_plan_destroy(qg_plan* plan) {

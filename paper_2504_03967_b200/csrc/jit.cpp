@@ -1,0 +1,894 @@
+// jit.cpp — straight-line PTX per fused pass (see jit.h).
+//
+// The emitted kernel is fused.cu's fused_pass_kernel<float, RB, WB, NBUF,
+// false> specialised to one PassDesc: the same persistent tile loop, io
+// mapping, SMEM transposes, op semantics (desc.h) and floating-point operation
+// order, so its results are bit-identical to the interpreter's.  What the
+// specialisation removes (per tile and thread, for a 32q random CX-block pass):
+//   * the op-word fetch + jump-table dispatch of every op (~11 instructions
+//     and a dependent LDC -> BRX chain each);
+//   * run-time coefficient offsets: coefficients are constant-bank operands;
+//   * flip-vector selects where the planner's program proves the thread's flip
+//     bit is 0 (tracked statically per slot bit);
+//   * OC_CXM register moves: a permutation of registers is a rename;
+//   * X-gate / phase lists: unrolled, each predicate a constant bit position;
+//   * Gray-code address walks: an SMEM / global address is a base register
+//     plus an immediate, one base per distinct low part of the slot offsets.
+#include "jit.h"
+
+#include <nvPTXCompiler.h>
+
+#include <sched.h>
+
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <sstream>
+
+namespace qg {
+
+namespace {
+
+using PD = PassDesc<float>;
+
+int par(uint64_t x) { return __builtin_parityll(x); }
+
+std::string u64s(uint64_t v) {
+    char b[24];
+    std::snprintf(b, sizeof b, "0x%llx", (unsigned long long)v);
+    return b;
+}
+
+struct Gen {
+    const PD& P;
+    int RB, WB, NBUF, R, NT, k;
+    std::ostringstream o;
+    int nq = 0, nr = 0, nf = 0, np = 0, nl = 0;
+    int amap[64];          // slot -> %a register index (register CX moves rename)
+    uint32_t fposs = 0;    // slot bits of the flip vector F that may be 1
+    size_t off_coef, off_ph, off_tph;
+    // smem layout
+    size_t buf_bytes, tab_gb, tab_so, tab_pf;
+    // decode table: code -> (fam, T, C); fam 7 = CXM, 8 = XF, 9 = END
+    struct Dec { int fam = -1, t = -1, c = -1; };
+    std::vector<Dec> dec;
+
+    Gen(const PD& p, int rb, int wb, int nbuf) : P(p), RB(rb), WB(wb), NBUF(nbuf) {
+        R = 1 << RB;
+        NT = 32 << WB;
+        k = P.k;
+        off_coef = offsetof(PD, coef);
+        off_ph = offsetof(PD, ph);
+        off_tph = offsetof(PD, tph);
+        buf_bytes = (size_t)8 << k;
+        tab_gb = NBUF * buf_bytes;
+        tab_so = tab_gb + (size_t)(P.n_stages + 1) * NT * 8;
+        tab_pf = tab_so + (size_t)(P.n_stages + 1) * NT * 4;
+        for (int i = 0; i < R; ++i) amap[i] = i;
+        dec.resize(oc_end(RB) + 1);
+        for (int t = 0; t < RB; ++t) {
+            dec[oc_std(F_RD, RB, t)] = {F_RD, t, -1};
+            dec[oc_std(F_CD, RB, t)] = {F_CD, t, -1};
+            dec[oc_std(F_PH, RB, t)] = {F_PH, t, -1};
+            for (int c = 0; c < RB; ++c) {
+                if (c == t) continue;
+                dec[oc_pair(F_RDW, RB, t, c)] = {F_RDW, t, c};
+                dec[oc_pair(F_RDV, RB, t, c)] = {F_RDV, t, c};
+                if (c < t) {
+                    dec[oc_tri(F_PHW, RB, t, c)] = {F_PHW, t, c};
+                    dec[oc_tri(F_PH2, RB, t, c)] = {F_PH2, t, c};
+                }
+                dec[oc_cxm(RB, t, c)] = {7, t, c};
+            }
+        }
+        dec[oc_xf(RB)] = {8, -1, -1};
+        dec[oc_end(RB)] = {9, -1, -1};
+    }
+    static size_t smem_bytes(const PD& P, int rb, int wb, int nbuf) {
+        (void)rb;
+        const size_t nt = (size_t)32 << wb;
+        return nbuf * ((size_t)8 << P.k) + (size_t)(P.n_stages + 1) * nt * 12 + nt * 8;
+    }
+
+    std::string q() { return "%q" + std::to_string(nq++); }
+    std::string r() { return "%r" + std::to_string(nr++); }
+    std::string f() { return "%f" + std::to_string(nf++); }
+    std::string p() { return "%p" + std::to_string(np++); }
+    std::string lab() { return "$J" + std::to_string(nl++); }
+    std::string a(int slot) const { return "%a" + std::to_string(amap[slot]); }
+    template <class... A>
+    void L(const A&... x) {
+        o << "\t";
+        (o << ... << x);
+        o << "\n";
+    }
+
+    // ---------------------------------------------------------------- values
+    std::string ldp_f32(size_t off) {
+        std::string v = f();
+        L("ld.param.f32 ", v, ", [P+", off, "];");
+        return v;
+    }
+    std::string bc(const std::string& fv) {  // {v, v}
+        std::string v = q();
+        L("mov.b64 ", v, ", {", fv, ", ", fv, "};");
+        return v;
+    }
+    // complex multiply / multiply-add in fused.cu's exact operation order
+    std::string swp(const std::string& x) {  // {-x.y, x.x}
+        std::string xr = f(), xi = f(), n = f(), s = q();
+        L("mov.b64 {", xr, ", ", xi, "}, ", x, ";");
+        L("neg.f32 ", n, ", ", xi, ";");
+        L("mov.b64 ", s, ", {", n, ", ", xr, "};");
+        return s;
+    }
+    void c_mul(const std::string& d, const std::string& x, const std::string& mr2, const std::string& mi2) {
+        std::string s = swp(x), t = q();
+        L("mul.rn.f32x2 ", t, ", ", x, ", ", mr2, ";");
+        L("fma.rn.f32x2 ", d, ", ", s, ", ", mi2, ", ", t, ";");
+    }
+    void c_fma(const std::string& d, const std::string& acc, const std::string& x, const std::string& mr2,
+               const std::string& mi2) {
+        std::string s = swp(x), t = q();
+        L("fma.rn.f32x2 ", t, ", ", x, ", ", mr2, ", ", acc, ";");
+        L("fma.rn.f32x2 ", d, ", ", s, ", ", mi2, ", ", t, ";");
+    }
+    // packed complex e -> ({e.x, e.x}, {e.y, e.y})
+    std::pair<std::string, std::string> split_bc(const std::string& e) {
+        std::string ex = f(), ey = f();
+        L("mov.b64 {", ex, ", ", ey, "}, ", e, ";");
+        return {bc(ex), bc(ey)};
+    }
+    std::string pack(const std::string& x, const std::string& y) {
+        std::string v = q();
+        L("mov.b64 ", v, ", {", x, ", ", y, "};");
+        return v;
+    }
+    // 1 if bit `pos` of the 64-bit value v is set (u32 0/1)
+    std::string bit(const std::string& v64, int pos) {
+        std::string t = q(), u = r();
+        L("shr.b64 ", t, ", ", v64, ", ", pos, ";");
+        L("cvt.u32.u64 ", u, ", ", t, ";");
+        L("and.b32 ", u, ", ", u, ", 1;");
+        return u;
+    }
+    std::string pred_nz(const std::string& u32) {
+        std::string pp = p();
+        L("setp.ne.u32 ", pp, ", ", u32, ", 0;");
+        return pp;
+    }
+    // parity(W & F) as a predicate (F runtime)
+    std::string fpar(uint32_t W) {
+        std::string t = r(), pp = p();
+        L("and.b32 ", t, ", %F, ", W, ";");
+        L("popc.b32 ", t, ", ", t, ";");
+        L("and.b32 ", t, ", ", t, ", 1;");
+        L("setp.ne.u32 ", pp, ", ", t, ", 0;");
+        return pp;
+    }
+
+    // ---------------------------------------------------------------- ops
+    // rotation as three in-place shears on pairs {i, i ^ V}, x = parity(W & i) = 0 member
+    void p_rot(uint32_t V, uint32_t W, const std::string& sa2, const std::string& sb2) {
+        for (int pass = 0; pass < 3; ++pass)
+            for (int i = 0; i < R; ++i) {
+                if (par(W & (uint32_t)i)) continue;
+                const int j = i ^ (int)V;
+                if (pass == 1) L("fma.rn.f32x2 ", a(j), ", ", a(i), ", ", sb2, ", ", a(j), ";");
+                else L("fma.rn.f32x2 ", a(i), ", ", a(j), ", ", sa2, ", ", a(i), ";");
+            }
+    }
+    void op_rd(uint32_t V, uint32_t W, uint32_t coef) {
+        std::string m0 = ldp_f32(off_coef + 4 * coef), m1 = ldp_f32(off_coef + 4 * (coef + 1));
+        std::string sa = m0, sb = m1;
+        if (W & fposs) {
+            std::string fp = fpar(W), n0 = f(), n1 = f();
+            sa = f();
+            sb = f();
+            L("neg.f32 ", n0, ", ", m0, ";");
+            L("neg.f32 ", n1, ", ", m1, ";");
+            L("selp.f32 ", sa, ", ", n0, ", ", m0, ", ", fp, ";");
+            L("selp.f32 ", sb, ", ", n1, ", ", m1, ", ", fp, ";");
+        }
+        p_rot(V, W, bc(sa), bc(sb));
+    }
+    void op_cd(uint32_t V, uint32_t W, uint32_t coef) {
+        std::string m[8];
+        for (int i = 0; i < 8; ++i) m[i] = ldp_f32(off_coef + 4 * (coef + i));
+        std::string c[8];
+        if (W & fposs) {  // X U X: c = (m11, m10, m01, m00)
+            std::string fp = fpar(W);
+            static const int sw[8] = {6, 7, 4, 5, 2, 3, 0, 1};
+            for (int i = 0; i < 8; ++i) {
+                c[i] = f();
+                L("selp.f32 ", c[i], ", ", m[sw[i]], ", ", m[i], ", ", fp, ";");
+            }
+        } else {
+            for (int i = 0; i < 8; ++i) c[i] = m[i];
+        }
+        std::string c00r = bc(c[0]), c00i = bc(c[1]), c01r = bc(c[2]), c01i = bc(c[3]);
+        std::string c10r = bc(c[4]), c10i = bc(c[5]), c11r = bc(c[6]), c11i = bc(c[7]);
+        for (int i = 0; i < R; ++i) {
+            if (par(W & (uint32_t)i)) continue;
+            const int j = i ^ (int)V;
+            std::string ty = q(), tx = q();
+            c_mul(ty, a(j), c01r, c01i);
+            c_mul(tx, a(i), c10r, c10i);
+            c_fma(a(i), ty, a(i), c00r, c00i);
+            c_fma(a(j), tx, a(j), c11r, c11i);
+        }
+    }
+    // multiply slots with parity(W & i) == P by e (packed)
+    void p_phase(uint32_t W, int Pp, const std::string& er2, const std::string& ei2) {
+        for (int i = 0; i < R; ++i)
+            if (par(W & (uint32_t)i) == Pp) c_mul(a(i), a(i), er2, ei2);
+    }
+    void op_ph(uint32_t W, const std::string& e) {
+        auto [er2, ei2] = split_bc(e);
+        if (!(W & fposs)) {
+            p_phase(W, 1, er2, ei2);
+            return;
+        }
+        std::string fp = fpar(W), bal = r(), p0 = p(), p1 = p();
+        std::string la = lab(), lb = lab(), le = lab();
+        L("vote.sync.ballot.b32 ", bal, ", ", fp, ", 0xffffffff;");
+        L("setp.eq.u32 ", p0, ", ", bal, ", 0;");
+        L("setp.eq.u32 ", p1, ", ", bal, ", 0xffffffff;");
+        L("@", p0, " bra.uni ", la, ";");
+        L("@", p1, " bra.uni ", lb, ";");
+        {  // mixed warp: per-thread diag(d0, d1)
+            std::string ex = f(), ey = f();
+            L("mov.b64 {", ex, ", ", ey, "}, ", e, ";");
+            std::string d0x = f(), d0y = f(), d1x = f(), d1y = f();
+            L("selp.f32 ", d0x, ", ", ex, ", 0f3F800000, ", fp, ";");
+            L("selp.f32 ", d0y, ", ", ey, ", 0f00000000, ", fp, ";");
+            L("selp.f32 ", d1x, ", 0f3F800000, ", ex, ", ", fp, ";");
+            L("selp.f32 ", d1y, ", 0f00000000, ", ey, ", ", fp, ";");
+            std::string d0r = bc(d0x), d0i = bc(d0y), d1r = bc(d1x), d1i = bc(d1y);
+            for (int i = 0; i < R; ++i) {
+                if (par(W & (uint32_t)i)) c_mul(a(i), a(i), d1r, d1i);
+                else c_mul(a(i), a(i), d0r, d0i);
+            }
+            L("bra.uni ", le, ";");
+        }
+        o << la << ":\n";
+        p_phase(W, 1, er2, ei2);
+        L("bra.uni ", le, ";");
+        o << lb << ":\n";
+        p_phase(W, 0, er2, ei2);
+        o << le << ":\n";
+    }
+    // ph_product<false>: entry 0 unconditional, then predicated factors in list order
+    std::string ph_product(uint32_t w, const std::string& tb) {
+        const int n = (w >> 8) & 0x7f, b = w >> 16;
+        std::string ex = ldp_f32(off_ph + 16 * b + 8), ey = ldp_f32(off_ph + 16 * b + 12);
+        std::string e = pack(ex, ey);
+        for (int kk = 1; kk < n; ++kk) {
+            const PhEnt<float>& E = P.ph[b + kk];
+            std::string on = pred_nz(bit(tb, (int)E.pos));
+            std::string vx = f(), vy = f();
+            std::string e0 = ldp_f32(off_ph + 16 * (b + kk) + 8), e1 = ldp_f32(off_ph + 16 * (b + kk) + 12);
+            L("selp.f32 ", vx, ", ", e0, ", 0f3F800000, ", on, ";");
+            L("selp.f32 ", vy, ", ", e1, ", 0f00000000, ", on, ";");
+            std::string ne = q();
+            c_mul(ne, e, bc(vx), bc(vy));
+            e = ne;
+        }
+        return e;
+    }
+    void op_ph2(int T, int C, uint32_t coef) {
+        std::string ex = ldp_f32(off_coef + 4 * coef), ey = ldp_f32(off_coef + 4 * (coef + 1));
+        std::string er2 = bc(ex), ei2 = bc(ey);
+        auto cphase = [&]() {
+            for (int i = 0; i < R; ++i)
+                if (((i >> T) & 1) && ((i >> C) & 1)) c_mul(a(i), a(i), er2, ei2);
+        };
+        if (!(fposs & ((1u << T) | (1u << C)))) {
+            cphase();
+            return;
+        }
+        std::string ft = r(), fc = r(), any = r(), bal = r(), p0 = p();
+        L("bfe.u32 ", ft, ", %F, ", T, ", 1;");
+        L("bfe.u32 ", fc, ", %F, ", C, ", 1;");
+        L("or.b32 ", any, ", ", ft, ", ", fc, ";");
+        std::string pany = pred_nz(any);
+        L("vote.sync.ballot.b32 ", bal, ", ", pany, ", 0xffffffff;");
+        L("setp.eq.u32 ", p0, ", ", bal, ", 0;");
+        std::string la = lab(), le = lab();
+        L("@", p0, " bra.uni ", la, ";");
+        {  // r_cphase_flip: v = (bt & bc) ? e : 1 for every slot
+            std::string vr[4], vi[4];
+            for (int combo = 0; combo < 4; ++combo) {  // (slot bit T, slot bit C)
+                const int st = combo & 1, sc = combo >> 1;
+                std::string bt = r(), bcv = r(), both = r(), pp;
+                L("xor.b32 ", bt, ", ", ft, ", ", st, ";");
+                L("xor.b32 ", bcv, ", ", fc, ", ", sc, ";");
+                L("and.b32 ", both, ", ", bt, ", ", bcv, ";");
+                pp = pred_nz(both);
+                std::string x = f(), y = f();
+                L("selp.f32 ", x, ", ", ex, ", 0f3F800000, ", pp, ";");
+                L("selp.f32 ", y, ", ", ey, ", 0f00000000, ", pp, ";");
+                vr[combo] = bc(x);
+                vi[combo] = bc(y);
+            }
+            for (int i = 0; i < R; ++i) {
+                const int combo = ((i >> T) & 1) | (((i >> C) & 1) << 1);
+                c_mul(a(i), a(i), vr[combo], vi[combo]);
+            }
+            L("bra.uni ", le, ";");
+        }
+        o << la << ":\n";
+        cphase();
+        o << le << ":\n";
+    }
+    void op_xf(uint32_t w, const std::string& tb) {
+        const int n = (w >> 8) & 0xff, b = w >> 16;
+        for (int kk = 0; kk < n; ++kk) {
+            const uint32_t e = P.xfe[b + kk];
+            const uint32_t v = e >> 8;
+            std::string on = bit(tb, (int)(e & 63u)), m = r();
+            L("neg.s32 ", m, ", ", on, ";");
+            L("and.b32 ", m, ", ", m, ", ", v, ";");
+            L("xor.b32 %F, %F, ", m, ";");
+            fposs |= v;
+        }
+    }
+    void op_cxm(int T, int C) {
+        // r_cx: swap slots i and i | 1<<T for i with bit C set and bit T clear — a rename
+        for (int i = 0; i < R; ++i) {
+            if ((i & (1 << T)) || !(i & (1 << C))) continue;
+            std::swap(amap[i], amap[i | (1 << T)]);
+        }
+        if (fposs & (1u << C)) {
+            std::string t = r();
+            L("bfe.u32 ", t, ", %F, ", C, ", 1;");
+            L("shl.b32 ", t, ", ", t, ", ", T, ";");
+            L("xor.b32 %F, %F, ", t, ";");
+            fposs |= 1u << T;
+        }
+    }
+
+    // ---------------------------------------------------------------- addressing
+    // per-thread table entries (SMEM, written in the prologue)
+    std::string gb_of(int m) {
+        std::string v = q();
+        L("ld.shared.u64 ", v, ", [%tgb+", (size_t)m * NT * 8, "];");
+        return v;
+    }
+    std::string so_of(int m) {
+        std::string v = r();
+        L("ld.shared.u32 ", v, ", [%tso+", (size_t)m * NT * 4, "];");
+        return v;
+    }
+    // thread-bit masks of a mapping: global positions of lane/warp bits, SMEM byte-offset bits
+    uint64_t thread_gmask(int m) const {
+        uint64_t g = 0;
+        for (int l = 0; l < kLaneBits; ++l) g |= 1ull << P.stg[m].lane_q[l];
+        for (int w = 0; w < WB; ++w) g |= 1ull << P.stg[m].warp_q[w];
+        return g;
+    }
+    uint32_t thread_smask(int m) const {
+        uint32_t s = 0;
+        for (int l = 0; l < kLaneBits; ++l) s |= (uint32_t)P.stg[m].lane_s[l] << 3;
+        for (int w = 0; w < WB; ++w) s |= (uint32_t)P.stg[m].warp_s[w] << 3;
+        return s;
+    }
+    // 64-bit value with large constant added, reusing bases per high part
+    struct Bases {
+        std::map<uint64_t, std::string> m;
+    };
+    std::string addr64(Bases& B, const std::string& base, uint64_t off) {
+        const uint64_t hi = off >> 22, lo = off & ((1ull << 22) - 1);
+        auto it = B.m.find(hi);
+        std::string br;
+        if (it == B.m.end()) {
+            if (hi == 0) br = base;
+            else {
+                br = q();
+                L("add.s64 ", br, ", ", base, ", ", u64s(hi << 22), ";");
+            }
+            B.m[hi] = br;
+        } else {
+            br = it->second;
+        }
+        return "[" + br + "+" + u64s(lo) + "]";
+    }
+
+    // SMEM store of every slot i at (T ^ O(i)), T runtime with bits within `lm`
+    void smem_store(const std::string& T, uint32_t lm, const std::vector<uint32_t>& O) {
+        std::map<uint32_t, std::string> base;
+        for (int i = 0; i < R; ++i) {
+            const uint32_t lo = O[i] & lm, hi = O[i] & ~lm;
+            auto it = base.find(lo);
+            std::string br;
+            if (it == base.end()) {
+                br = r();
+                L("xor.b32 ", br, ", ", T, ", ", lo, ";");
+                L("add.u32 ", br, ", ", br, ", %smb;");
+                base[lo] = br;
+            } else {
+                br = it->second;
+            }
+            L("st.shared.b64 [", br, "+", hi, "], ", a(i), ";");
+        }
+    }
+    void smem_load(const std::string& T, uint32_t lm, const std::vector<uint32_t>& O) {
+        std::map<uint32_t, std::string> base;
+        for (int i = 0; i < R; ++i) {
+            const uint32_t lo = O[i] & lm, hi = O[i] & ~lm;
+            auto it = base.find(lo);
+            std::string br;
+            if (it == base.end()) {
+                br = r();
+                L("xor.b32 ", br, ", ", T, ", ", lo, ";");
+                L("add.u32 ", br, ", ", br, ", %smb;");
+                base[lo] = br;
+            } else {
+                br = it->second;
+            }
+            L("ld.shared.b64 ", a(i), ", [", br, "+", hi, "];");
+        }
+    }
+
+    // transpose from mapping m1 (with the current F) into mapping m2
+    void transpose(int m1, int m2) {
+        if (NBUF == 1) L("bar.sync 0;");
+        const StageDesc& S1 = P.stg[m1];
+        std::string T = so_of(m1);
+        uint32_t lm = thread_smask(m1);
+        for (int b = 0; b < RB; ++b) {
+            if (!(fposs & (1u << b))) continue;
+            std::string t = r();
+            L("bfe.u32 ", t, ", %F, ", b, ", 1;");
+            L("neg.s32 ", t, ", ", t, ";");
+            L("and.b32 ", t, ", ", t, ", ", S1.out_s[b], ";");
+            L("xor.b32 ", T, ", ", T, ", ", t, ";");
+            lm |= S1.out_s[b];
+        }
+        std::vector<uint32_t> O(R);
+        for (int i = 0; i < R; ++i) {
+            uint32_t v = 0;
+            for (int b = 0; b < RB; ++b)
+                if (i & (1 << b)) v ^= S1.out_s[b];
+            O[i] = v;
+        }
+        smem_store(T, lm, O);
+        L("bar.sync 0;");
+        for (int i = 0; i < R; ++i) amap[i] = i;  // register renames end with the stage
+        const StageDesc& S2 = P.stg[m2];
+        std::string T2 = so_of(m2);
+        for (int i = 0; i < R; ++i) {
+            uint32_t v = 0;
+            for (int b = 0; b < RB; ++b)
+                if (i & (1 << b)) v ^= S2.reg_s[b];
+            O[i] = v;
+        }
+        smem_load(T2, thread_smask(m2), O);
+        L("mov.u32 %F, 0;");
+        fposs = 0;
+    }
+
+    // ---------------------------------------------------------------- prologue pieces
+    // deposit the low bits of u32 x into the positions comp_q[0..n) (u64 result)
+    std::string deposit(const std::string& x, int n) {
+        std::string g = q();
+        L("mov.u64 ", g, ", 0;");
+        int i = 0;
+        while (i < n) {
+            int len = 1;
+            while (i + len < n && P.comp_q[i + len] == P.comp_q[i] + len) ++len;
+            std::string t = r(), t64 = q();
+            L("bfe.u32 ", t, ", ", x, ", ", i, ", ", len, ";");
+            L("cvt.u64.u32 ", t64, ", ", t, ";");
+            L("shl.b64 ", t64, ", ", t64, ", ", (int)P.comp_q[i], ";");
+            L("or.b64 ", g, ", ", g, ", ", t64, ";");
+            i += len;
+        }
+        return g;
+    }
+    // per-thread global bits / SMEM offset of mapping m (prologue)
+    void thread_map(int m, const std::string& lane, const std::string& warp, std::string& gb, std::string& so) {
+        const StageDesc& S = P.stg[m];
+        gb = q();
+        so = r();
+        L("mov.u64 ", gb, ", 0;");
+        L("mov.u32 ", so, ", 0;");
+        auto add = [&](const std::string& src, int bitn, int pos, uint32_t soff) {
+            std::string t = r(), t64 = q(), m2 = r();
+            L("bfe.u32 ", t, ", ", src, ", ", bitn, ", 1;");
+            L("cvt.u64.u32 ", t64, ", ", t, ";");
+            L("shl.b64 ", t64, ", ", t64, ", ", pos, ";");
+            L("or.b64 ", gb, ", ", gb, ", ", t64, ";");
+            L("neg.s32 ", m2, ", ", t, ";");
+            L("and.b32 ", m2, ", ", m2, ", ", soff, ";");
+            L("xor.b32 ", so, ", ", so, ", ", m2, ";");
+        };
+        for (int l = 0; l < kLaneBits; ++l) add(lane, l, S.lane_q[l], (uint32_t)S.lane_s[l] << 3);
+        for (int w = 0; w < WB; ++w) add(warp, w, S.warp_q[w], (uint32_t)S.warp_s[w] << 3);
+    }
+
+    std::string tb_of(int s) {  // base | rank_bits | thread bits of stage s
+        std::string g = gb_of(s), t = q();
+        L("or.b64 ", t, ", %base, %rk;");
+        L("or.b64 ", t, ", ", t, ", ", g, ";");
+        return t;
+    }
+
+    bool supported() const {
+        if (P.n_uph != 0) return false;  // tile-uniform phase slots: interpreter variant
+        if (NBUF != 1 || RB < 3 || RB > 6) return false;
+        if (P.n_stages < 1 || P.n_stages > kMaxStages) return false;
+        return true;
+    }
+
+    std::string run(const std::string& name) {
+        const int ns = P.n_stages;
+        const int li = P.load_direct ? 1 : 0;
+        const int si = P.store_direct ? ns : 0;
+        const int n_comp = 63 - __builtin_clzll(P.n_tiles);
+        uint64_t cmask = 0;
+        for (int i = 0; i < n_comp; ++i) cmask |= 1ull << P.comp_q[i];
+
+        // ---- prologue
+        L("mov.u32 %xtid, %tid.x;");
+        std::string lane = r(), warp = r();
+        L("and.b32 ", lane, ", %xtid, 31;");
+        L("shr.u32 ", warp, ", %xtid, 5;");
+        L("mov.u32 %smb, smem;");
+        L("mul.wide.u32 %q_t8, %xtid, 8;");
+        L("cvt.u32.u64 %tgb, %q_t8;");
+        L("add.u32 %tgb, %tgb, %smb;");
+        L("add.u32 %tgb, %tgb, ", tab_gb, ";");
+        L("shl.b32 %tso, %xtid, 2;");
+        L("add.u32 %tso, %tso, %smb;");
+        L("add.u32 %tso, %tso, ", tab_so, ";");
+        L("shl.b32 %tpf, %xtid, 3;");
+        L("add.u32 %tpf, %tpf, %smb;");
+        L("add.u32 %tpf, %tpf, ", tab_pf, ";");
+        for (int m = 0; m <= ns; ++m) {
+            std::string gb, so;
+            thread_map(m, lane, warp, gb, so);
+            L("st.shared.u64 [%tgb+", (size_t)m * NT * 8, "], ", gb, ";");
+            L("st.shared.u32 [%tso+", (size_t)m * NT * 4, "], ", so, ";");
+        }
+        {  // L2 prefetch offset: lanes < R cover the register runs of the io load mapping
+            const StageDesc& S = P.stg[li];
+            std::string g = q();
+            L("mov.u64 ", g, ", 0;");
+            for (int w = 0; w < WB; ++w) {
+                std::string t = r(), t64 = q();
+                L("bfe.u32 ", t, ", ", warp, ", ", w, ", 1;");
+                L("cvt.u64.u32 ", t64, ", ", t, ";");
+                L("shl.b64 ", t64, ", ", t64, ", ", (int)S.warp_q[w], ";");
+                L("or.b64 ", g, ", ", g, ", ", t64, ";");
+            }
+            for (int b = 0; b < RB; ++b) {
+                std::string t = r(), t64 = q();
+                L("bfe.u32 ", t, ", ", lane, ", ", b, ", 1;");
+                L("cvt.u64.u32 ", t64, ", ", t, ";");
+                L("shl.b64 ", t64, ", ", t64, ", ", (int)S.reg_q[b], ";");
+                L("or.b64 ", g, ", ", g, ", ", t64, ";");
+            }
+            L("st.shared.u64 [%tpf], ", g, ";");
+        }
+        L("setp.lt.u32 %pfl, ", lane, ", ", R, ";");
+        L("bar.sync 0;");
+        L("mov.u32 %ctile, %ctaid.x;");
+        L("mov.u32 %nctile, %nctaid.x;");
+        L("cvt.u64.u32 %tile, %ctile;");
+        L("cvt.u64.u32 %G, %nctile;");
+        {
+            std::string b0 = deposit("%ctile", n_comp), dg = deposit("%nctile", n_comp);
+            L("mov.u64 %base, ", b0, ";");
+            L("mov.u64 %dG, ", dg, ";");
+        }
+        L("ld.param.u64 %psi, [psi];");
+        L("ld.param.u64 %rk, [rk];");
+
+        // ---- tile loop
+        o << "$LOOP:\n";
+        L("setp.ge.u64 %pend, %tile, ", u64s(P.n_tiles), ";");
+        L("@%pend bra.uni $END;");
+        L("shl.b64 %pt, %base, 3;");
+        L("add.s64 %pt, %pt, %psi;");
+        {  // load (io or stage-1 mapping): thread bits and register bits are disjoint
+            std::string g = gb_of(li), ad = q();
+            L("shl.b64 ", ad, ", ", g, ", 3;");
+            L("add.s64 ", ad, ", ", ad, ", %pt;");
+            Bases B;
+            for (int i = 0; i < R; ++i) {
+                uint64_t off = 0;
+                for (int b = 0; b < RB; ++b)
+                    if (i & (1 << b)) off |= 1ull << P.stg[li].reg_q[b];
+                L("ld.global.cs.b64 ", a(i), ", ", addr64(B, ad, off * 8), ";");
+            }
+        }
+        L("add.s64 %ntile, %tile, %G;");
+        L("or.b64 %nbase, %base, ", u64s(~cmask), ";");
+        L("add.s64 %nbase, %nbase, %dG;");
+        L("and.b64 %nbase, %nbase, ", u64s(cmask), ";");
+        {  // warm L2 with this CTA's next tile
+            std::string pp = p(), pf = q(), ad = q();
+            L("setp.lt.u64 ", pp, ", %ntile, ", u64s(P.n_tiles), ";");
+            L("and.pred ", pp, ", ", pp, ", %pfl;");
+            std::string ls = lab();
+            L("@!", pp, " bra.uni ", ls, ";");
+            L("ld.shared.u64 ", pf, ", [%tpf];");
+            L("or.b64 ", ad, ", ", pf, ", %nbase;");
+            L("shl.b64 ", ad, ", ", ad, ", 3;");
+            L("add.s64 ", ad, ", ", ad, ", %psi;");
+            L("prefetch.global.L2 [", ad, "];");
+            L("prefetch.global.L2 [", ad, "+128];");
+            o << ls << ":\n";
+        }
+        L("mov.u32 %F, 0;");
+        fposs = 0;
+        for (int i = 0; i < R; ++i) amap[i] = i;
+        int cur = li;
+        for (int s = 1; s <= ns; ++s) {
+            const StageDesc& S = P.stg[s];
+            if (cur != s) {
+                transpose(cur, s);
+                cur = s;
+            }
+            std::string tb;  // lazily
+            auto TB = [&]() -> const std::string& {
+                if (tb.empty()) tb = tb_of(s);
+                return tb;
+            };
+            for (int oi = S.op_begin;; ++oi) {
+                const uint32_t w = P.ops[oi];
+                const uint32_t code = w & 0xffu;
+                if (code >= dec.size() || dec[code].fam < 0) return "";
+                const Dec d = dec[code];
+                if (d.fam == 9) break;
+                const uint32_t T = d.t >= 0 ? 1u << d.t : 0u, Cb = d.c >= 0 ? 1u << d.c : 0u;
+                switch (d.fam) {
+                    case F_RD: op_rd(T, T, w >> 16); break;
+                    case F_CD: op_cd(T, T, w >> 16); break;
+                    case F_PH: op_ph(T, ph_product(w, TB())); break;
+                    case F_RDW: op_rd(T, T | Cb, w >> 16); break;
+                    case F_RDV: op_rd(T | Cb, T, w >> 16); break;
+                    case F_PHW: op_ph(T | Cb, ph_product(w, TB())); break;
+                    case F_PH2: op_ph2(d.t, d.c, w >> 16); break;
+                    case 7: op_cxm(d.t, d.c); break;
+                    case 8: op_xf(w, TB()); break;
+                    default: return "";
+                }
+            }
+            if (S.tph_end > S.tph_begin) {
+                std::string one = f(), zero = f();
+                L("mov.f32 ", one, ", 0f3F800000;");
+                L("mov.f32 ", zero, ", 0f00000000;");
+                std::string ph = pack(one, zero);
+                const std::string& t = TB();
+                for (int e = S.tph_begin; e < S.tph_end; ++e) {
+                    const Entry<float>& E = P.tph[e];
+                    std::string pc = p(), ph_ = p(), m1 = q(), m2 = q();
+                    L("and.b64 ", m1, ", ", t, ", ", u64s(E.cmask), ";");
+                    L("setp.eq.u64 ", pc, ", ", m1, ", ", u64s(E.cmask), ";");
+                    L("and.b64 ", m2, ", ", t, ", ", u64s(E.qmask), ";");
+                    L("setp.ne.u64 ", ph_, ", ", m2, ", 0;");
+                    const size_t vo = off_tph + 32 * (size_t)e + 16;
+                    std::string v0 = ldp_f32(vo), v1 = ldp_f32(vo + 4), v2 = ldp_f32(vo + 8), v3 = ldp_f32(vo + 12);
+                    std::string vx = f(), vy = f(), np_ = q();
+                    L("selp.f32 ", vx, ", ", v2, ", ", v0, ", ", ph_, ";");
+                    L("selp.f32 ", vy, ", ", v3, ", ", v1, ", ", ph_, ";");
+                    c_mul(np_, ph, bc(vx), bc(vy));
+                    std::string nph = q();
+                    L("selp.b64 ", nph, ", ", np_, ", ", ph, ", ", pc, ";");
+                    ph = nph;
+                }
+                auto [r2, i2] = split_bc(ph);
+                for (int i = 0; i < R; ++i) c_mul(a(i), a(i), r2, i2);
+            }
+        }
+        if (cur != si) {
+            transpose(cur, si);
+            cur = si;
+        }
+        {  // store through the output mapping (register CX map and flips folded in)
+            const StageDesc& S = P.stg[si];
+            std::string g = gb_of(si);
+            uint64_t lm = thread_gmask(si);
+            std::string idx = g;
+            if (fposs) {
+                idx = q();
+                L("mov.b64 ", idx, ", ", g, ";");
+                for (int b = 0; b < RB; ++b) {
+                    if (!(fposs & (1u << b))) continue;
+                    std::string t = r(), t64 = q();
+                    L("bfe.u32 ", t, ", %F, ", b, ", 1;");
+                    L("cvt.u64.u32 ", t64, ", ", t, ";");
+                    L("neg.s64 ", t64, ", ", t64, ";");
+                    L("and.b64 ", t64, ", ", t64, ", ", u64s(S.out_g[b]), ";");
+                    L("xor.b64 ", idx, ", ", idx, ", ", t64, ";");
+                    lm |= S.out_g[b];
+                }
+            }
+            std::map<uint64_t, std::pair<std::string, Bases>> bases;
+            for (int i = 0; i < R; ++i) {
+                uint64_t og = 0;
+                for (int b = 0; b < RB; ++b)
+                    if (i & (1 << b)) og ^= S.out_g[b];
+                const uint64_t lo = og & lm, hi = og & ~lm;
+                auto it = bases.find(lo);
+                if (it == bases.end()) {
+                    std::string x = q();
+                    if (lo) L("xor.b64 ", x, ", ", idx, ", ", u64s(lo), ";");
+                    else L("mov.b64 ", x, ", ", idx, ";");
+                    L("shl.b64 ", x, ", ", x, ", 3;");
+                    L("add.s64 ", x, ", ", x, ", %pt;");
+                    it = bases.emplace(lo, std::make_pair(x, Bases{})).first;
+                }
+                L("st.global.cs.b64 ", addr64(it->second.second, it->second.first, hi * 8), ", ", a(i), ";");
+            }
+        }
+        L("mov.u64 %tile, %ntile;");
+        L("mov.u64 %base, %nbase;");
+        L("bra.uni $LOOP;");
+        o << "$END:\n";
+        L("ret;");
+
+        // ---- header
+        std::ostringstream h;
+        h << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
+        h << ".extern .shared .align 16 .b8 smem[];\n\n";
+        h << ".visible .entry " << name << "(\n\t.param .align 8 .b8 P[" << sizeof(PD)
+          << "],\n\t.param .u64 psi,\n\t.param .u64 rk\n)\n";
+        h << ".maxntid " << NT << ", 1, 1\n.minnctapersm " << ((WB >= 4 || RB >= 6) ? 1 : 2) << "\n{\n";
+        h << "\t.reg .b64 %a<" << R << ">;\n";
+        h << "\t.reg .b64 %q<" << (nq + 1) << ">;\n";
+        h << "\t.reg .b32 %r<" << (nr + 1) << ">;\n";
+        h << "\t.reg .f32 %f<" << (nf + 1) << ">;\n";
+        h << "\t.reg .pred %p<" << (np + 1) << ">;\n";
+        h << "\t.reg .b32 %xtid, %smb, %tgb, %tso, %tpf, %F, %ctile, %nctile;\n";
+        h << "\t.reg .b64 %q_t8, %tile, %ntile, %G, %base, %nbase, %dG, %psi, %rk, %pt;\n";
+        h << "\t.reg .pred %pfl, %pend;\n";
+        return h.str() + o.str() + "}\n";
+    }
+};
+
+}  // namespace
+
+std::string jit_ptx_c64(const PassDesc<float>& P, int rb, int wb, int nbuf, const std::string& name) {
+    Gen g(P, rb, wb, nbuf);
+    if (!g.supported()) return "";
+    return g.run(name);
+}
+
+size_t jit_smem_bytes(const PassDesc<float>& P, int rb, int wb, int nbuf) {
+    return Gen::smem_bytes(P, rb, wb, nbuf);
+}
+
+bool jit_compile(const std::string& ptx, std::vector<char>& cubin, std::string& log) {
+    nvPTXCompilerHandle h = nullptr;
+    if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
+        log = "nvPTXCompilerCreate failed";
+        return false;
+    }
+    const char* opts[] = {"--gpu-name=sm_100a", "-O3"};
+    nvPTXCompileResult rc = nvPTXCompilerCompile(h, 2, opts);
+    if (rc != NVPTXCOMPILE_SUCCESS) {
+        size_t n = 0;
+        nvPTXCompilerGetErrorLogSize(h, &n);
+        log.assign(n + 1, '\0');
+        if (n) nvPTXCompilerGetErrorLog(h, &log[0]);
+        nvPTXCompilerDestroy(&h);
+        return false;
+    }
+    size_t n = 0;
+    nvPTXCompilerGetCompiledProgramSize(h, &n);
+    cubin.resize(n);
+    nvPTXCompilerGetCompiledProgram(h, cubin.data());
+    nvPTXCompilerDestroy(&h);
+    return true;
+}
+
+JitKernel::~JitKernel() {
+    for (Dev& d : dev)
+        if (d.lib) cudaLibraryUnload(d.lib);
+}
+
+cudaError_t launch_jit(JitKernel& k, const PassDesc<float>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
+    int dv = 0;
+    cudaError_t e = cudaGetDevice(&dv);
+    if (e != cudaSuccess) return e;
+    if ((int)k.dev.size() <= dv) k.dev.resize(dv + 1);
+    JitKernel::Dev& D = k.dev[dv];
+    if (!D.kern) {
+        e = cudaLibraryLoadData(&D.lib, k.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+        if (e != cudaSuccess) return e;
+        e = cudaLibraryGetKernel(&D.kern, D.lib, k.name.c_str());
+        if (e != cudaSuccess) return e;
+        e = cudaKernelSetAttributeForDevice(D.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem, dv);
+        if (e != cudaSuccess) return e;
+        int sms = 0, occ = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(D.kern), k.threads,
+                                                          k.smem);
+        if (e != cudaSuccess) return e;
+        D.grid = sms * (occ > 0 ? occ : 1);
+    }
+    const uint64_t grid = P.n_tiles < (uint64_t)D.grid ? P.n_tiles : (uint64_t)D.grid;
+    void* args[] = {const_cast<PassDesc<float>*>(&P), &psi, &rank_bits};
+    return cudaLaunchKernel(reinterpret_cast<const void*>(D.kern), dim3((unsigned)grid), dim3(k.threads), args, k.smem,
+                            st);
+}
+
+// ---------------------------------------------------------------- per-plan compilation
+int jit_default_threads() {
+    if (const char* e = std::getenv("QG_JIT_THREADS")) {
+        const int n = std::atoi(e);
+        if (n > 0) return n;
+    }
+    cpu_set_t cs;
+    int n = 0;
+    if (sched_getaffinity(0, sizeof cs, &cs) == 0) n = CPU_COUNT(&cs);
+    if (n <= 0) n = (int)std::thread::hardware_concurrency();
+    return n < 1 ? 1 : (n > 64 ? 64 : n);
+}
+
+JitState::~JitState() { join(true); }
+
+void JitState::join(bool cancel) {
+    if (cancel) next.store((int64_t)k.size());  // workers stop after their current pass
+    for (std::thread& t : workers)
+        if (t.joinable()) t.join();
+    workers.clear();
+}
+
+JitKernel* JitState::wait(int64_t i) {
+    if (i < 0 || i >= (int64_t)k.size()) return nullptr;
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return ready[i] != 0; });
+    JitKernel* j = k[i].get();
+    return (j && j->ok) ? j : nullptr;
+}
+
+std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int rb, int wb, int nbuf, int threads) {
+    auto S = std::make_shared<JitState>();
+    const int64_t n = (int64_t)d32.size();
+    S->k.resize(n);
+    S->ready.assign(n, 0);
+    S->t0 = std::chrono::steady_clock::now();
+    if (n == 0) return S;
+    const PassDesc<float>* descs = d32.data();
+    JitState* st = S.get();
+    auto work = [st, descs, n, rb, wb, nbuf]() {
+        for (;;) {
+            const int64_t i = st->next.fetch_add(1);
+            if (i >= n) return;
+            const auto c0 = std::chrono::steady_clock::now();
+            auto jk = std::make_unique<JitKernel>();
+            jk->name = "qg_jit_pass";
+            jk->threads = 32 << wb;
+            const PassDesc<float>& P = descs[i];
+            const std::string ptx = jit_ptx_c64(P, rb, wb, nbuf, jk->name);
+            if (!ptx.empty()) {
+                jk->smem = jit_smem_bytes(P, rb, wb, nbuf);
+                jk->ok = jit_compile(ptx, jk->cubin, jk->err);
+            } else {
+                jk->err = "pass not covered by the emitter";
+            }
+            const auto c1 = std::chrono::steady_clock::now();
+            st->compile_us += std::chrono::duration_cast<std::chrono::microseconds>(c1 - c0).count();
+            (jk->ok ? st->n_ok : st->n_fallback) += 1;
+            {
+                std::lock_guard<std::mutex> lk(st->mu);
+                if (!jk->ok && st->first_error.empty()) st->first_error = jk->err;
+                st->k[i] = std::move(jk);
+                st->ready[i] = 1;
+                st->wall_us = std::chrono::duration_cast<std::chrono::microseconds>(c1 - st->t0).count();
+            }
+            st->cv.notify_all();
+        }
+    };
+    const int nt = (int)std::min<int64_t>(threads < 1 ? 1 : threads, n);
+    for (int t = 0; t < nt; ++t) S->workers.emplace_back(work);
+    return S;
+}
+
+}  // namespace qg

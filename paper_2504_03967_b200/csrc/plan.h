@@ -8,6 +8,7 @@
 #pragma once
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -80,6 +81,10 @@ struct PlanStats {
 
 }  // namespace qg
 
+namespace qg {
+struct JitState;
+}
+
 struct qg_plan {
     int n = 0, n_local = 0, g = 0, dtype = 0;
     int64_t n_body = 0;
@@ -94,6 +99,10 @@ struct qg_plan {
     std::vector<qg::PassDesc<float>> d32;
     std::vector<qg::PassDesc<double>> d64;
     std::vector<std::vector<int64_t>> desc_index;  // [seg][pass] -> index into d32/d64 (-1 unfused)
+    // circuit-specialised kernels of the d32 passes (jit.h), compiled asynchronously
+    std::shared_ptr<qg::JitState> jit;
+    int jit_threads = 0;
+    int jit_mode = 0;  // qg_plan_opts.jit
 };
 
 namespace qg {

@@ -181,7 +181,7 @@ def execute_distributed(circuit, workers: int, options: sv.SimOptions | None = N
     sv._check_budget(n, options.precision, options.memory_budget)
     g = workers.bit_length() - 1
     plan = sv.CompiledCircuit(gt, gp, n, options.precision, g, options.fuse, options.tile_qubits,
-                              options.max_stages, options.max_cost)
+                              options.max_stages, options.max_cost, jit=options.jit)
     n_local = plan.n_local
     dtype = sv._DTYPES[options.precision]
 

@@ -329,7 +329,7 @@ def run_gates(gate_type: np.ndarray, gate_param: np.ndarray, n_qubits: int, opti
     for it in items:  # plan everything first: gate errors raise before any device work
         if it[0] == "gates":
             plans.append(sv.CompiledCircuit(it[1], it[2], n_qubits, options.precision, 0, options.fuse,
-                                            options.tile_qubits, options.max_stages, options.max_cost))
+                                            options.tile_qubits, options.max_stages, options.max_cost, jit=options.jit))
     state = sv.init_zero_state(n_qubits, options.precision, options.memory_budget, options.device)
     if lead_mask:  # leading H layer on distinct qubits, applied to |0...0>: uniform superposition
         N.call("qg_state_init_uniform", C.c_void_p(state.amplitudes.data_ptr()), n_qubits,

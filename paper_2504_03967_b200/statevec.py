@@ -104,6 +104,7 @@ class SimOptions:
     tile_qubits: int = 0
     max_stages: int = 0
     max_cost: int = 0
+    jit: int = 0                 # circuit-specialised pass kernels: 0 auto (large complex64 shards), 1 on, -1 off
 
 
 @dataclass
@@ -274,7 +275,7 @@ class CompiledCircuit:
 
     def __init__(self, gate_type: np.ndarray, gate_param: np.ndarray, n_qubits: int, precision: str = "fp64",
                  log2_ranks: int = 0, fuse: bool = True, tile_qubits: int = 0, max_stages: int = 0,
-                 max_cost: int = 0, kernel_cfg: int = 0):
+                 max_cost: int = 0, kernel_cfg: int = 0, jit: int = 0):
         gt = np.ascontiguousarray(gate_type, dtype=np.int32).reshape(-1, 3)
         gp = np.ascontiguousarray(gate_param, dtype=np.float64).reshape(-1)
         if gt.shape[0] != gp.shape[0]:
@@ -286,7 +287,7 @@ class CompiledCircuit:
         self.log2_ranks = int(log2_ranks)
         opts = N.PlanOpts(dtype=_QG_DTYPE[precision], log2_ranks=log2_ranks, fuse=1 if fuse else 0,
                           tile_qubits=tile_qubits, max_stages=max_stages, max_cost=max_cost,
-                          kernel_cfg=kernel_cfg)
+                          kernel_cfg=kernel_cfg, jit=int(jit))
         h = C.c_void_p()
         self._lib = N.lib()
         N.check(self._lib.qg_plan_create(gt.ctypes.data_as(C.c_void_p), gp.ctypes.data_as(C.c_void_p),
@@ -304,6 +305,20 @@ class CompiledCircuit:
         fm = np.zeros(self.n_qubits, dtype=np.int32)
         N.check(self._lib.qg_plan_get_final_map(self._h, fm.ctypes.data_as(C.c_void_p)))
         self.final_map = fm  # logical qubit -> physical position
+
+    def jit_status(self, wait: bool = False) -> dict:
+        """Circuit-specialised pass kernels (include/qgear_b200.h qg_plan_jit_status)."""
+        st = N.JitStatus()
+        N.check(self._lib.qg_plan_jit_status(self._h, 1 if wait else 0, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in N.JitStatus._fields_}
+
+    def pass_ptx(self, index: int) -> str:
+        """PTX the emitter produces for fused pass `index` (complex64 plans)."""
+        n = C.c_int64()
+        N.check(self._lib.qg_plan_pass_ptx(self._h, int(index), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        N.check(self._lib.qg_plan_pass_ptx(self._h, int(index), buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def rebind(self, gate_param: np.ndarray) -> "CompiledCircuit":
         """New parameters for the same gate structure (a CircuitSet's batched
@@ -356,7 +371,7 @@ def compile_circuit(circuit, options: SimOptions | None = None, log2_ranks: int 
     gt, gp, n = circuit_arrays(circuit)
     _trailing_split_arrays(gt[:, 0])
     return CompiledCircuit(gt, gp, n, options.precision, log2_ranks, options.fuse, options.tile_qubits,
-                           options.max_stages, options.max_cost)
+                           options.max_stages, options.max_cost, jit=options.jit)
 
 
 def run_circuit(circuit, options: SimOptions | None = None):
@@ -373,7 +388,7 @@ def run_circuit(circuit, options: SimOptions | None = None):
             return qcrank.run_gates(gt, gp, n, options)
     _check_budget(n, options.precision, options.memory_budget)     # then TooManyQubitsError
     plan = CompiledCircuit(gt, gp, n, options.precision, 0, options.fuse, options.tile_qubits,
-                           options.max_stages, options.max_cost)   # then gate errors
+                           options.max_stages, options.max_cost, jit=options.jit)   # then gate errors
     state = init_zero_state(n, options.precision, options.memory_budget, options.device)
     plan.execute(state)
     counts = None
