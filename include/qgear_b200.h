@@ -65,7 +65,9 @@ typedef struct {
     int32_t kernel_cfg;       /* 0 = auto; else 1 + id of the fused-kernel configuration (tuning) */
     int32_t jit;              /* circuit-specialised pass kernels (complex64): 0 = auto (large shards),
                                  1 = on, -1 = off (the op-stream interpreter runs every pass) */
-    int32_t reserved[4];
+    int32_t low_qubits;       /* 0 = auto; else the lowest qubits every fused tile contains (>= 5 on
+                                 large shards): contiguous runs of 2^low_qubits amplitudes per HBM access */
+    int32_t reserved[3];
 } qg_plan_opts;
 
 typedef struct {

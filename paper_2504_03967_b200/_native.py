@@ -24,7 +24,8 @@ DTYPE_C128 = 1
 class PlanOpts(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("log2_ranks", C.c_int32), ("fuse", C.c_int32),
                 ("tile_qubits", C.c_int32), ("max_stages", C.c_int32), ("max_cost", C.c_int32),
-                ("kernel_cfg", C.c_int32), ("jit", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("kernel_cfg", C.c_int32), ("jit", C.c_int32), ("low_qubits", C.c_int32),
+                ("reserved", C.c_int32 * 3)]
 
 
 class JitStatus(C.Structure):

@@ -59,9 +59,10 @@ int jit_nbuf(const qg_plan& p) { return p.cfg.id >= 4 ? 1 : 2; }
 bool jit_wanted(const qg_plan& p, int mode) {
     if (mode < 0 || p.dtype != QG_DTYPE_C64 || p.d32.empty() || jit_nbuf(p) != 1) return false;
     if (mode > 0) return true;
-    // auto: shards large enough that a pass takes milliseconds (compilation,
-    // ~0.2 s of one host core per pass, overlaps the execution of earlier passes)
-    return p.n_local >= 30;
+    // auto: shards large enough that a pass takes longer than its share of the
+    // compilation (~0.2 s of one host core per pass, spread over the host's cores
+    // and overlapped with the execution of the earlier passes): >= 2^31 amplitudes
+    return p.n_local >= 31;
 }
 
 void jit_launch(qg_plan& p, int mode) {

@@ -48,9 +48,12 @@ struct Gen {
     int nq = 0, nr = 0, nf = 0, np = 0, nl = 0;
     int amap[64];          // slot -> %a register index (register CX moves rename)
     uint32_t fposs = 0;    // slot bits of the flip vector F that may be 1
+    int variant = 1;       // bit 0: tile loads as cp.async into the SMEM buffer, issued a tile ahead
+    int reads_left = 0;    // SMEM buffer reads left in the tile (async loads: the last one frees it)
     size_t off_coef, off_ph, off_tph;
     // smem layout
-    size_t buf_bytes, tab_gb, tab_so, tab_pf;
+    size_t buf_bytes, tab_gb, tab_pf, tab_uph;
+    static constexpr size_t kMapBytes = 576;  // 32 x u64 + 16 x u64 + 32 x u32 + 16 x u32
     // decode table: code -> (fam, T, C); fam 7 = CXM, 8 = XF, 9 = END
     struct Dec { int fam = -1, t = -1, c = -1; };
     std::vector<Dec> dec;
@@ -63,9 +66,9 @@ struct Gen {
         off_ph = offsetof(PD, ph);
         off_tph = offsetof(PD, tph);
         buf_bytes = (size_t)8 << k;
-        tab_gb = NBUF * buf_bytes;
-        tab_so = tab_gb + (size_t)(P.n_stages + 1) * NT * 8;
-        tab_pf = tab_so + (size_t)(P.n_stages + 1) * NT * 4;
+        tab_gb = NBUF * buf_bytes;                        // per mapping: [lane g | warp g | lane s | warp s]
+        tab_pf = tab_gb + (size_t)(P.n_stages + 1) * kMapBytes;  // [lane part | warp part] of the prefetch offset
+        tab_uph = tab_pf + 384;                                   // tile-uniform phase slots (float2 each)
         for (int i = 0; i < R; ++i) amap[i] = i;
         dec.resize(oc_end(RB) + 1);
         for (int t = 0; t < RB; ++t) {
@@ -89,7 +92,8 @@ struct Gen {
     static size_t smem_bytes(const PD& P, int rb, int wb, int nbuf) {
         (void)rb;
         const size_t nt = (size_t)32 << wb;
-        return nbuf * ((size_t)8 << P.k) + (size_t)(P.n_stages + 1) * nt * 12 + nt * 8;
+        (void)nt;
+        return nbuf * ((size_t)8 << P.k) + (size_t)(P.n_stages + 1) * kMapBytes + 384 + 8 * (size_t)kMaxUph;
     }
 
     std::string q() { return "%q" + std::to_string(nq++); }
@@ -265,6 +269,14 @@ struct Gen {
         const int n = (w >> 8) & 0x7f, b = w >> 16;
         std::string ex = ldp_f32(off_ph + 16 * b + 8), ey = ldp_f32(off_ph + 16 * b + 12);
         std::string e = pack(ex, ey);
+        if ((w & 0x8000u) && P.n_uph > 0) {  // the tile-uniform factors (computed at the tile start)
+            std::string u = q(), ne = q(), ad = r();
+            L("add.u32 ", ad, ", %smb, ", tab_uph + 8 * (size_t)P.ph[b].pad, ";");
+            L("ld.shared.b64 ", u, ", [", ad, "];");
+            auto [ur2, ui2] = split_bc(u);
+            c_mul(ne, e, ur2, ui2);
+            e = ne;
+        }
         for (int kk = 1; kk < n; ++kk) {
             const PhEnt<float>& E = P.ph[b + kk];
             std::string on = pred_nz(bit(tb, (int)E.pos));
@@ -353,13 +365,17 @@ struct Gen {
     // ---------------------------------------------------------------- addressing
     // per-thread table entries (SMEM, written in the prologue)
     std::string gb_of(int m) {
-        std::string v = q();
-        L("ld.shared.u64 ", v, ", [%tgb+", (size_t)m * NT * 8, "];");
+        std::string a1 = q(), a2 = q(), v = q();
+        L("ld.shared.u64 ", a1, ", [%tl8+", (size_t)m * kMapBytes, "];");
+        L("ld.shared.u64 ", a2, ", [%tw8+", (size_t)m * kMapBytes + 256, "];");
+        L("or.b64 ", v, ", ", a1, ", ", a2, ";");
         return v;
     }
     std::string so_of(int m) {
-        std::string v = r();
-        L("ld.shared.u32 ", v, ", [%tso+", (size_t)m * NT * 4, "];");
+        std::string a1 = r(), a2 = r(), v = r();
+        L("ld.shared.u32 ", a1, ", [%tl4+", (size_t)m * kMapBytes + 384, "];");
+        L("ld.shared.u32 ", a2, ", [%tw4+", (size_t)m * kMapBytes + 512, "];");
+        L("xor.b32 ", v, ", ", a1, ", ", a2, ";");
         return v;
     }
     // thread-bit masks of a mapping: global positions of lane/warp bits, SMEM byte-offset bits
@@ -468,7 +484,57 @@ struct Gen {
         smem_load(T2, thread_smask(m2), O);
         L("mov.u32 %F, 0;");
         fposs = 0;
+        after_read();
     }
+
+    // async tile load: global (mapping m, tile base register) -> SMEM buffer in
+    // mapping m's layout (the layout a transpose out of m would write)
+    void async_load(int m, const std::string& base) {
+        const StageDesc& S = P.stg[m];
+        std::string g = gb_of(m), ad = q(), pa = q();
+        L("shl.b64 ", pa, ", ", base, ", 3;");
+        L("add.s64 ", pa, ", ", pa, ", %psi;");
+        L("shl.b64 ", ad, ", ", g, ", 3;");
+        L("add.s64 ", ad, ", ", ad, ", ", pa, ";");
+        std::string T = so_of(m);
+        const uint32_t lm = thread_smask(m);
+        Bases B;
+        std::map<uint32_t, std::string> sb;
+        for (int i = 0; i < R; ++i) {
+            uint64_t off = 0;
+            uint32_t so = 0;
+            for (int b = 0; b < RB; ++b)
+                if (i & (1 << b)) {
+                    off |= 1ull << S.reg_q[b];
+                    so ^= S.reg_s[b];
+                }
+            const uint32_t lo = so & lm, hi = so & ~lm;
+            auto it = sb.find(lo);
+            if (it == sb.end()) {
+                std::string br = r();
+                L("xor.b32 ", br, ", ", T, ", ", lo, ";");
+                L("add.u32 ", br, ", ", br, ", %smb;");
+                it = sb.emplace(lo, br).first;
+            }
+            L("cp.async.ca.shared.global [", it->second, "+", hi, "], ", addr64(B, ad, off * 8), ", 8;");
+        }
+        L("cp.async.commit_group;");
+    }
+    // called after each SMEM buffer read of a tile: after the last one, every
+    // thread is done with the buffer and the next tile's loads may land in it
+    void after_read() {
+        if (!(variant & 1) || --reads_left != 0) return;
+        std::string ls = lab();
+        L("bar.sync 0;");
+        L("@%pnext bra.uni ", ls, "_go;");
+        L("bra.uni ", ls, ";");
+        o << ls << "_go:\n";
+        async_load(load_map, "%nbase");
+        o << ls << ":\n";
+    }
+    int load_map = 0;
+    int stagger_ns = 4000;
+    uint64_t cmask_ = 0;
 
     // ---------------------------------------------------------------- prologue pieces
     // deposit the low bits of u32 x into the positions comp_q[0..n) (u64 result)
@@ -489,7 +555,8 @@ struct Gen {
         return g;
     }
     // per-thread global bits / SMEM offset of mapping m (prologue)
-    void thread_map(int m, const std::string& lane, const std::string& warp, std::string& gb, std::string& so) {
+    void thread_map(int m, const std::string& lane, const std::string& warp, std::string& gb, std::string& so,
+                    bool lanes = true, bool warps = true) {
         const StageDesc& S = P.stg[m];
         gb = q();
         so = r();
@@ -505,8 +572,10 @@ struct Gen {
             L("and.b32 ", m2, ", ", m2, ", ", soff, ";");
             L("xor.b32 ", so, ", ", so, ", ", m2, ";");
         };
-        for (int l = 0; l < kLaneBits; ++l) add(lane, l, S.lane_q[l], (uint32_t)S.lane_s[l] << 3);
-        for (int w = 0; w < WB; ++w) add(warp, w, S.warp_q[w], (uint32_t)S.warp_s[w] << 3);
+        if (lanes)
+            for (int l = 0; l < kLaneBits; ++l) add(lane, l, S.lane_q[l], (uint32_t)S.lane_s[l] << 3);
+        if (warps)
+            for (int w = 0; w < WB; ++w) add(warp, w, S.warp_q[w], (uint32_t)S.warp_s[w] << 3);
     }
 
     std::string tb_of(int s) {  // base | rank_bits | thread bits of stage s
@@ -517,7 +586,6 @@ struct Gen {
     }
 
     bool supported() const {
-        if (P.n_uph != 0) return false;  // tile-uniform phase slots: interpreter variant
         if (NBUF != 1 || RB < 3 || RB > 6) return false;
         if (P.n_stages < 1 || P.n_stages > kMaxStages) return false;
         return true;
@@ -530,40 +598,51 @@ struct Gen {
         const int n_comp = 63 - __builtin_clzll(P.n_tiles);
         uint64_t cmask = 0;
         for (int i = 0; i < n_comp; ++i) cmask |= 1ull << P.comp_q[i];
+        cmask_ = cmask;
 
         // ---- prologue
         L("mov.u32 %xtid, %tid.x;");
         std::string lane = r(), warp = r();
         L("and.b32 ", lane, ", %xtid, 31;");
         L("shr.u32 ", warp, ", %xtid, 5;");
+        L("mov.u32 %xlane, ", lane, ";");
+        L("mov.u32 %xwarp, ", warp, ";");
         L("mov.u32 %smb, smem;");
-        L("mul.wide.u32 %q_t8, %xtid, 8;");
-        L("cvt.u32.u64 %tgb, %q_t8;");
-        L("add.u32 %tgb, %tgb, %smb;");
-        L("add.u32 %tgb, %tgb, ", tab_gb, ";");
-        L("shl.b32 %tso, %xtid, 2;");
-        L("add.u32 %tso, %tso, %smb;");
-        L("add.u32 %tso, %tso, ", tab_so, ";");
-        L("shl.b32 %tpf, %xtid, 3;");
-        L("add.u32 %tpf, %tpf, %smb;");
-        L("add.u32 %tpf, %tpf, ", tab_pf, ";");
+        // per-mapping tables of the lane and warp parts of a thread's global bits and
+        // SMEM offset (a thread's value = lane part | warp part); warp 0 writes the lane
+        // entries, lane 0 of every warp its warp's entries
+        auto base_reg = [&](const char* reg, const std::string& idx, int scale) {
+            L("shl.b32 ", reg, ", ", idx, ", ", scale, ";");
+            L("add.u32 ", reg, ", ", reg, ", %smb;");
+            L("add.u32 ", reg, ", ", reg, ", ", tab_gb, ";");
+        };
+        base_reg("%tl8", lane, 3);
+        base_reg("%tw8", warp, 3);
+        base_reg("%tl4", lane, 2);
+        base_reg("%tw4", warp, 2);
+        L("setp.eq.u32 %pw0, ", warp, ", 0;");
+        L("setp.eq.u32 %pl0, ", lane, ", 0;");
         for (int m = 0; m <= ns; ++m) {
-            std::string gb, so;
-            thread_map(m, lane, warp, gb, so);
-            L("st.shared.u64 [%tgb+", (size_t)m * NT * 8, "], ", gb, ";");
-            L("st.shared.u32 [%tso+", (size_t)m * NT * 4, "], ", so, ";");
+            std::string gl, sl, gw, sw;
+            thread_map(m, lane, warp, gl, sl, true, false);
+            thread_map(m, lane, warp, gw, sw, false, true);
+            L("@%pw0 st.shared.u64 [%tl8+", (size_t)m * kMapBytes, "], ", gl, ";");
+            L("@%pw0 st.shared.u32 [%tl4+", (size_t)m * kMapBytes + 384, "], ", sl, ";");
+            L("@%pl0 st.shared.u64 [%tw8+", (size_t)m * kMapBytes + 256, "], ", gw, ";");
+            L("@%pl0 st.shared.u32 [%tw4+", (size_t)m * kMapBytes + 512, "], ", sw, ";");
         }
         {  // L2 prefetch offset: lanes < R cover the register runs of the io load mapping
             const StageDesc& S = P.stg[li];
-            std::string g = q();
-            L("mov.u64 ", g, ", 0;");
+            std::string g = q(), gw = q();
+            L("mov.u64 ", gw, ", 0;");
             for (int w = 0; w < WB; ++w) {
                 std::string t = r(), t64 = q();
                 L("bfe.u32 ", t, ", ", warp, ", ", w, ", 1;");
                 L("cvt.u64.u32 ", t64, ", ", t, ";");
                 L("shl.b64 ", t64, ", ", t64, ", ", (int)S.warp_q[w], ";");
-                L("or.b64 ", g, ", ", g, ", ", t64, ";");
+                L("or.b64 ", gw, ", ", gw, ", ", t64, ";");
             }
+            L("mov.u64 ", g, ", 0;");
             for (int b = 0; b < RB; ++b) {
                 std::string t = r(), t64 = q();
                 L("bfe.u32 ", t, ", ", lane, ", ", b, ", 1;");
@@ -571,29 +650,83 @@ struct Gen {
                 L("shl.b64 ", t64, ", ", t64, ", ", (int)S.reg_q[b], ";");
                 L("or.b64 ", g, ", ", g, ", ", t64, ";");
             }
-            L("st.shared.u64 [%tpf], ", g, ";");
+            const size_t pf = tab_pf - tab_gb;
+            L("@%pw0 st.shared.u64 [%tl8+", pf, "], ", g, ";");
+            L("@%pl0 st.shared.u64 [%tw8+", pf + 256, "], ", gw, ";");
         }
         L("setp.lt.u32 %pfl, ", lane, ", ", R, ";");
         L("bar.sync 0;");
         L("mov.u32 %ctile, %ctaid.x;");
         L("mov.u32 %nctile, %nctaid.x;");
-        L("cvt.u64.u32 %tile, %ctile;");
-        L("cvt.u64.u32 %G, %nctile;");
-        {
+        if (variant & 4) {  // contiguous tile ranges per CTA: consecutive tiles are adjacent runs
+            std::string c64 = q(), g64 = q(), t0 = q(), t1 = q(), t0s = r();
+            L("cvt.u64.u32 ", c64, ", %ctile;");
+            L("cvt.u64.u32 ", g64, ", %nctile;");
+            L("mul.lo.u64 ", t0, ", ", c64, ", ", u64s(P.n_tiles), ";");
+            L("div.u64 ", t0, ", ", t0, ", ", g64, ";");
+            L("add.s64 ", t1, ", ", c64, ", 1;");
+            L("mul.lo.u64 ", t1, ", ", t1, ", ", u64s(P.n_tiles), ";");
+            L("div.u64 %tend, ", t1, ", ", g64, ";");
+            L("mov.u64 %tile, ", t0, ";");
+            L("mov.u64 %G, 1;");
+            L("cvt.u32.u64 ", t0s, ", ", t0, ";");
+            std::string b0 = deposit(t0s, n_comp);
+            L("mov.u64 %base, ", b0, ";");
+            L("mov.u64 %dG, ", u64s(n_comp > 0 ? (1ull << P.comp_q[0]) : 0), ";");
+        } else {
+            L("cvt.u64.u32 %tile, %ctile;");
+            L("cvt.u64.u32 %G, %nctile;");
+            L("mov.u64 %tend, ", u64s(P.n_tiles), ";");
             std::string b0 = deposit("%ctile", n_comp), dg = deposit("%nctile", n_comp);
             L("mov.u64 %base, ", b0, ";");
             L("mov.u64 %dG, ", dg, ";");
         }
         L("ld.param.u64 %psi, [psi];");
         L("ld.param.u64 %rk, [rk];");
+        if (variant & 64) {  // desynchronise the CTAs sharing an SM: the second half starts late
+            std::string h = r(), pp = p(), ls = lab();
+            L("shr.u32 ", h, ", %nctile, 1;");
+            L("setp.lt.u32 ", pp, ", %ctile, ", h, ";");
+            L("@", pp, " bra.uni ", ls, ";");
+            L("nanosleep.u32 ", stagger_ns, ";");
+            o << ls << ":\n";
+        }
+        load_map = li;
+        if (variant & 1) {  // the CTA's first tile
+            std::string ls = lab();
+            L("setp.ge.u64 %pend, %tile, %tend;");
+            L("@%pend bra.uni ", ls, ";");
+            async_load(li, "%base");
+            o << ls << ":\n";
+        }
 
         // ---- tile loop
         o << "$LOOP:\n";
-        L("setp.ge.u64 %pend, %tile, ", u64s(P.n_tiles), ";");
+        L("setp.ge.u64 %pend, %tile, %tend;");
         L("@%pend bra.uni $END;");
         L("shl.b64 %pt, %base, 3;");
         L("add.s64 %pt, %pt, %psi;");
-        {  // load (io or stage-1 mapping): thread bits and register bits are disjoint
+        L("add.s64 %ntile, %tile, %G;");
+        L("or.b64 %nbase, %base, ", u64s(~cmask), ";");
+        L("add.s64 %nbase, %nbase, %dG;");
+        L("and.b64 %nbase, %nbase, ", u64s(cmask), ";");
+        L("setp.lt.u64 %pnext, %ntile, %tend;");
+        if (variant & 1) {  // this tile was loaded into the SMEM buffer by cp.async; read stage 1's mapping
+            L("cp.async.wait_all;");
+            L("bar.sync 0;");
+            reads_left = 1 + (ns - 1) + (P.store_direct ? 0 : 1);
+            std::vector<uint32_t> O(R);
+            for (int i = 0; i < R; ++i) {
+                uint32_t v = 0;
+                for (int b = 0; b < RB; ++b)
+                    if (i & (1 << b)) v ^= P.stg[1].reg_s[b];
+                O[i] = v;
+            }
+            smem_load(so_of(1), thread_smask(1), O);
+            after_read();
+        } else if (variant & 32) {  // timing probe: no global memory traffic (wrong results)
+            for (int i = 0; i < R; ++i) L("mov.b64 ", a(i), ", 0;");
+        } else {  // load (io or stage-1 mapping): thread bits and register bits are disjoint
             std::string g = gb_of(li), ad = q();
             L("shl.b64 ", ad, ", ", g, ", 3;");
             L("add.s64 ", ad, ", ", ad, ", %pt;");
@@ -605,31 +738,105 @@ struct Gen {
                 L("ld.global.cs.b64 ", a(i), ", ", addr64(B, ad, off * 8), ";");
             }
         }
-        L("add.s64 %ntile, %tile, %G;");
-        L("or.b64 %nbase, %base, ", u64s(~cmask), ";");
-        L("add.s64 %nbase, %nbase, %dG;");
-        L("and.b64 %nbase, %nbase, ", u64s(cmask), ";");
-        {  // warm L2 with this CTA's next tile
+        if (!(variant & 128)) {  // warm L2 with this CTA's next tile (variant 512: the one after)
             std::string pp = p(), pf = q(), ad = q();
-            L("setp.lt.u64 ", pp, ", %ntile, ", u64s(P.n_tiles), ";");
-            L("and.pred ", pp, ", ", pp, ", %pfl;");
+            std::string tgt = "%nbase";
+            if (variant & 512) {
+                std::string t2 = q(), nb2 = q();
+                pp = p();
+                L("add.s64 ", t2, ", %ntile, %G;");
+                L("setp.lt.u64 ", pp, ", ", t2, ", %tend;");
+                L("and.pred ", pp, ", ", pp, ", %pfl;");
+                L("or.b64 ", nb2, ", %nbase, ", u64s(~cmask_), ";");
+                L("add.s64 ", nb2, ", ", nb2, ", %dG;");
+                L("and.b64 ", nb2, ", ", nb2, ", ", u64s(cmask_), ";");
+                tgt = nb2;
+            } else {
+                L("and.pred ", pp, ", %pnext, %pfl;");
+            }
             std::string ls = lab();
             L("@!", pp, " bra.uni ", ls, ";");
-            L("ld.shared.u64 ", pf, ", [%tpf];");
-            L("or.b64 ", ad, ", ", pf, ", %nbase;");
+            {
+                const size_t pfo = tab_pf - tab_gb;
+                std::string a1 = q(), a2 = q();
+                L("ld.shared.u64 ", a1, ", [%tl8+", pfo, "];");
+                L("ld.shared.u64 ", a2, ", [%tw8+", pfo + 256, "];");
+                L("or.b64 ", pf, ", ", a1, ", ", a2, ";");
+            }
+            L("or.b64 ", ad, ", ", pf, ", ", tgt, ";");
             L("shl.b64 ", ad, ", ", ad, ", 3;");
             L("add.s64 ", ad, ", ", ad, ", %psi;");
-            L("prefetch.global.L2 [", ad, "];");
-            L("prefetch.global.L2 [", ad, "+128];");
+            if (variant & 256) {
+                L("cp.async.bulk.prefetch.L2.global [", ad, "], 256;");
+            } else if (variant & 1024) {  // 64 B granules
+                for (int o2 = 0; o2 < 256; o2 += 64) L("prefetch.global.L2 [", ad, "+", o2, "];");
+            } else {
+                L("prefetch.global.L2 [", ad, "];");
+                L("prefetch.global.L2 [", ad, "+128];");
+            }
             o << ls << ":\n";
+        }
+        if (P.n_uph > 0) {  // tile-uniform phase slots: one warp per slot, lanes split the factors
+            std::string ub = q(), pb = q();
+            L("or.b64 ", ub, ", %base, %rk;");
+            L("mov.b64 ", pb, ", P;");
+            L("bar.sync 0;");  // every thread is done with the previous tile's slots
+            for (int u = 0; u < P.n_uph; ++u) {
+                const uint32_t d = P.uph[u];
+                const int first = (int)(d & 0xffffu), cnt = (int)(d >> 16);
+                std::string ls = lab(), pp = p();
+                L("setp.ne.u32 ", pp, ", %xwarp, ", u % (NT / 32), ";");
+                L("@", pp, " bra.uni ", ls, ";");
+                std::string one = f(), zero = f();
+                L("mov.f32 ", one, ", 0f3F800000;");
+                L("mov.f32 ", zero, ", 0f00000000;");
+                std::string e = pack(one, zero);
+                for (int r0 = 0; r0 < cnt; r0 += 32) {
+                    // entry first + r0 + lane (runtime index into the param space)
+                    std::string idx = r(), off = q(), ad = q(), pos = r(), ex = f(), ey = f();
+                    std::string inr = p(), on = p(), t = q(), tb = r();
+                    L("setp.lt.u32 ", inr, ", %xlane, ", cnt - r0, ";");
+                    L("add.u32 ", idx, ", %xlane, ", first + r0, ";");
+                    L("mul.wide.u32 ", off, ", ", idx, ", 16;");
+                    L("add.s64 ", ad, ", ", pb, ", ", off, ";");
+                    L("add.s64 ", ad, ", ", ad, ", ", off_ph, ";");
+                    L("@", inr, " ld.param.u32 ", pos, ", [", ad, "];");
+                    L("@", inr, " ld.param.f32 ", ex, ", [", ad, "+8];");
+                    L("@", inr, " ld.param.f32 ", ey, ", [", ad, "+12];");
+                    L("@!", inr, " mov.u32 ", pos, ", 0;");
+                    L("shr.b64 ", t, ", ", ub, ", ", pos, ";");
+                    L("cvt.u32.u64 ", tb, ", ", t, ";");
+                    L("and.b32 ", tb, ", ", tb, ", 1;");
+                    L("setp.ne.u32 ", on, ", ", tb, ", 0;");
+                    L("and.pred ", on, ", ", on, ", ", inr, ";");
+                    std::string ne = q(), ns2 = q();
+                    std::string vr = bc(ex), vi = bc(ey);
+                    c_mul(ne, e, vr, vi);
+                    L("selp.b64 ", ns2, ", ", ne, ", ", e, ", ", on, ";");
+                    e = ns2;
+                }
+                for (int o2 = 16; o2; o2 >>= 1) {  // product tree over the lanes
+                    std::string ex = f(), ey = f(), sx = f(), sy = f(), ne = q();
+                    L("mov.b64 {", ex, ", ", ey, "}, ", e, ";");
+                    L("shfl.sync.bfly.b32 ", sx, ", ", ex, ", ", o2, ", 31, 0xffffffff;");
+                    L("shfl.sync.bfly.b32 ", sy, ", ", ey, ", ", o2, ", 31, 0xffffffff;");
+                    c_mul(ne, e, bc(sx), bc(sy));
+                    e = ne;
+                }
+                std::string ad = r();
+                L("add.u32 ", ad, ", %smb, ", tab_uph + 8 * (size_t)u, ";");
+                L("@%pl0 st.shared.b64 [", ad, "], ", e, ";");
+                o << ls << ":\n";
+            }
+            L("bar.sync 0;");
         }
         L("mov.u32 %F, 0;");
         fposs = 0;
         for (int i = 0; i < R; ++i) amap[i] = i;
-        int cur = li;
+        int cur = (variant & 1) ? 1 : li;
         for (int s = 1; s <= ns; ++s) {
             const StageDesc& S = P.stg[s];
-            if (cur != s) {
+            if (cur != s && !(variant & 16)) {  // (variant 16: timing probe without transposes)
                 transpose(cur, s);
                 cur = s;
             }
@@ -642,6 +849,7 @@ struct Gen {
                 const uint32_t w = P.ops[oi];
                 const uint32_t code = w & 0xffu;
                 if (code >= dec.size() || dec[code].fam < 0) return "";
+                if ((variant & 8) && dec[code].fam != 9) continue;  // timing probe: no ops (wrong results)
                 const Dec d = dec[code];
                 if (d.fam == 9) break;
                 const uint32_t T = d.t >= 0 ? 1u << d.t : 0u, Cb = d.c >= 0 ? 1u << d.c : 0u;
@@ -658,7 +866,7 @@ struct Gen {
                     default: return "";
                 }
             }
-            if (S.tph_end > S.tph_begin) {
+            if (S.tph_end > S.tph_begin && !(variant & 8)) {
                 std::string one = f(), zero = f();
                 L("mov.f32 ", one, ", 0f3F800000;");
                 L("mov.f32 ", zero, ", 0f00000000;");
@@ -685,11 +893,11 @@ struct Gen {
                 for (int i = 0; i < R; ++i) c_mul(a(i), a(i), r2, i2);
             }
         }
-        if (cur != si) {
+        if (cur != si && !(variant & 16)) {
             transpose(cur, si);
             cur = si;
         }
-        {  // store through the output mapping (register CX map and flips folded in)
+        if (!(variant & 32)) {  // store through the output mapping (register CX map and flips folded in)
             const StageDesc& S = P.stg[si];
             std::string g = gb_of(si);
             uint64_t lm = thread_gmask(si);
@@ -738,23 +946,34 @@ struct Gen {
         h << ".extern .shared .align 16 .b8 smem[];\n\n";
         h << ".visible .entry " << name << "(\n\t.param .align 8 .b8 P[" << sizeof(PD)
           << "],\n\t.param .u64 psi,\n\t.param .u64 rk\n)\n";
-        h << ".maxntid " << NT << ", 1, 1\n.minnctapersm " << ((WB >= 4 || RB >= 6) ? 1 : 2) << "\n{\n";
+        const int min_ctas = (WB >= 4 || RB >= 6) ? 1 : ((variant & 2) ? 3 : 2);
+        h << ".maxntid " << NT << ", 1, 1\n.minnctapersm " << min_ctas << "\n{\n";
         h << "\t.reg .b64 %a<" << R << ">;\n";
         h << "\t.reg .b64 %q<" << (nq + 1) << ">;\n";
         h << "\t.reg .b32 %r<" << (nr + 1) << ">;\n";
         h << "\t.reg .f32 %f<" << (nf + 1) << ">;\n";
         h << "\t.reg .pred %p<" << (np + 1) << ">;\n";
-        h << "\t.reg .b32 %xtid, %smb, %tgb, %tso, %tpf, %F, %ctile, %nctile;\n";
-        h << "\t.reg .b64 %q_t8, %tile, %ntile, %G, %base, %nbase, %dG, %psi, %rk, %pt;\n";
-        h << "\t.reg .pred %pfl, %pend;\n";
+        h << "\t.reg .b32 %xtid, %xlane, %xwarp, %smb, %tl8, %tw8, %tl4, %tw4, %F, %ctile, %nctile;\n";
+        h << "\t.reg .b64 %tile, %tend, %ntile, %G, %base, %nbase, %dG, %psi, %rk, %pt;\n";
+        h << "\t.reg .pred %pfl, %pend, %pnext, %pw0, %pl0;\n";
         return h.str() + o.str() + "}\n";
     }
 };
 
 }  // namespace
 
+int jit_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("QG_JIT_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 std::string jit_ptx_c64(const PassDesc<float>& P, int rb, int wb, int nbuf, const std::string& name) {
     Gen g(P, rb, wb, nbuf);
+    g.variant = jit_variant();
+    if (const char* e = std::getenv("QG_JIT_STAGGER_NS")) g.stagger_ns = std::atoi(e);
     if (!g.supported()) return "";
     return g.run(name);
 }
@@ -869,6 +1088,7 @@ std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int
             const std::string ptx = jit_ptx_c64(P, rb, wb, nbuf, jk->name);
             if (!ptx.empty()) {
                 jk->smem = jit_smem_bytes(P, rb, wb, nbuf);
+                if (const char* e = std::getenv("QG_JIT_SMEM_PAD")) jk->smem += (size_t)std::atol(e);  // occupancy probe
                 jk->ok = jit_compile(ptx, jk->cubin, jk->err);
             } else {
                 jk->err = "pass not covered by the emitter";

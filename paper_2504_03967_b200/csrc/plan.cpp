@@ -1057,7 +1057,10 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
     plan.cfg = cfg;
     const int max_stages = opts.max_stages > 0 ? std::min(opts.max_stages, kMaxStages) : kMaxStages;
     const double max_cost = opts.max_cost > 0 ? (double)opts.max_cost : 350.0;
-    const int c_low = n_local >= 20 ? kLaneBits : 0;  // small states live in L2: no coalescing constraint
+    // small states live in L2: no coalescing constraint; large ones keep the lowest
+    // c_low qubits in every tile, so each HBM access is a 2^c_low-amplitude run
+    int c_low = n_local >= 20 ? kLaneBits : 0;
+    if (opts.low_qubits > 0 && n_local >= 20) c_low = std::min(std::max(opts.low_qubits, kLaneBits), cfg.k() - 1);
 
     std::vector<int> phys(n), inv(n);  // logical -> physical, physical -> logical
     for (int q = 0; q < n; ++q) phys[q] = inv[q] = q;

@@ -275,7 +275,7 @@ class CompiledCircuit:
 
     def __init__(self, gate_type: np.ndarray, gate_param: np.ndarray, n_qubits: int, precision: str = "fp64",
                  log2_ranks: int = 0, fuse: bool = True, tile_qubits: int = 0, max_stages: int = 0,
-                 max_cost: int = 0, kernel_cfg: int = 0, jit: int = 0):
+                 max_cost: int = 0, kernel_cfg: int = 0, jit: int = 0, low_qubits: int = 0):
         gt = np.ascontiguousarray(gate_type, dtype=np.int32).reshape(-1, 3)
         gp = np.ascontiguousarray(gate_param, dtype=np.float64).reshape(-1)
         if gt.shape[0] != gp.shape[0]:
@@ -287,7 +287,7 @@ class CompiledCircuit:
         self.log2_ranks = int(log2_ranks)
         opts = N.PlanOpts(dtype=_QG_DTYPE[precision], log2_ranks=log2_ranks, fuse=1 if fuse else 0,
                           tile_qubits=tile_qubits, max_stages=max_stages, max_cost=max_cost,
-                          kernel_cfg=kernel_cfg, jit=int(jit))
+                          kernel_cfg=kernel_cfg, jit=int(jit), low_qubits=int(low_qubits))
         h = C.c_void_p()
         self._lib = N.lib()
         N.check(self._lib.qg_plan_create(gt.ctypes.data_as(C.c_void_p), gp.ctypes.data_as(C.c_void_p),

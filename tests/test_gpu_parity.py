@@ -146,6 +146,53 @@ def test_qft_on_basis_state_is_dft():
     assert rel_l2(got, expect) <= 1e-11
 
 
+def _basis_then_qft(n, k, reversed_=False):
+    """|bitrev(k)> prepared with X = RX(pi) (global phase (-i)^popcount), then QFT(n)."""
+    rk = int(format(k, f"0{n}b")[::-1], 2)
+    gt, gp = qft_arrays(n, reversed_)
+    pre = [(GateKind.RX, -1, q) for q in range(n) if (rk >> q) & 1]
+    gt2 = np.concatenate([np.array(pre, dtype=np.int32).reshape(-1, 3), gt])
+    gp2 = np.concatenate([np.full(len(pre), math.pi), gp])
+    return gt2, gp2, len(pre)
+
+
+def test_qft28_complex64_on_basis_state_is_dft():
+    """C2 scale (QFT 28 q, complex64) with FIRING controlled phases: on |0...0> every
+    CR1 acts as the identity, on |bitrev(k)> every row's phase list is non-trivial
+    (long predicated PH lists, tile-uniform slots, register/thread-controlled factors).
+    Checked on the device against the closed form e^{2 pi i j k / 2^n} / sqrt(2^n),
+    rel-L2 <= 1e-5 (north_star complex64 tolerance)."""
+    n, k = 28, 0x5A5A5A7
+    gt, gp, npre = _basis_then_qft(n, k)
+    st, _ = sv.run_circuit(circuit(gt, gp, n), sv.SimOptions(precision="fp32", memory_budget=1 << 40))
+    a = st.amplitudes
+    phase = complex(1j ** npre)
+    num = den = 0.0
+    step = 1 << 24
+    for j0 in range(0, 1 << n, step):
+        j = torch.arange(j0, j0 + step, dtype=torch.int64, device=a.device)
+        ph = ((j * k) % (1 << n)).to(torch.float64) * (2 * math.pi / (1 << n))
+        expect = torch.polar(torch.full_like(ph, 2.0 ** (-n / 2)), ph)
+        got = a[j0:j0 + step].to(torch.complex128) * phase
+        num += float(torch.linalg.vector_norm(got - expect) ** 2)
+        den += float(torch.linalg.vector_norm(expect) ** 2)
+    assert math.sqrt(num / den) <= 1e-5
+
+
+@pytest.mark.parametrize("n,reversed_", [(24, False), (22, True)])
+def test_qft_after_random_ry_layer_vs_oracle(n, reversed_):
+    """QFT on a generic (non-basis) input: every phase list fires with amplitude-dependent
+    weight; complex64 against the oracle's fp64 run."""
+    rng = np.random.default_rng(n)
+    pre_t = np.array([(GateKind.RY, -1, q) for q in range(n)], dtype=np.int32)
+    pre_p = rng.uniform(0, 2 * math.pi, n)
+    gt, gp = qft_arrays(n, reversed_)
+    gt2, gp2 = np.concatenate([pre_t, gt]), np.concatenate([pre_p, gp])
+    ref = oracle.run_arrays(gt2, gp2, n, gt2.shape[0], "fp64")
+    st, _ = sv.run_circuit(circuit(gt2, gp2, n), sv.SimOptions(precision="fp32", memory_budget=1 << 40))
+    assert rel_l2(st.to_numpy(), ref) <= 1e-5
+
+
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_circuit_then_inverse_is_identity(precision):
     n = 27 if precision == "fp32" else 26
