@@ -36,6 +36,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+NVL_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction per GPU
 METRIC = "circuit wall-time, gates/s & HBM GB/s, 32q random-CX at 1/2/4/8 B200"
 
 
@@ -48,17 +49,103 @@ def load_json(path):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def cpu_sample(n_qubits_target: int, sample_qubits: int, sample_blocks: int, seed: int = 0):
-    """Reference algorithm (oracle port of statevec.run_circuit) on a bounded sample."""
-    import oracle
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _ref_modules():
+    """The reference package itself (installed into baseline/_ref), else the oracle port."""
+    if os.path.isdir(os.path.join(REF_DIR, "qgear")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from qgear import generators as rg, partition as rp, statevec as rs  # noqa: E402
+
+        return "reference", rg, rs, rp
+    import oracle  # test infrastructure: the CPU restatement, used only as the baseline arm
+
+    return "port", oracle, None, None
+
+
+def _threads() -> int:
+    c = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    w = 1
+    while w * 2 <= min(8, c):
+        w *= 2
+    return w
+
+
+def ref_sec_per_gate(n: int, blocks: int, seed: int = 0) -> tuple[float, int, str]:
+    """Wall seconds per gate of the reference CPU executor on RandomSpec(n, blocks, seed).
+
+    The reference's fastest CPU path for this circuit is its threaded partitioned
+    executor (partition.execute_distributed, W = min(8, cores) worker threads; fp64
+    only, partition.py:300-301) -- faster than the single-threaded fp32
+    statevec.run_circuit from 22 qubits up (measured in this container: 22 q x 30
+    gates 1.50 s vs 2.31 s)."""
+    kind, rg, rs, rp = _ref_modules()
+    if kind == "reference":
+        circ = rg.generate_random_gate_list(rg.RandomSpec(n, blocks, seed))
+        w = _threads()
+        t0 = time.perf_counter()
+        rp.execute_distributed(circ, w, rs.SimOptions(precision="fp64", memory_budget=1 << 40))
+        dt = time.perf_counter() - t0
+        return dt / (3 * blocks), w, "partition.execute_distributed(fp64, %d threads)" % w
     from paper_2504_03967_b200.generators import RandomSpec, random_arrays
 
-    gt, gp = random_arrays(RandomSpec(sample_qubits, sample_blocks, seed))
+    gt, gp = random_arrays(RandomSpec(n, blocks, seed))
     t0 = time.perf_counter()
-    oracle.run_arrays(gt, gp, sample_qubits, gt.shape[0], "fp32")
-    dt = time.perf_counter() - t0
-    sec_per_gate_target = dt / gt.shape[0] * 2.0 ** (n_qubits_target - sample_qubits)
-    return 1.0 / sec_per_gate_target, dt, gt.shape[0]
+    rg.run_arrays(gt, gp, n, gt.shape[0], "fp32")
+    return (time.perf_counter() - t0) / gt.shape[0], 1, "oracle port of statevec.run_circuit (fp32, 1 thread)"
+
+
+def ref_ladder(ladder=(20, 21, 22, 23, 24), blocks: int = 10) -> dict:
+    """Per-gate time at n = ladder, fitted log2(t) = a + b n (the 2^n cost of a
+    state-vector gate); the fit extrapolates to sizes the host cannot hold."""
+    pts = []
+    for n in ladder:
+        spg, w, how = ref_sec_per_gate(n, blocks)
+        pts.append((n, spg))
+    x = np.array([p[0] for p in pts], dtype=float)
+    y = np.log2(np.array([p[1] for p in pts]))
+    b, a = np.polyfit(x, y, 1)
+    return {"points_sec_per_gate": [[int(n), float(s)] for n, s in pts], "fit_log2": [float(a), float(b)],
+            "blocks": blocks, "threads": w, "how": how}
+
+
+def ref_rate(fit: dict, n_target: int, sample_n: int, blocks: int) -> tuple[float, float]:
+    """One bounded sample at sample_n, scaled to n_target with the fitted slope."""
+    spg, _, _ = ref_sec_per_gate(sample_n, blocks)
+    b = fit["fit_log2"][1]
+    spg_target = spg * 2.0 ** (b * (n_target - sample_n))
+    return 1.0 / spg_target, spg
+
+
+def ref_c1_ms() -> float | None:
+    """BASELINE configs[0] run directly: RandomSpec(16, 100, 0), complex128, 3000 shots."""
+    kind, rg, rs, _ = _ref_modules()
+    if kind != "reference":
+        return None
+    circ = rg.generate_random_gate_list(rg.RandomSpec(16, 100, 0))
+    best = 1e30
+    for _ in range(3):
+        t0 = time.perf_counter()
+        rs.run_circuit(circ, rs.SimOptions(precision="fp64", shots=3000, rng_seed=0))
+        best = min(best, time.perf_counter() - t0)
+    return best * 1000.0
+
+
+def _ladder(s: str) -> tuple:
+    return tuple(int(x) for x in s.split(","))
+
+
+def cpu_baseline_entry(n_target: int, sample_n: int, blocks: int, ladder: str, steps: int = 1) -> dict:
+    fit = ref_ladder(_ladder(ladder), blocks)
+    vals = [ref_rate(fit, n_target, sample_n, blocks)[0] for _ in range(steps)]
+    kind = _ref_modules()[0]
+    return {"value": float(np.mean(vals)), "unit": "gates/s", "cores": fit["threads"], "kind": kind,
+            "sample": (f"{fit['how']} on RandomSpec(n, {blocks} blocks, seed 0), n = {ladder}; "
+                       f"log2(sec/gate) fitted linear in n (slope {fit['fit_log2'][1]:.3f}) and extrapolated from "
+                       f"the n = {sample_n} sample to {n_target} qubits (the host cannot hold a {n_target}-qubit state)"),
+            "ladder": fit, "steps_values": vals, "c1_ms": ref_c1_ms(), "host": host_info()}
 
 
 def host_info() -> dict:
@@ -73,8 +160,8 @@ def host_info() -> dict:
     except OSError:
         pass
     return {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "model": model,
-            "threads": "1: statevec.run_circuit is single-threaded numpy; the reference's threaded executor "
-                       "(partition.execute_distributed) is fp64-only (partition.py:300-301), not this c64 config"}
+            "threads": "the reference's threaded executor partition.execute_distributed (fp64 only, "
+                       "partition.py:300-301) with min(8, cores) worker threads"}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -130,27 +217,34 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, rank: int):
+    """The reference's own CPU executor (baseline/_ref), rank 0 only, all host threads
+    it can use.  Warm-up = the n ladder that fixes the 2^n slope (once); each timed
+    step = one bounded sample at --ref-sample-qubits scaled to --qubits."""
     if rank != 0:
         return
-    steps, warm = args.steps, args.warmup
-    for _ in range(warm):
-        cpu_sample(args.qubits, args.ref_sample_qubits, args.ref_sample_blocks)
-    vals = []
+    steps = args.steps
+    fit = ref_ladder(_ladder(args.ref_ladder), args.ref_sample_blocks)
+    vals, spgs = [], []
     for _ in range(steps):
-        v, dt, g = cpu_sample(args.qubits, args.ref_sample_qubits, args.ref_sample_blocks)
+        v, spg = ref_rate(fit, args.qubits, args.ref_sample_qubits, args.ref_sample_blocks)
         vals.append(v)
+        spgs.append(spg)
     value = float(np.mean(vals))
-    sample = (f"oracle port of statevec.run_circuit (numpy, fp32/complex64, 1 core) on "
-              f"RandomSpec({args.ref_sample_qubits}, {args.ref_sample_blocks}, seed 0); per-gate time scaled "
-              f"x2^{args.qubits - args.ref_sample_qubits} to {args.qubits} qubits")
+    kind = _ref_modules()[0]
+    sample = (f"{fit['how']} on RandomSpec({args.ref_sample_qubits}, {args.ref_sample_blocks} blocks, seed 0) "
+              f"per step; sec/gate scaled to {args.qubits} qubits by the slope of log2(sec/gate) fitted over "
+              f"n = {args.ref_ladder} (warm-up ladder)")
     ms_per_step = 3 * args.blocks / value * 1000.0
-    out = {"metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-           "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-           "dtype": "c64", "data": "synthetic (reference generator stream, PCG64 seed 0)", "impl": "reference",
-           "config": {"workload": f"random CX-block, {args.qubits} qubits, {args.blocks} blocks, complex64",
+    out = {"metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": args.gpus, "steps": steps,
+           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "c128" if kind == "reference" else "c64",
+           "data": "synthetic (reference generator stream, PCG64 seed 0)", "impl": "reference",
+           "config": {"workload": f"random CX-block, {args.qubits} qubits, {args.blocks} blocks "
+                                  f"(extrapolated from fit over n={args.ref_ladder})",
                       "n_qubits": args.qubits, "blocks": args.blocks, "gates": 3 * args.blocks},
-           "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "port", "sample": sample,
-                            "host": host_info()},
+           "cpu_baseline": {"value": value, "unit": "gates/s", "cores": fit["threads"], "kind": kind,
+                            "sample": sample, "ladder": fit, "sample_sec_per_gate": spgs,
+                            "c1_ms": ref_c1_ms(), "host": host_info()},
            "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -184,7 +278,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     stream = torch.cuda.current_stream(dev)
     staging = None
 
-    def step(timed_passes: bool):
+    remap_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(plan.n_segments - 1)]
+    remap_egress = [shard_bytes * ((1 << len(g_)) - 1) // (1 << len(g_)) for g_, _ in plan.remaps]
+
+    def step(timed_passes: bool, timed_remaps: bool = False):
         sv.N.call("qg_state_init_zero", C.c_void_p(shard.data_ptr()), n_local, sv._QG_DTYPE[prec], rank,
                   C.c_void_p(stream.cuda_stream))
         pms, launches = 0.0, 0
@@ -194,8 +292,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             launches += st.pass_launches
             if seg < plan.n_segments - 1:
                 gpos, lpos = plan.remaps[seg]
-                stream.synchronize()
+                if timed_remaps:
+                    remap_ev[seg][0].record(stream)
                 pt.remap_dist(shard, n_local, gpos, lpos, rank, None, staging)
+                if timed_remaps:
+                    remap_ev[seg][1].record(stream)
         return pms, launches
 
     def barrier():
@@ -218,18 +319,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e1.record(stream)
     barrier()
     total_ms = e0.elapsed_time(e1)
-    # pass-kernel time on the launching stream (library CUDA events), same steps again
-    pass_ms, launches = 0.0, 0
+    # pass-kernel time on the launching stream (library CUDA events), same steps again;
+    # each remap bracketed by CUDA events on the same stream (NCCL waits on it, and it
+    # waits on NCCL before the copy-back)
+    pass_ms, launches, remap_ms = 0.0, 0, []
     for _ in range(args.steps):
-        pm, ln = step(True)
+        pm, ln = step(True, True)
         pass_ms += pm
         launches += ln
+        torch.cuda.synchronize(dev)
+        remap_ms.append([a.elapsed_time(b) for a, b in remap_ev])
     barrier()
     clock_info = clocks.stop() if clocks else None
-    t = torch.tensor([total_ms, pass_ms], dtype=torch.float64, device=dev)
+    remap_tot = float(np.sum(remap_ms)) / max(1, args.steps)  # per step, this rank
+    t = torch.tensor([total_ms, pass_ms, remap_tot], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, pass_ms = t.tolist()
+    total_ms, pass_ms, remap_tot = t.tolist()
     ms_per_step = total_ms / args.steps
     gates = gt.shape[0]
     value = gates / (ms_per_step / 1000.0)
@@ -278,12 +384,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     traffic = prof.get(f"{n_local}q_{prec}", {}).get("dram_bytes_per_launch")
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        v, dt, g_s = cpu_sample(n, args.cpu_sample_qubits, args.cpu_sample_blocks)
-        cpu = {"value": v, "unit": "gates/s", "cores": 1, "kind": "port",
-               "sample": (f"oracle port of statevec.run_circuit (numpy fp32, 1 core), RandomSpec("
-                          f"{args.cpu_sample_qubits}, {args.cpu_sample_blocks}, seed 0) = {g_s} gates in {dt:.2f} s, "
-                          f"per-gate time scaled x2^{n - args.cpu_sample_qubits} to {n} qubits"),
-               "host": host_info()}
+        cpu = cpu_baseline_entry(n, args.cpu_sample_qubits, args.cpu_sample_blocks, args.ref_ladder)
     out = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -301,12 +402,44 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "peak_source": "MEASURED_PEAKS.json:hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                      else "fallback 6.65 TB/s (B200_PROFILING.md)",
                      "algorithmic_bytes_per_launch": 2 * shard_bytes, "avg_launch_ms": avg_launch_ms},
+        "roofline_nvl": None if not plan.remaps else {
+            "bound": "nvlink", "achieved": sum(remap_egress) / (remap_tot / 1000.0) / 1e9,
+            "peak": NVL_PEAK_GBS, "unit": "GB/s",
+            "frac": sum(remap_egress) / (remap_tot / 1000.0) / 1e9 / NVL_PEAK_GBS,
+            "peak_source": "B200_PROFILING.md: measured peer copy 770 GB/s per direction (900 nominal)",
+            "egress_bytes_per_step_per_rank": int(sum(remap_egress)), "remap_ms_per_step": remap_tot,
+            "remaps": len(plan.remaps),
+            "per_remap": [{"s": len(g_), "egress_bytes": int(e_), "ms": float(np.mean([r[i] for r in remap_ms])),
+                           "gbs": e_ / (float(np.mean([r[i] for r in remap_ms])) / 1000.0) / 1e9}
+                          for i, ((g_, _), e_) in enumerate(zip(plan.remaps, remap_egress))]},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int((plan.info["n_passes"] + 1) * args.steps),
         "clocks": clock_info,
     }
     print(json.dumps(out), flush=True)
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: start N ranks (one per GPU) under
+    torch.distributed.run on this node, or fail if the node has fewer GPUs."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} requested but this node has {have} CUDA device(s)", file=sys.stderr)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the init log shows the communicator's rank count
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -325,10 +458,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-qubits", type=int, default=24)
-    ap.add_argument("--cpu-sample-blocks", type=int, default=20)
-    ap.add_argument("--ref-sample-qubits", type=int, default=22)
-    ap.add_argument("--ref-sample-blocks", type=int, default=30)
+    ap.add_argument("--cpu-sample-qubits", type=int, default=25)
+    ap.add_argument("--cpu-sample-blocks", type=int, default=10)
+    ap.add_argument("--ref-sample-qubits", type=int, default=25)
+    ap.add_argument("--ref-ladder", default="23,24,25,26")
+    ap.add_argument("--ref-sample-blocks", type=int, default=10)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -336,6 +470,12 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args.gpus))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a different GPU count",
+              file=sys.stderr)
+        sys.exit(2)
     if world > 1:
         import torch
         import torch.distributed as dist

@@ -203,6 +203,36 @@ int qg_sample(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, u
               int64_t* out_index_dev, int64_t* out_count_dev, int64_t* n_unique_host,
               double* norm_sq_host, void* stream);
 
+/* Tree sampler (tree.cu): the counts of a multinomial draw of `shots` outcomes
+ * from |a|^2, generated top-down by binomial splits over the binary tree of
+ * the index bits (exactly multinomial; replaces sample_counts statevec.py:221-234
+ * when shots are large or the state is sharded).  shots is int64 (< 2^53), the
+ * workspace is O(n_amps / 256) (never O(shots)); the result for a given
+ * (seed, tag) does not depend on the launch geometry.
+ *   prepare: masses of every tree node (one HBM read of the state); *mass_host
+ *            = sum |a|^2 (fp64) — the shard mass of a sharded state;
+ *   draw:    mode 0: the outcomes with a nonzero count as (index_base + index,
+ *            count) pairs in ascending index order, *n_out_host = their number
+ *            (capacity >= min(shots, n_amps)); mode 1: dense counts
+ *            out_count_dev[n_amps] (capacity >= n_amps), out_index_dev unused.
+ *            tag (< 2^24) selects an independent stream (the rank of a shard).
+ * A sharded state: every rank prepares, the rank masses are all-gathered, and
+ * qg_split_shots (same seed on every rank) splits the shots over the ranks by
+ * the same binomial tree (tag 1); each rank then draws its count with tag 2+rank.
+ * This path does not check the norm: the caller compares the mass with 1. */
+int64_t qg_sample_tree_workspace_bytes(int64_t n_amps);
+int qg_sample_tree_prepare(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
+                           double* mass_host, void* stream);
+int qg_sample_tree_draw(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
+                        int64_t shots, uint64_t seed, uint32_t tag, int32_t mode, int64_t index_base,
+                        int64_t* out_index_dev, int64_t* out_count_dev, int64_t capacity, int64_t* n_out_host,
+                        void* stream);
+/* counts_host[r] for r < n_parts (a power of two <= 64) from masses_host[r];
+ * workspace: >= 1 KiB of device memory */
+int qg_split_shots(const double* masses_host, int32_t n_parts, int64_t shots, uint64_t seed, void* workspace,
+                   int64_t workspace_bytes, int64_t* counts_host, void* stream);
+/* test hook: out_dev[s] = Binomial(n, p) draws s = 0..count-1 of the sampler's generator */
+int qg_binomial_test(double n, double p, uint64_t seed, int64_t count, int64_t* out_dev, void* stream);
 /* ---- QGIR1 container (container.py:1-16, 71-115): native parse / write ------
  * qg_qgir1_parse validates a whole file image and reports the byte offsets of
  * its arrays (zero-copy ingest: map the file, pass the int32 / float64 arrays

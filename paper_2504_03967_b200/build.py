@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
-SOURCES = ["plan.cpp", "container.cpp", "capi.cu", "fused.cu", "reduce.cu", "ucry.cu", "jit.cpp"]
+SOURCES = ["plan.cpp", "container.cpp", "capi.cu", "fused.cu", "reduce.cu", "ucry.cu", "tree.cu", "jit.cpp"]
 HEADERS = ["desc.h", "kernels.h", "plan.h", "jt_lists.h", "jit.h"]
 
 

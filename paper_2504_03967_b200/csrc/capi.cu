@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -513,6 +514,77 @@ int qg_sample(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, u
             "sample draw");
     QG_CUDA(cudaMemcpyAsync(n_unique_host, nu, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "nunique copy");
     QG_CUDA(cudaStreamSynchronize(st), "sample sync");
+    return QG_OK;
+}
+
+// ---- tree (binomial-split) sampler --------------------------------------------
+int64_t qg_sample_tree_workspace_bytes(int64_t n_amps) {
+    if (n_amps < 1 || (n_amps & (n_amps - 1))) return -1;
+    return (int64_t)qg::tree_layout(n_amps).total;
+}
+
+int qg_sample_tree_prepare(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
+                           double* mass_host, void* stream) {
+    DeviceGuard dg_(state);
+    if (int rc = check_dtype(dtype)) return rc;
+    if (!state || !workspace || n_amps < 1 || (n_amps & (n_amps - 1)))
+        return fail(QG_E_INVALID_ARG, "bad sampler arguments");
+    if (workspace_bytes < qg_sample_tree_workspace_bytes(n_amps)) return fail(QG_E_INVALID_ARG, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    QG_CUDA(qg::tree_prepare(state, n_amps, dtype, workspace, st), "tree prepare");
+    if (mass_host) {
+        QG_CUDA(cudaMemcpyAsync(mass_host, qg::tree_total_ptr(workspace), 8, cudaMemcpyDeviceToHost, st), "mass copy");
+        QG_CUDA(cudaStreamSynchronize(st), "tree sync");
+    }
+    return QG_OK;
+}
+
+int qg_sample_tree_draw(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
+                        int64_t shots, uint64_t seed, uint32_t tag, int32_t mode, int64_t index_base,
+                        int64_t* out_index_dev, int64_t* out_count_dev, int64_t capacity, int64_t* n_out_host,
+                        void* stream) {
+    DeviceGuard dg_(state);
+    if (int rc = check_dtype(dtype)) return rc;
+    if (shots < 0 || shots >= (1ll << 53)) return fail(QG_E_INVALID_ARG, "shots must be in [0, 2^53)");
+    if (!state || !workspace || !out_count_dev || n_amps < 1 || (n_amps & (n_amps - 1)) || (mode != 0 && mode != 1) ||
+        tag > 0xffffffu)
+        return fail(QG_E_INVALID_ARG, "bad sampler arguments");
+    if (workspace_bytes < qg_sample_tree_workspace_bytes(n_amps)) return fail(QG_E_INVALID_ARG, "workspace too small");
+    const int64_t need = mode == 1 ? n_amps : std::min<int64_t>(shots, n_amps);
+    if (capacity < need || (mode == 0 && !out_index_dev))
+        return fail(QG_E_INVALID_ARG, "output capacity " + std::to_string(capacity) + " < " + std::to_string(need));
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t* nu = const_cast<int64_t*>(qg::tree_nunique_ptr(workspace, n_amps));
+    QG_CUDA(qg::tree_draw(state, n_amps, dtype, workspace, shots, seed, tag, mode, index_base, out_index_dev,
+                          out_count_dev, mode == 0 ? nu : nullptr, st),
+            "tree draw");
+    if (n_out_host) {
+        if (mode == 0) {
+            QG_CUDA(cudaMemcpyAsync(n_out_host, nu, 8, cudaMemcpyDeviceToHost, st), "nunique copy");
+            QG_CUDA(cudaStreamSynchronize(st), "tree sync");
+        } else {
+            *n_out_host = n_amps;
+        }
+    }
+    return QG_OK;
+}
+
+int qg_split_shots(const double* masses_host, int32_t n_parts, int64_t shots, uint64_t seed, void* workspace,
+                   int64_t workspace_bytes, int64_t* counts_host, void* stream) {
+    DeviceGuard dg_(workspace);
+    if (!masses_host || !counts_host || !workspace || n_parts < 1 || n_parts > 64 || (n_parts & (n_parts - 1)) ||
+        workspace_bytes < 1024 || shots < 0 || shots >= (1ll << 53))
+        return fail(QG_E_INVALID_ARG, "bad split arguments");
+    QG_CUDA(qg::tree_split_parts(masses_host, n_parts, shots, seed, workspace, counts_host, (cudaStream_t)stream),
+            "split shots");
+    return QG_OK;
+}
+
+int qg_binomial_test(double n, double p, uint64_t seed, int64_t count, int64_t* out_dev, void* stream) {
+    DeviceGuard dg_(out_dev);
+    if (!out_dev || count < 1 || !(n >= 0) || n >= 9007199254740992.0 || !(p >= 0 && p <= 1))
+        return fail(QG_E_INVALID_ARG, "bad binomial test arguments");
+    QG_CUDA(qg::binomial_test(n, p, seed, count, out_dev, (cudaStream_t)stream), "binomial test");
     return QG_OK;
 }
 

@@ -38,4 +38,22 @@ cudaError_t sample_draw(const void* psi, int64_t n_amps, int dtype, int64_t shot
 const double* sample_total_ptr(const void* ws, int64_t n_amps);
 const int64_t* sample_nunique_ptr(const void* ws, int64_t n_amps, int64_t shots);
 
+// tree (binomial-split) sampler, tree.cu
+struct TreeLayout {
+    int64_t sb, n_sub;
+    int D;
+    size_t off_mass, off_cnt, off_nz, off_nzpre, off_cub, cub_bytes, total;
+};
+TreeLayout tree_layout(int64_t n_amps);
+cudaError_t tree_prepare(const void* psi, int64_t n_amps, int dtype, void* ws, cudaStream_t st);
+const double* tree_total_ptr(const void* ws);
+// mode 0: (index, count) of the outcomes with a count, ascending; mode 1: dense counts
+cudaError_t tree_draw(const void* psi, int64_t n_amps, int dtype, void* ws, int64_t shots, uint64_t seed, uint32_t tag,
+                      int mode, int64_t idx_base, int64_t* out_idx, int64_t* out_cnt, int64_t* n_unique_dev,
+                      cudaStream_t st);
+const int64_t* tree_nunique_ptr(const void* ws, int64_t n_amps);
+cudaError_t tree_split_parts(const double* masses_host, int n_parts, int64_t shots, uint64_t seed, void* ws,
+                             int64_t* out_host, cudaStream_t st);
+cudaError_t binomial_test(double n, double p, uint64_t seed, int64_t count, int64_t* out, cudaStream_t st);
+
 }  // namespace qg

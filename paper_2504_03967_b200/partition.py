@@ -87,17 +87,39 @@ def remap_local(shards: list[torch.Tensor], n_local: int, global_pos, local_pos)
 
 
 REMAP_CHUNK_BYTES = 1 << 30  # per peer and round: bounds the staging memory (37 q / 8 ranks = 128 GiB shards)
+_STAGING: dict = {}
+
+
+def _host_wire(group) -> bool:
+    """gloo moves host tensors only: device blocks are staged through host memory."""
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "gloo"
+
+
+def _staging(numel: int, dtype, device) -> torch.Tensor:
+    key = (str(device), dtype)
+    t = _STAGING.get(key)
+    if t is None or t.numel() < numel:
+        _STAGING.pop(key, None)
+        t = torch.empty(numel, dtype=dtype, device=device)
+        _STAGING[key] = t
+    return t
 
 
 def remap_dist(shard: torch.Tensor, n_local: int, global_pos, local_pos, rank: int, group=None,
-               staging: torch.Tensor | None = None, chunk_bytes: int = REMAP_CHUNK_BYTES) -> int:
+               staging: torch.Tensor | None = None, chunk_bytes: int | None = None) -> int:
     """torch.distributed remap of this rank's shard; returns the number of sends.
 
     Block j of this shard goes to the rank whose swapped bits equal j and comes
     back from it (an all-to-all within the group of 2^s ranks sharing the other
     rank bits).  The exchange runs in rounds of at most `chunk_bytes` per peer
-    through a staging buffer of (2^s - 1) chunks, so a 128 GiB shard needs
-    ~7 GiB of staging, not another 112 GiB."""
+    through two staging halves of (2^s - 1) chunks each (a 37-qubit / 8-rank
+    shard is 128 GiB: a whole-block staging buffer would not fit next to it):
+    round r+1's transfers run while round r's received blocks are copied into
+    the shard on a side stream.  Nothing here blocks the host on NCCL: the
+    collectives are ordered after the fused passes on the current stream and the
+    current stream waits for the last copy-back."""
     import torch.distributed as dist
 
     s = len(global_pos)
@@ -105,24 +127,49 @@ def remap_dist(shard: torch.Tensor, n_local: int, global_pos, local_pos, rank: i
     own, peers = remap_peers(rank, n_local, global_pos, local_pos)
     if not peers:
         return 0
+    host = shard.is_cuda and _host_wire(group)
+    chunk_bytes = REMAP_CHUNK_BYTES if chunk_bytes is None else chunk_bytes
     chunk = max(1, min(blk, chunk_bytes // shard.element_size()))
-    need = len(peers) * chunk
-    if staging is None or staging.numel() < need or staging.dtype != shard.dtype:
-        staging = torch.empty(need, dtype=shard.dtype, device=shard.device)
+    rounds = list(range(0, blk, chunk))
+    nbuf = 2 if len(rounds) > 1 and not host else 1
+    per = len(peers) * chunk
+    sdev = torch.device("cpu") if host or not shard.is_cuda else shard.device
+    if staging is None or staging.numel() < nbuf * per or staging.dtype != shard.dtype or staging.device != sdev:
+        staging = _staging(nbuf * per, shard.dtype, sdev)
 
     def wire(t: torch.Tensor) -> torch.Tensor:  # complex blocks travel as (re, im) pairs
         return torch.view_as_real(t) if t.is_complex() else t
 
-    for off in range(0, blk, chunk):
+    side = cur = None
+    done = [None] * nbuf
+    if shard.is_cuda and not host:
+        cur = torch.cuda.current_stream(shard.device)
+        side = torch.cuda.Stream(shard.device)
+    for r, off in enumerate(rounds):
         n = min(chunk, blk - off)
+        buf = staging[(r % nbuf) * per:(r % nbuf + 1) * per]
+        if done[r % nbuf] is not None:  # this half's previous copy-back must have read it
+            cur.wait_event(done[r % nbuf])
         ops = []
         for k, (j, peer) in enumerate(peers):
-            ops.append(dist.P2POp(dist.isend, wire(shard[j * blk + off:j * blk + off + n]), peer, group=group))
-            ops.append(dist.P2POp(dist.irecv, wire(staging[k * chunk:k * chunk + n]), peer, group=group))
+            src = shard[j * blk + off:j * blk + off + n]
+            ops.append(dist.P2POp(dist.isend, wire(src.cpu() if host else src), peer, group=group))
+            ops.append(dist.P2POp(dist.irecv, wire(buf[k * chunk:k * chunk + n]), peer, group=group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-        for k, (j, _) in enumerate(peers):
-            shard[j * blk + off:j * blk + off + n].copy_(staging[k * chunk:k * chunk + n])
+        if side is None:
+            for k, (j, _) in enumerate(peers):
+                shard[j * blk + off:j * blk + off + n].copy_(buf[k * chunk:k * chunk + n])
+            continue
+        side.wait_stream(cur)  # the received round
+        with torch.cuda.stream(side):
+            for k, (j, _) in enumerate(peers):
+                shard[j * blk + off:j * blk + off + n].copy_(buf[k * chunk:k * chunk + n])
+            ev = torch.cuda.Event()
+            ev.record(side)
+            done[r % nbuf] = ev
+    if side is not None:
+        cur.wait_stream(side)
     return len(peers)
 
 
@@ -149,6 +196,80 @@ def _permute_to_logical(full: torch.Tensor, n: int, phys_of_logical) -> torch.Te
     want = list(reversed(runs))              # logical most significant first
     dims = [order_phys.index(r) for r in want]
     return x.permute(*dims).contiguous().reshape(-1)
+
+
+# --------------------------------------------------------------------------- sampling
+def logical_indices(phys: torch.Tensor, phys_of_logical) -> torch.Tensor:
+    """Physical basis indices (rank bits on top) -> logical indices: logical qubit q
+    is physical bit phys_of_logical[q] (the plan's final map)."""
+    perm = [int(p) for p in phys_of_logical]
+    if perm == list(range(len(perm))):
+        return phys
+    out = torch.zeros_like(phys)
+    for q, p in enumerate(perm):
+        out |= ((phys >> p) & 1) << q
+    return out
+
+
+def _comm(t: torch.Tensor, group) -> torch.Tensor:
+    return t.cpu() if _host_wire(group) else t
+
+
+def sample_shards(shards: list[torch.Tensor], n_local: int, phys_of_logical, shots: int, rng_seed: int,
+                  norm_tol: float, ranks=None, group=None) -> tuple[torch.Tensor, torch.Tensor] | None:
+    """Counts of `shots` draws from a sharded state without gathering it.
+
+    Every rank: tree masses of its shard (one HBM read); the P masses are
+    all-gathered (P doubles); the shots are split over the ranks by the top of the
+    binomial tree (same seed everywhere, so every rank computes the same split);
+    each rank draws its own count from its shard (tag 2 + rank); outcome indices
+    get the rank bits and the logical qubit order; rank 0 gathers the (index,
+    count) lists.  The reference gathers the state and samples it centrally
+    (partition.py:345-348, statevec.py:221-234).  In-process shards (``ranks``
+    None, all shards here): the same steps without communication.
+    Returns (logical index ascending, count) on rank 0 (None on other ranks)."""
+    import torch.distributed as dist
+
+    distributed = ranks is not None
+    samplers = [sv.TreeSampler(t, (r if not distributed else ranks) << n_local)
+                for r, t in enumerate(shards)]
+    mine = [s.prepare() for s in samplers]
+    if distributed:
+        rank, workers = ranks, dist.get_world_size(group)
+        mt = _comm(torch.tensor(mine, dtype=torch.float64, device=shards[0].device), group)
+        allm = [torch.empty_like(mt) for _ in range(workers)]
+        dist.all_gather(allm, mt, group=group)
+        masses = [float(x.item()) for x in allm]
+    else:
+        rank, workers, masses = 0, len(shards), mine
+    total = float(sum(masses))
+    if not abs(total - 1.0) <= norm_tol:  # statevec.py:226-228, on every rank
+        raise UnnormalizedStateError(f"sharded norm^2 = {total!r}")
+    per_rank = sv.split_shots(masses, shots, rng_seed, shards[0].device)
+    idx_parts, cnt_parts = [], []
+    for i, s in enumerate(samplers):
+        r = rank if distributed else i
+        idx, cnt = s.draw(per_rank[r], rng_seed, tag=2 + r)
+        idx_parts.append(logical_indices(idx, phys_of_logical))
+        cnt_parts.append(cnt)
+    idx, cnt = torch.cat(idx_parts), torch.cat(cnt_parts)
+    if distributed:
+        k = _comm(torch.tensor([idx.numel()], dtype=torch.int64, device=idx.device), group)
+        sizes = [torch.empty_like(k) for _ in range(workers)]
+        dist.all_gather(sizes, k, group=group)
+        mx = max(int(x.item()) for x in sizes)
+        pair = torch.full((2, mx), -1, dtype=torch.int64, device=idx.device)
+        pair[0, :idx.numel()] = idx
+        pair[1, :idx.numel()] = cnt
+        pair = _comm(pair, group)
+        parts = [torch.empty_like(pair) for _ in range(workers)] if rank == 0 else None
+        dist.gather(pair, parts, dst=0, group=group)
+        if rank != 0:
+            return None
+        allp = torch.cat([p[:, :int(sz.item())] for p, sz in zip(parts, sizes)], dim=1)
+        idx, cnt = allp[0], allp[1]
+    order = torch.argsort(idx)
+    return idx[order], cnt[order]
 
 
 @dataclass
@@ -189,6 +310,7 @@ def execute_distributed(circuit, workers: int, options: sv.SimOptions | None = N
 
     distributed = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) == workers and workers > 1
     sent = [0] * workers
+    sampled = None
     if distributed:
         rank = dist.get_rank(group)
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -202,18 +324,24 @@ def execute_distributed(circuit, workers: int, options: sv.SimOptions | None = N
                 gpos, lpos = plan.remaps[seg]
                 if delay_hook is not None:
                     delay_hook(rank, seg)
-                torch.cuda.current_stream(dev).synchronize()
                 sent[rank] += remap_dist(shard, n_local, gpos, lpos, rank, group, staging)
-        counts_all = torch.tensor(sent, dtype=torch.int64, device=dev)
+        counts_all = _comm(torch.tensor(sent, dtype=torch.int64, device=dev), group)
         dist.all_reduce(counts_all, group=group)
         sent = counts_all.cpu().tolist()
         shards = [shard]
         state = None
+        if options.shots > 0:  # sampled where the shards live; no state gather
+            res = sample_shards(shards, n_local, plan.final_map, options.shots, options.rng_seed,
+                                sv.NORM_TOL[options.precision], ranks=rank, group=group)
+            if res is not None:
+                sampled = sv.counts_from_arrays(res[0].cpu().numpy(), res[1].cpu().numpy(), options.shots, n)
         if gather:
-            parts = [torch.empty_like(shard) for _ in range(workers)] if rank == 0 else None
-            dist.gather(shard, parts, dst=0, group=group)
+            host = _host_wire(group)
+            mine = shard.cpu() if host else shard
+            parts = [torch.empty_like(mine) for _ in range(workers)] if rank == 0 else None
+            dist.gather(mine, parts, dst=0, group=group)
             if rank == 0:
-                full = _permute_to_logical(torch.cat(parts), n, plan.final_map)
+                full = _permute_to_logical(torch.cat(parts).to(dev), n, plan.final_map)
                 state = sv.StateVector(n, options.precision, full)
     else:
         dev = sv._device(options.device)
@@ -238,12 +366,16 @@ def execute_distributed(circuit, workers: int, options: sv.SimOptions | None = N
         if gather:
             full = _permute_to_logical(torch.cat(shards), n, plan.final_map)
             state = sv.StateVector(n, options.precision, full)
-    counts = None
+        if options.shots > 0 and (not gather or options.sampler == "tree"):
+            res = sample_shards(shards, n_local, plan.final_map, options.shots, options.rng_seed,
+                                sv.NORM_TOL[options.precision])
+            sampled = sv.counts_from_arrays(res[0].cpu().numpy(), res[1].cpu().numpy(), options.shots, n)
+    counts = sampled
     if state is not None:
         nsq = state.norm_sq()
         if abs(nsq - 1.0) > sv.NORM_TOL[options.precision]:
             raise UnnormalizedStateError(f"gathered norm^2 = {nsq!r}")  # partition.py:139-140
-        if options.shots > 0:
+        if options.shots > 0 and counts is None:
             counts = sv.sample_counts(state, options.shots, options.rng_seed, options.sampler)
     if len(set(sent)) > 1 and not distributed:
         raise SequenceMismatchError(f"workers exchanged different message counts: {sent}")

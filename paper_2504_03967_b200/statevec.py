@@ -30,6 +30,7 @@ from .errors import (
     MeasureMidCircuitError,
     SelfPairError,
     TooManyQubitsError,
+    UnnormalizedStateError,
 )
 from .ir import CircuitTensor, GateKind, GateRecord, records_to_arrays
 
@@ -98,7 +99,8 @@ class SimOptions:
     shots: int = 0
     rng_seed: int = 0
     memory_budget: int = DEFAULT_MEMORY_BUDGET
-    sampler: str = "philox"      # "philox" (device RNG) | "numpy" (reference's PCG64 uniforms)
+    sampler: str = "philox"      # "philox" (device RNG) | "numpy" (reference's PCG64 uniforms) |
+                                 # "tree" (binomial splits: int64 shots, O(n/256) workspace, sharded states)
     device: str | int | None = None
     fuse: bool = True
     tile_qubits: int = 0
@@ -416,15 +418,79 @@ def exact_probabilities(state: StateVector) -> torch.Tensor:
     return out
 
 
+class TreeSampler:
+    """Device tree sampler over one state or shard (include/qgear_b200.h
+    qg_sample_tree_*): ``prepare()`` reads the state once and returns its mass
+    sum |a|^2; ``draw(shots)`` returns the multinomial counts of `shots` draws,
+    as (index, count) int64 device tensors of the outcomes with a count (index
+    ascending, offset by ``index_base``) or, with ``dense=True``, one int64
+    count per amplitude."""
+
+    def __init__(self, amps: torch.Tensor, index_base: int = 0):
+        self.n = _check_amps(amps)
+        self.amps = amps
+        self.dtype = _QG_DTYPE[_precision_of(amps)]
+        self.index_base = int(index_base)
+        self.ws = torch.empty(max(N.lib().qg_sample_tree_workspace_bytes(1 << self.n), 1024), dtype=torch.uint8,
+                              device=amps.device)
+        self.mass = None
+
+    def prepare(self) -> float:
+        m = C.c_double()
+        N.call("qg_sample_tree_prepare", C.c_void_p(self.amps.data_ptr()), 1 << self.n, self.dtype,
+               C.c_void_p(self.ws.data_ptr()), self.ws.numel(), C.byref(m), _stream(self.amps.device))
+        self.mass = m.value
+        return self.mass
+
+    def draw(self, shots: int, rng_seed: int = 0, tag: int = 2, dense: bool = False):
+        if self.mass is None:
+            self.prepare()
+        na = 1 << self.n
+        dev = self.amps.device
+        cap = na if dense else max(1, min(int(shots), na))
+        cnt = torch.empty(cap, dtype=torch.int64, device=dev)
+        idx = None if dense else torch.empty(cap, dtype=torch.int64, device=dev)
+        nout = C.c_int64()
+        N.call("qg_sample_tree_draw", C.c_void_p(self.amps.data_ptr()), na, self.dtype, C.c_void_p(self.ws.data_ptr()),
+               self.ws.numel(), int(shots), C.c_uint64(rng_seed & (2**64 - 1)), int(tag), 1 if dense else 0,
+               self.index_base, C.c_void_p(0 if idx is None else idx.data_ptr()), C.c_void_p(cnt.data_ptr()), cap,
+               C.byref(nout), _stream(dev))
+        if dense:
+            return cnt
+        k = nout.value
+        return idx[:k], cnt[:k]
+
+
+def split_shots(masses, shots: int, rng_seed: int, device=None) -> list[int]:
+    """Shots per part (a sharded state's ranks) from the parts' masses: the top of
+    the tree sampler's binomial tree (qg_split_shots); identical on every rank."""
+    m = np.ascontiguousarray(np.asarray(masses, dtype=np.float64))
+    out = np.zeros(m.shape[0], dtype=np.int64)
+    dev = _device(device)
+    ws = torch.empty(1024, dtype=torch.uint8, device=dev)
+    N.call("qg_split_shots", m.ctypes.data_as(C.c_void_p), m.shape[0], int(shots), C.c_uint64(rng_seed & (2**64 - 1)),
+           C.c_void_p(ws.data_ptr()), ws.numel(), out.ctypes.data_as(C.c_void_p), _stream(dev))
+    return out.tolist()
+
+
 def sample_indices(amps: torch.Tensor, shots: int, rng_seed: int = 0, sampler: str = "philox",
                    norm_tol: float | None = None) -> tuple[torch.Tensor, torch.Tensor]:
-    """Device sampler: (unique outcome indices ascending, counts) as int64 device tensors."""
+    """Device sampler: (unique outcome indices ascending, counts) as int64 device tensors.
+
+    ``sampler="philox"`` switches to the tree sampler above 2^31 - 1 shots (the
+    per-shot sampler keeps one record per shot)."""
     if shots < 1:
         raise ValueError(f"shots must be >= 1, got {shots}")
     n = _check_amps(amps)
     prec = _precision_of(amps)
     tol = NORM_TOL[prec] if norm_tol is None else norm_tol
     dev = amps.device
+    if sampler == "tree" or (sampler == "philox" and shots > 2**31 - 1):
+        ts = TreeSampler(amps)
+        m = ts.prepare()
+        if not abs(m - 1.0) <= tol:  # statevec.py:226-228
+            raise UnnormalizedStateError(f"norm^2 = {m!r} outside tolerance")
+        return ts.draw(shots, rng_seed)
     ws_bytes = N.lib().qg_sample_workspace_bytes(1 << n, shots)
     ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
     idx = torch.empty(shots, dtype=torch.int64, device=dev)
@@ -433,7 +499,7 @@ def sample_indices(amps: torch.Tensor, shots: int, rng_seed: int = 0, sampler: s
     if sampler == "numpy":  # the reference's exact uniform stream: Generator.choice -> random(shots)
         uni = torch.from_numpy(np.random.default_rng(rng_seed).random(shots)).to(dev)
     elif sampler != "philox":
-        raise ValueError(f"sampler must be 'philox' or 'numpy', got {sampler!r}")
+        raise ValueError(f"sampler must be 'philox', 'numpy' or 'tree', got {sampler!r}")
     nu = C.c_int64()
     nsq = C.c_double()
     N.call("qg_sample", C.c_void_p(amps.data_ptr()), 1 << n, _QG_DTYPE[prec], shots, C.c_uint64(rng_seed & (2**64 - 1)),
