@@ -48,7 +48,12 @@ struct Gen {
     int nq = 0, nr = 0, nf = 0, np = 0, nl = 0;
     int amap[64];          // slot -> %a register index (register CX moves rename)
     uint32_t fposs = 0;    // slot bits of the flip vector F that may be 1
-    int variant = 1;       // bit 0: tile loads as cp.async into the SMEM buffer, issued a tile ahead
+    // bit 0: tile loads as cp.async into the SMEM buffer, issued a tile ahead; 2048: one CTA per SM
+    // (up to 255 registers); 4096: register double-buffered tiles (the next tile's loads are issued
+    // into a second register bank when a tile starts; implies 2048); 8192: two transpose buffers
+    int variant = 1;
+    int tbuf = 0;          // transpose buffer of the next transpose (variant 8192)
+    bool first_tr = true;  // first transpose of the tile
     int reads_left = 0;    // SMEM buffer reads left in the tile (async loads: the last one frees it)
     size_t off_coef, off_ph, off_tph;
     // smem layout
@@ -58,7 +63,7 @@ struct Gen {
     struct Dec { int fam = -1, t = -1, c = -1; };
     std::vector<Dec> dec;
 
-    Gen(const PD& p, int rb, int wb, int nbuf) : P(p), RB(rb), WB(wb), NBUF(nbuf) {
+    Gen(const PD& p, int rb, int wb, int nbuf, int var) : P(p), RB(rb), WB(wb), NBUF(nbuf), variant(var) {
         R = 1 << RB;
         NT = 32 << WB;
         k = P.k;
@@ -66,7 +71,7 @@ struct Gen {
         off_ph = offsetof(PD, ph);
         off_tph = offsetof(PD, tph);
         buf_bytes = (size_t)8 << k;
-        tab_gb = NBUF * buf_bytes;                        // per mapping: [lane g | warp g | lane s | warp s]
+        tab_gb = tbufs(var) * NBUF * buf_bytes;           // per mapping: [lane g | warp g | lane s | warp s]
         tab_pf = tab_gb + (size_t)(P.n_stages + 1) * kMapBytes;  // [lane part | warp part] of the prefetch offset
         tab_uph = tab_pf + 384;                                   // tile-uniform phase slots (float2 each)
         for (int i = 0; i < R; ++i) amap[i] = i;
@@ -89,11 +94,13 @@ struct Gen {
         dec[oc_xf(RB)] = {8, -1, -1};
         dec[oc_end(RB)] = {9, -1, -1};
     }
-    static size_t smem_bytes(const PD& P, int rb, int wb, int nbuf) {
+    // variant 8192: transposes alternate between two SMEM tile buffers (one barrier each)
+    static int tbufs(int var) { return (var & 8192) ? 2 : 1; }
+    static size_t smem_bytes(const PD& P, int rb, int wb, int nbuf, int var) {
         (void)rb;
-        const size_t nt = (size_t)32 << wb;
-        (void)nt;
-        return nbuf * ((size_t)8 << P.k) + (size_t)(P.n_stages + 1) * kMapBytes + 384 + 8 * (size_t)kMaxUph;
+        (void)wb;
+        return tbufs(var) * nbuf * ((size_t)8 << P.k) + (size_t)(P.n_stages + 1) * kMapBytes + 384 +
+               8 * (size_t)kMaxUph;
     }
 
     std::string q() { return "%q" + std::to_string(nq++); }
@@ -413,7 +420,8 @@ struct Gen {
     }
 
     // SMEM store of every slot i at (T ^ O(i)), T runtime with bits within `lm`
-    void smem_store(const std::string& T, uint32_t lm, const std::vector<uint32_t>& O) {
+    void smem_store(const std::string& T, uint32_t lm, const std::vector<uint32_t>& O,
+                    const std::string& sb = "%smb") {
         std::map<uint32_t, std::string> base;
         for (int i = 0; i < R; ++i) {
             const uint32_t lo = O[i] & lm, hi = O[i] & ~lm;
@@ -422,7 +430,7 @@ struct Gen {
             if (it == base.end()) {
                 br = r();
                 L("xor.b32 ", br, ", ", T, ", ", lo, ";");
-                L("add.u32 ", br, ", ", br, ", %smb;");
+                L("add.u32 ", br, ", ", br, ", ", sb, ";");
                 base[lo] = br;
             } else {
                 br = it->second;
@@ -430,7 +438,8 @@ struct Gen {
             L("st.shared.b64 [", br, "+", hi, "], ", a(i), ";");
         }
     }
-    void smem_load(const std::string& T, uint32_t lm, const std::vector<uint32_t>& O) {
+    void smem_load(const std::string& T, uint32_t lm, const std::vector<uint32_t>& O,
+                   const std::string& sb = "%smb") {
         std::map<uint32_t, std::string> base;
         for (int i = 0; i < R; ++i) {
             const uint32_t lo = O[i] & lm, hi = O[i] & ~lm;
@@ -439,7 +448,7 @@ struct Gen {
             if (it == base.end()) {
                 br = r();
                 L("xor.b32 ", br, ", ", T, ", ", lo, ";");
-                L("add.u32 ", br, ", ", br, ", %smb;");
+                L("add.u32 ", br, ", ", br, ", ", sb, ";");
                 base[lo] = br;
             } else {
                 br = it->second;
@@ -450,7 +459,12 @@ struct Gen {
 
     // transpose from mapping m1 (with the current F) into mapping m2
     void transpose(int m1, int m2) {
-        if (NBUF == 1) L("bar.sync 0;");
+        const bool two = (variant & 8192) != 0;
+        if ((variant & 262144) && first_tr) L("cp.async.bulk.wait_group.read 0;");  // the last tile's stores
+        if (NBUF == 1 && (!two || first_tr)) L("bar.sync 0;");  // WAR on the buffer last read
+        first_tr = false;
+        const std::string sb = (two && tbuf) ? std::string("%smb2") : std::string("%smb");
+        if (two) tbuf ^= 1;
         const StageDesc& S1 = P.stg[m1];
         std::string T = so_of(m1);
         uint32_t lm = thread_smask(m1);
@@ -470,7 +484,7 @@ struct Gen {
                 if (i & (1 << b)) v ^= S1.out_s[b];
             O[i] = v;
         }
-        smem_store(T, lm, O);
+        smem_store(T, lm, O, sb);
         L("bar.sync 0;");
         for (int i = 0; i < R; ++i) amap[i] = i;  // register renames end with the stage
         const StageDesc& S2 = P.stg[m2];
@@ -481,10 +495,94 @@ struct Gen {
                 if (i & (1 << b)) v ^= S2.reg_s[b];
             O[i] = v;
         }
-        smem_load(T2, thread_smask(m2), O);
+        smem_load(T2, thread_smask(m2), O, sb);
         L("mov.u32 %F, 0;");
         fposs = 0;
         after_read();
+    }
+
+    // the planner's SMEM swizzle of a tile index (plan.cpp swz, complex64); an involution
+    static uint32_t swz(uint32_t j) { return j ^ (((j >> 4) ^ (j >> 8) ^ (j >> 12)) & 15u); }
+    int run_bits() const {  // contiguous low qubits of the tile: one run = 2^c amplitudes in HBM
+        int c = 0;
+        while (c < k && P.tile_q[c] == c) ++c;
+        return c;
+    }
+    // variant 262144: the tile leaves through the TMA engine.  The registers (store
+    // mapping si, flips folded in) go to the SMEM buffer in the LINEAR tile-index layout
+    // (offset = tile index * 8: each HBM run is one contiguous SMEM range), then warp 0
+    // issues one cp.async.bulk shared -> global copy per run; the buffer is reused only
+    // after the copies have read it (cp.async.bulk.wait_group.read before the tile's
+    // first SMEM write).  Warps never wait on the stores' L2 / HBM write path.
+    void tma_store(int si) {
+        const StageDesc& S = P.stg[si];
+        L("cp.async.bulk.wait_group.read 0;");
+        L("bar.sync 0;");  // WAR: the buffer's last reads (final transpose) are done
+        std::string T = r();
+        L("mov.u32 ", T, ", %tlin;");
+        uint32_t lm = tlin_mask;
+        uint32_t Ol[kMaxRegBits];
+        for (int b = 0; b < RB; ++b) Ol[b] = swz(S.out_s[b] >> 3) << 3;
+        for (int b = 0; b < RB; ++b) {
+            if (!(fposs & (1u << b))) continue;
+            std::string t = r();
+            L("bfe.u32 ", t, ", %F, ", b, ", 1;");
+            L("neg.s32 ", t, ", ", t, ";");
+            L("and.b32 ", t, ", ", t, ", ", Ol[b], ";");
+            L("xor.b32 ", T, ", ", T, ", ", t, ";");
+            lm |= Ol[b];
+        }
+        std::vector<uint32_t> O(R);
+        for (int i = 0; i < R; ++i) {
+            uint32_t v = 0;
+            for (int b = 0; b < RB; ++b)
+                if (i & (1 << b)) v ^= Ol[b];
+            O[i] = v;
+        }
+        smem_store(T, lm, O, "%smb");
+        L("fence.proxy.async.shared::cta;");
+        L("bar.sync 0;");
+        const int c = run_bits(), nrb = k - c;  // 2^nrb runs of 2^c amplitudes
+        const int64_t nr = 1ll << nrb, rs = 8ll << c;
+        std::string ls = lab();
+        L("@!%pw0 bra.uni ", ls, ";");
+        std::string pl = p();
+        if (nr < 32) {
+            L("setp.ge.u32 ", pl, ", %xlane, ", nr, ";");
+            L("@", pl, " bra.uni ", ls, ";");
+        }
+        std::string gl = q(), sl = r();
+        L("or.b64 ", gl, ", %base, %rdl;");    // tile base | this lane's run bits (deposited)
+        L("shl.b32 ", sl, ", %xlane, ", c + 3, ";");
+        L("add.u32 ", sl, ", ", sl, ", %smb;");
+        for (int64_t m = 0; m * 32 < nr; ++m) {
+            uint64_t dm = 0;  // run bits 5.. of run index 32 m
+            for (int i = 5; i < nrb; ++i)
+                if (((32 * m) >> i) & 1) dm |= 1ull << P.tile_q[c + i];
+            std::string ga = q();
+            L("or.b64 ", ga, ", ", gl, ", ", u64s(dm), ";");
+            L("shl.b64 ", ga, ", ", ga, ", 3;");
+            L("add.s64 ", ga, ", ", ga, ", %psi;");
+            L("cp.async.bulk.global.shared::cta.bulk_group [", ga, "], [", sl, "+", (size_t)(m * 32 * rs), "], ", rs,
+              ";");
+        }
+        L("cp.async.bulk.commit_group;");
+        o << ls << ":\n";
+    }
+    uint32_t tlin_mask = 0;
+
+    // tile load (mapping m) from the tile at byte pointer `ptr` into registers <bank>0..R-1
+    void reg_load(int m, const std::string& ptr, const std::string& bank) {
+        std::string g = gb_of(m), ad = q();
+        L("shl.b64 ", ad, ", ", g, ", 3;");
+        L("add.s64 ", ad, ", ", ad, ", ", ptr, ";");
+        Bases B;
+        for (int i = 0; i < R; ++i) {
+            uint64_t off = 0;
+            for (int b = 0; b < RB; ++b)
+                if (i & (1 << b)) off |= 1ull << P.stg[m].reg_q[b];
+            L("ld.global.cs.b64 ", bank, i, ", ", addr64(B, ad, off * 8), ";");
+        }
     }
 
     // async tile load: global (mapping m, tile base register) -> SMEM buffer in
@@ -608,6 +706,7 @@ struct Gen {
         L("mov.u32 %xlane, ", lane, ";");
         L("mov.u32 %xwarp, ", warp, ";");
         L("mov.u32 %smb, smem;");
+        L("add.u32 %smb2, %smb, ", buf_bytes, ";");
         // per-mapping tables of the lane and warp parts of a thread's global bits and
         // SMEM offset (a thread's value = lane part | warp part); warp 0 writes the lane
         // entries, lane 0 of every warp its warp's entries
@@ -655,6 +754,29 @@ struct Gen {
             L("@%pl0 st.shared.u64 [%tw8+", pf + 256, "], ", gw, ";");
         }
         L("setp.lt.u32 %pfl, ", lane, ", ", R, ";");
+        if (variant & 262144) {
+            const StageDesc& S = P.stg[si];
+            L("mov.u32 %tlin, 0;");
+            auto addl = [&](const std::string& src, int bitn, uint32_t off) {
+                std::string t = r();
+                L("bfe.u32 ", t, ", ", src, ", ", bitn, ", 1;");
+                L("neg.s32 ", t, ", ", t, ";");
+                L("and.b32 ", t, ", ", t, ", ", off, ";");
+                L("xor.b32 %tlin, %tlin, ", t, ";");
+                tlin_mask |= off;
+            };
+            for (int l = 0; l < kLaneBits; ++l) addl(lane, l, swz(S.lane_s[l]) << 3);
+            for (int w = 0; w < WB; ++w) addl(warp, w, swz(S.warp_s[w]) << 3);
+            const int c = run_bits(), nrb = k - c;
+            L("mov.u64 %rdl, 0;");
+            for (int i = 0; i < nrb && i < 5; ++i) {
+                std::string t = r(), t64 = q();
+                L("bfe.u32 ", t, ", ", lane, ", ", i, ", 1;");
+                L("cvt.u64.u32 ", t64, ", ", t, ";");
+                L("shl.b64 ", t64, ", ", t64, ", ", (int)P.tile_q[c + i], ";");
+                L("or.b64 %rdl, %rdl, ", t64, ";");
+            }
+        }
         L("bar.sync 0;");
         L("mov.u32 %ctile, %ctaid.x;");
         L("mov.u32 %nctile, %nctaid.x;");
@@ -699,6 +821,15 @@ struct Gen {
             async_load(li, "%base");
             o << ls << ":\n";
         }
+        if (variant & 4096) {  // the CTA's first tile into the prefetch bank
+            std::string ls = lab(), pt0 = q();
+            L("setp.ge.u64 %pend, %tile, %tend;");
+            L("@%pend bra.uni ", ls, ";");
+            L("shl.b64 ", pt0, ", %base, 3;");
+            L("add.s64 ", pt0, ", ", pt0, ", %psi;");
+            reg_load(li, pt0, "%b");
+            o << ls << ":\n";
+        }
 
         // ---- tile loop
         o << "$LOOP:\n";
@@ -711,7 +842,17 @@ struct Gen {
         L("add.s64 %nbase, %nbase, %dG;");
         L("and.b64 %nbase, %nbase, ", u64s(cmask), ";");
         L("setp.lt.u64 %pnext, %ntile, %tend;");
-        if (variant & 1) {  // this tile was loaded into the SMEM buffer by cp.async; read stage 1's mapping
+        first_tr = true;
+        tbuf = 0;
+        if (variant & 4096) {  // this tile from the prefetch bank; the next tile's loads into it
+            for (int i = 0; i < R; ++i) L("mov.b64 ", a(i), ", %b", i, ";");
+            std::string ls = lab(), pn = q();
+            L("@!%pnext bra.uni ", ls, ";");
+            L("shl.b64 ", pn, ", %nbase, 3;");
+            L("add.s64 ", pn, ", ", pn, ", %psi;");
+            reg_load(li, pn, "%b");
+            o << ls << ":\n";
+        } else if (variant & 1) {  // this tile was loaded into the SMEM buffer by cp.async; read stage 1's mapping
             L("cp.async.wait_all;");
             L("bar.sync 0;");
             reads_left = 1 + (ns - 1) + (P.store_direct ? 0 : 1);
@@ -724,7 +865,7 @@ struct Gen {
             }
             smem_load(so_of(1), thread_smask(1), O);
             after_read();
-        } else if (variant & 32) {  // timing probe: no global memory traffic (wrong results)
+        } else if (variant & (32 | 32768)) {  // timing probes: no global loads (wrong results)
             for (int i = 0; i < R; ++i) L("mov.b64 ", a(i), ", 0;");
         } else {  // load (io or stage-1 mapping): thread bits and register bits are disjoint
             std::string g = gb_of(li), ad = q();
@@ -735,13 +876,13 @@ struct Gen {
                 uint64_t off = 0;
                 for (int b = 0; b < RB; ++b)
                     if (i & (1 << b)) off |= 1ull << P.stg[li].reg_q[b];
-                L("ld.global.cs.b64 ", a(i), ", ", addr64(B, ad, off * 8), ";");
+                L((variant & 131072) ? "ld.global.b64 " : "ld.global.cs.b64 ", a(i), ", ", addr64(B, ad, off * 8), ";");
             }
         }
         if (!(variant & 128)) {  // warm L2 with this CTA's next tile (variant 512: the one after)
             std::string pp = p(), pf = q(), ad = q();
             std::string tgt = "%nbase";
-            if (variant & 512) {
+            if (variant & (512 | 4096)) {
                 std::string t2 = q(), nb2 = q();
                 pp = p();
                 L("add.s64 ", t2, ", %ntile, %G;");
@@ -897,7 +1038,9 @@ struct Gen {
             transpose(cur, si);
             cur = si;
         }
-        if (!(variant & 32)) {  // store through the output mapping (register CX map and flips folded in)
+        if ((variant & 262144) && !(variant & (32 | 16384))) {
+            tma_store(si);
+        } else if (!(variant & (32 | 16384))) {  // store through the output mapping (register CX map and flips folded in)
             const StageDesc& S = P.stg[si];
             std::string g = gb_of(si);
             uint64_t lm = thread_gmask(si);
@@ -931,13 +1074,15 @@ struct Gen {
                     L("add.s64 ", x, ", ", x, ", %pt;");
                     it = bases.emplace(lo, std::make_pair(x, Bases{})).first;
                 }
-                L("st.global.cs.b64 ", addr64(it->second.second, it->second.first, hi * 8), ", ", a(i), ";");
+                L((variant & 65536) ? "st.global.b64 " : "st.global.cs.b64 ",
+                  addr64(it->second.second, it->second.first, hi * 8), ", ", a(i), ";");
             }
         }
         L("mov.u64 %tile, %ntile;");
         L("mov.u64 %base, %nbase;");
         L("bra.uni $LOOP;");
         o << "$END:\n";
+        if (variant & 262144) L("cp.async.bulk.wait_group 0;");
         L("ret;");
 
         // ---- header
@@ -946,14 +1091,16 @@ struct Gen {
         h << ".extern .shared .align 16 .b8 smem[];\n\n";
         h << ".visible .entry " << name << "(\n\t.param .align 8 .b8 P[" << sizeof(PD)
           << "],\n\t.param .u64 psi,\n\t.param .u64 rk\n)\n";
-        const int min_ctas = (WB >= 4 || RB >= 6) ? 1 : ((variant & 2) ? 3 : 2);
+        const int min_ctas = (WB >= 4 || RB >= 6 || (variant & (2048 | 4096))) ? 1 : ((variant & 2) ? 3 : 2);
         h << ".maxntid " << NT << ", 1, 1\n.minnctapersm " << min_ctas << "\n{\n";
         h << "\t.reg .b64 %a<" << R << ">;\n";
+        if (variant & 4096) h << "\t.reg .b64 %b<" << R << ">;\n";
         h << "\t.reg .b64 %q<" << (nq + 1) << ">;\n";
         h << "\t.reg .b32 %r<" << (nr + 1) << ">;\n";
         h << "\t.reg .f32 %f<" << (nf + 1) << ">;\n";
         h << "\t.reg .pred %p<" << (np + 1) << ">;\n";
-        h << "\t.reg .b32 %xtid, %xlane, %xwarp, %smb, %tl8, %tw8, %tl4, %tw4, %F, %ctile, %nctile;\n";
+        h << "\t.reg .b32 %xtid, %xlane, %xwarp, %smb, %smb2, %tlin, %tl8, %tw8, %tl4, %tw4, %F, %ctile, %nctile;\n";
+        h << "\t.reg .b64 %rdl;\n";
         h << "\t.reg .b64 %tile, %tend, %ntile, %G, %base, %nbase, %dG, %psi, %rk, %pt;\n";
         h << "\t.reg .pred %pfl, %pend, %pnext, %pw0, %pl0;\n";
         return h.str() + o.str() + "}\n";
@@ -971,15 +1118,14 @@ int jit_variant() {
 }
 
 std::string jit_ptx_c64(const PassDesc<float>& P, int rb, int wb, int nbuf, const std::string& name) {
-    Gen g(P, rb, wb, nbuf);
-    g.variant = jit_variant();
+    Gen g(P, rb, wb, nbuf, jit_variant());
     if (const char* e = std::getenv("QG_JIT_STAGGER_NS")) g.stagger_ns = std::atoi(e);
     if (!g.supported()) return "";
     return g.run(name);
 }
 
 size_t jit_smem_bytes(const PassDesc<float>& P, int rb, int wb, int nbuf) {
-    return Gen::smem_bytes(P, rb, wb, nbuf);
+    return Gen::smem_bytes(P, rb, wb, nbuf, jit_variant());
 }
 
 bool jit_compile(const std::string& ptx, std::vector<char>& cubin, std::string& log) {

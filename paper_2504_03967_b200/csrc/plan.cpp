@@ -22,9 +22,11 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <climits>
 #include <cassert>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 
 namespace qg {
@@ -312,12 +314,20 @@ static void assign_mapping(int dtype, const KernelCfg& cfg, const std::vector<in
         for (int b = kLaneBits; b < k && (int)hs.reg_tile.size() < cfg.rb; ++b)
             if (!used[b]) { hs.reg_tile.push_back(b); used[b] = 1; }
     } else {
-        for (int b = k - 1; b >= 0 && (int)hs.reg_tile.size() < cfg.rb; --b)
-            if (!used[b]) { hs.reg_tile.push_back(b); used[b] = 1; }
         // conflict-free lanes: the lanes of one SMEM wavefront must cover every
         // residue class of the swizzle (8B amps: 16-lane phases, 4 classes mod 4;
-        // 16B amps: 8-lane phases, 3 classes mod 3)
+        // 16B amps: 8-lane phases, 3 classes mod 3), so the register fill (top bits
+        // first) skips a bit whose class would be left without an unused member
         const int M = dtype == QG_DTYPE_C64 ? 4 : 3;
+        auto spare = [&](int b) {
+            int c = 0;
+            for (int x = b % M; x < k; x += M) c += (!used[x] && x != b) ? 1 : 0;
+            return c;
+        };
+        for (int b = k - 1; b >= 0 && (int)hs.reg_tile.size() < cfg.rb; --b)
+            if (!used[b] && spare(b) >= 1) { hs.reg_tile.push_back(b); used[b] = 1; }
+        for (int b = k - 1; b >= 0 && (int)hs.reg_tile.size() < cfg.rb; --b)
+            if (!used[b]) { hs.reg_tile.push_back(b); used[b] = 1; }
         for (int r = 0; r < M; ++r)
             for (int b = 0; b < k; ++b)
                 if (!used[b] && b % M == r) { hs.lane_tile.push_back(b); used[b] = 1; break; }
@@ -1028,6 +1038,8 @@ int rebind_plan(qg_plan& plan, const double* gate_param, int64_t n_gates, std::s
 }
 
 // ------------------------------------------------------------------ driver
+constexpr int kRemapMinPos = 10;  // 8 KiB runs (complex64) in a remap's strided blocks
+
 int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gates, int n_qubits,
                const qg_plan_opts& opts, qg_plan& plan, std::string& err) {
     if (n_qubits < 1 || n_qubits > 62) { err = "n_qubits must be in [1, 62]"; return QG_E_INVALID_ARG; }
@@ -1124,9 +1136,33 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
         if (need.empty()) { err = "planner made no progress"; return QG_E_PROTOCOL; }
         qg_remap rm{};
         rm.s = (int)need.size();
+        // Belady eviction: the s local qubits whose next use as a non-diagonal target
+        // is furthest away (never used again first) go global; ties prefer higher
+        // positions (longer contiguous runs in the exchange's strided blocks)
+        std::vector<int64_t> next_use(n, INT64_MAX);
+        for (int64_t gi = (int64_t)rem_logical.size() - 1; gi >= 0; --gi) {
+            const Gate& g = rem_logical[(size_t)gi];
+            if (!is_diag(g)) next_use[g.t] = gi;
+        }
+        // victims sit at positions >= min_pos so each exchanged block is a set of
+        // contiguous runs of >= 2^min_pos amplitudes (packed / unpacked at HBM speed)
+        static const int min_pos_env = [] {
+            const char* e = std::getenv("QG_REMAP_MIN_POS");
+            return e ? std::atoi(e) : -1;
+        }();
+        const int min_pos = std::max(0, std::min(n_local - (int)need.size(),
+                                                 min_pos_env >= 0 ? min_pos_env : kRemapMinPos));
+        std::vector<int> cand;
+        for (int pl = min_pos; pl < n_local; ++pl) cand.push_back(pl);
+        std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) {
+            const int64_t ua = next_use[inv[a]], ub = next_use[inv[b]];
+            return ua != ub ? ua > ub : a > b;
+        });
+        std::vector<int> victims(cand.begin(), cand.begin() + rm.s);
+        std::sort(victims.begin(), victims.end());
         for (int j = 0; j < rm.s; ++j) {
             rm.global_pos[j] = need[j];
-            rm.local_pos[j] = n_local - rm.s + j;
+            rm.local_pos[j] = victims[j];
         }
         for (int j = 0; j < rm.s; ++j) {
             const int pg = rm.global_pos[j], pl = rm.local_pos[j];

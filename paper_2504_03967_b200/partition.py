@@ -56,12 +56,12 @@ def partner_mask(n_qubits: int, workers: int, qubit: int) -> int:
 def remap_peers(rank: int, n_local: int, global_pos, local_pos):
     """For one remap: [(block j, peer rank)] this rank exchanges, plus its own block index.
 
-    Local positions n_local-s .. n_local-1 (block index bits) swap with global
-    positions global_pos[i] (rank bits global_pos[i] - n_local).  Rank r keeps
-    block g_r (its own G-bits) and trades block j with the rank whose G-bits are j.
-    """
+    Local position local_pos[i] swaps with global position global_pos[i] (rank bit
+    global_pos[i] - n_local).  Block j of a shard = the amplitudes whose local bits
+    local_pos[i] equal bit i of j.  Rank r keeps block g_r (its own G-bits) and
+    trades block j with the rank whose G-bits are j."""
     s = len(global_pos)
-    assert list(local_pos) == list(range(n_local - s, n_local)), "remap must use the top local positions"
+    assert len(local_pos) == s and all(0 <= p < n_local for p in local_pos)
     rb = [p - n_local for p in global_pos]
     own = sum(((rank >> b) & 1) << i for i, b in enumerate(rb))
     clear = rank & ~sum(1 << b for b in rb)
@@ -74,16 +74,46 @@ def remap_peers(rank: int, n_local: int, global_pos, local_pos):
     return own, peers
 
 
+def _contiguous(n_local: int, local_pos) -> bool:
+    """Blocks are contiguous ranges iff the swapped local positions are the top ones."""
+    s = len(local_pos)
+    return list(local_pos) == list(range(n_local - s, n_local))
+
+
+def block_view(t: torch.Tensor, n_local: int, local_pos, j: int) -> torch.Tensor:
+    """Strided view of block j of a shard (local bit local_pos[i] = bit i of j): one
+    dimension per run of untouched index bits, runs of 2^min(local_pos) amplitudes."""
+    order = sorted(range(len(local_pos)), key=lambda i: -local_pos[i])  # most significant first
+    shape, idx, hi = [], [], n_local
+    for i in order:
+        p = local_pos[i]
+        shape += [1 << (hi - 1 - p), 2]
+        idx += [slice(None), (j >> i) & 1]
+        hi = p
+    shape.append(1 << hi)
+    idx.append(slice(None))
+    return t.view(shape)[tuple(idx)]
+
+
+def _chunks(v: torch.Tensor, max_elems: int):
+    """Split a (strided) view into sub-views of at most max_elems elements."""
+    if v.numel() <= max_elems:
+        yield v
+        return
+    d = next(i for i, sz in enumerate(v.shape) if sz > 1)
+    h = v.shape[d] // 2
+    yield from _chunks(v.narrow(d, 0, h), max_elems)
+    yield from _chunks(v.narrow(d, h, v.shape[d] - h), max_elems)
+
+
 def remap_local(shards: list[torch.Tensor], n_local: int, global_pos, local_pos) -> None:
     """In-process remap of W shards (exact semantics of the distributed exchange)."""
-    s = len(global_pos)
-    blk = 1 << (n_local - s)
     old = [t.clone() for t in shards]
     for r, t in enumerate(shards):
         own, peers = remap_peers(r, n_local, global_pos, local_pos)
         for j, peer in peers:
             # peer's block at index `own` (= my G-bits) comes to my block j
-            t[j * blk:(j + 1) * blk].copy_(old[peer][own * blk:(own + 1) * blk])
+            block_view(t, n_local, local_pos, j).copy_(block_view(old[peer], n_local, local_pos, own))
 
 
 REMAP_CHUNK_BYTES = 1 << 30  # per peer and round: bounds the staging memory (37 q / 8 ranks = 128 GiB shards)
@@ -129,6 +159,8 @@ def remap_dist(shard: torch.Tensor, n_local: int, global_pos, local_pos, rank: i
         return 0
     host = shard.is_cuda and _host_wire(group)
     chunk_bytes = REMAP_CHUNK_BYTES if chunk_bytes is None else chunk_bytes
+    if not _contiguous(n_local, local_pos):
+        return _remap_dist_strided(shard, n_local, local_pos, peers, group, host, chunk_bytes)
     chunk = max(1, min(blk, chunk_bytes // shard.element_size()))
     rounds = list(range(0, blk, chunk))
     nbuf = 2 if len(rounds) > 1 and not host else 1
@@ -170,6 +202,39 @@ def remap_dist(shard: torch.Tensor, n_local: int, global_pos, local_pos, rank: i
             done[r % nbuf] = ev
     if side is not None:
         cur.wait_stream(side)
+    return len(peers)
+
+
+def _remap_dist_strided(shard, n_local, local_pos, peers, group, host, chunk_bytes) -> int:
+    """remap_dist for swapped local positions below the top ones (the planner's
+    Belady victims): block j is a strided set of runs of 2^min(local_pos)
+    amplitudes; each round packs one chunk of every outgoing block into a send
+    buffer, exchanges, and unpacks the received chunks into the same positions."""
+    import torch.distributed as dist
+
+    chunk = max(1, chunk_bytes // shard.element_size())
+    per = len(peers) * chunk
+    sdev = torch.device("cpu") if host or not shard.is_cuda else shard.device
+    sendbuf = torch.empty(per, dtype=shard.dtype, device=sdev)
+    recvbuf = torch.empty(per, dtype=shard.dtype, device=sdev)
+    views = [list(_chunks(block_view(shard, n_local, local_pos, j), chunk)) for j, _ in peers]
+
+    def wire(t: torch.Tensor) -> torch.Tensor:
+        return torch.view_as_real(t) if t.is_complex() else t
+
+    for c in range(len(views[0])):
+        ops = []
+        for k, (_, peer) in enumerate(peers):
+            v = views[k][c]
+            m = v.numel()
+            sendbuf[k * chunk:k * chunk + m].view(v.shape).copy_(v)  # pack
+            ops.append(dist.P2POp(dist.isend, wire(sendbuf[k * chunk:k * chunk + m]), peer, group=group))
+            ops.append(dist.P2POp(dist.irecv, wire(recvbuf[k * chunk:k * chunk + m]), peer, group=group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        for k in range(len(peers)):
+            v = views[k][c]
+            v.copy_(recvbuf[k * chunk:k * chunk + v.numel()].view(v.shape))  # unpack
     return len(peers)
 
 
@@ -337,11 +402,13 @@ def execute_distributed(circuit, workers: int, options: sv.SimOptions | None = N
                 sampled = sv.counts_from_arrays(res[0].cpu().numpy(), res[1].cpu().numpy(), options.shots, n)
         if gather:
             host = _host_wire(group)
-            mine = shard.cpu() if host else shard
+            mine = torch.view_as_real(shard)  # complex blocks travel as (re, im) pairs
+            mine = mine.cpu() if host else mine
             parts = [torch.empty_like(mine) for _ in range(workers)] if rank == 0 else None
             dist.gather(mine, parts, dst=0, group=group)
             if rank == 0:
-                full = _permute_to_logical(torch.cat(parts).to(dev), n, plan.final_map)
+                full = torch.view_as_complex(torch.cat(parts).to(dev))
+                full = _permute_to_logical(full, n, plan.final_map)
                 state = sv.StateVector(n, options.precision, full)
     else:
         dev = sv._device(options.device)

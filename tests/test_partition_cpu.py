@@ -52,6 +52,10 @@ def _run(world, n, remaps, chunk_bytes=pt.REMAP_CHUNK_BYTES):
     (2, 6, [([5], [4])], pt.REMAP_CHUNK_BYTES),
     (4, 7, [([6], [4]), ([5, 6], [3, 4]), ([5], [4])], pt.REMAP_CHUNK_BYTES),
     (4, 7, [([5, 6], [3, 4]), ([6], [4])], 48),   # several exchange rounds per block (3 x 16 B chunks)
+    # Belady victims below the top local positions: strided blocks, packed per round
+    (2, 6, [([5], [2])], pt.REMAP_CHUNK_BYTES),
+    (4, 8, [([6, 7], [1, 4]), ([7], [0]), ([6, 7], [5, 2])], pt.REMAP_CHUNK_BYTES),
+    (8, 9, [([6, 7, 8], [0, 3, 5]), ([8, 6], [2, 1])], 32),  # and several rounds
 ])
 def test_gloo_remap_equals_local(world, n, remaps, chunk_bytes):
     got, ref = _run(world, n, remaps, chunk_bytes)
@@ -70,6 +74,21 @@ def test_local_remap_is_a_qubit_swap():
     idx = np.arange(1 << n)
     src = idx.copy()
     for a, b in [(2, 4), (3, 5)]:
+        ba, bb = (src >> a) & 1, (src >> b) & 1
+        src = src ^ ((ba ^ bb) << a) ^ ((ba ^ bb) << b)
+    assert np.array_equal(new, full.numpy()[src])
+
+
+def test_local_remap_arbitrary_positions_is_a_qubit_swap():
+    n, world = 7, 4
+    n_local = n - 2
+    full = torch.arange(1 << n, dtype=torch.float64)
+    shards = [full[r << n_local:(r + 1) << n_local].clone() for r in range(world)]
+    pt.remap_local(shards, n_local, [6, 5], [1, 3])  # swap physical bits (1,6) and (3,5)
+    new = torch.cat(shards).numpy()
+    idx = np.arange(1 << n)
+    src = idx.copy()
+    for a, b in [(1, 6), (3, 5)]:
         ba, bb = (src >> a) & 1, (src >> b) & 1
         src = src ^ ((ba ^ bb) << a) ^ ((ba ^ bb) << b)
     assert np.array_equal(new, full.numpy()[src])

@@ -159,3 +159,23 @@ def test_all_qubits_global_needs_a_local_qubit():
 def test_small_state_tile_choice(precision, n, k):
     gt, gp = random_arrays(RandomSpec(n, 20, 0))
     assert CompiledCircuit(gt, gp, n, precision).info["tile_qubits"] == k
+
+
+def test_belady_remap_counts():
+    """Remap planner: a remap brings in the global targets
+    needed next and evicts the local qubits whose next non-diagonal-target use is
+    furthest away (Belady), at positions >= 10 so each exchanged block is a set of
+    >= 8 KiB runs.  Bounds: SURVEY's Belady estimates (28 at 32 q / 8 ranks, 23 at
+    37 q / 8 ranks); the pre-eviction planner needed 37 and 32."""
+    from paper_2504_03967_b200.generators import RandomSpec, random_arrays
+
+    got = {}
+    for n, g in [(32, 1), (32, 2), (32, 3), (37, 3)]:
+        gt, gp = random_arrays(RandomSpec(n, 1000, 0))
+        p = CompiledCircuit(gt, gp, n, "fp32", g, jit=-1)
+        got[(n, 1 << g)] = p.info["n_remaps"]
+        n_local = n - g
+        for gpos, lpos in p.remaps:
+            assert all(10 <= q < n_local for q in lpos) and all(q >= n_local for q in gpos)
+    assert got[(32, 8)] <= 28 and got[(37, 8)] <= 23
+    assert got[(32, 2)] <= 16 and got[(32, 4)] <= 22
