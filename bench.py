@@ -12,13 +12,14 @@ launching stream, max over ranks.  The state (32 GiB) is far larger than L2
 (126 MB), so no L2 flush is needed between steps.
 
 e2e = the same circuit through the public API paper_2504_03967_b200.statevec.
-run_circuit (planning on the host, the program shipped to the device as kernel
-parameters, execution) followed by the norm read back to the host.
+run_circuit (host gate records -> planning -> JIT pass kernels (process-wide
+cubin cache) -> execution -> tree sampler, --e2e-shots shots) with the (index,
+count) pairs read back to the host.
 
---impl reference: the reference's own CPU algorithm for this path (the oracle
-port of statevec.run_circuit, single-threaded numpy as in the reference) on a
-bounded sample of the same circuit family, extrapolated to 32 qubits with the
-O(2^n) per-gate cost.
+--impl reference: the reference's own CPU executor from baseline/_ref (its
+threaded partition.execute_distributed, the fastest CPU path it has for this
+circuit), rank 0 only: a warm-up ladder n = 23..26 fixes the 2^n slope of the
+per-gate time; each timed step is one bounded sample at 25 qubits scaled to 32.
 """
 
 from __future__ import annotations
@@ -343,20 +344,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---- e2e through the public API (host gate tensor -> plan -> kernels -> norm to host)
     e2e = None
     if not args.no_e2e:
-        opts = sv.SimOptions(precision=prec, memory_budget=1 << 45, device=local_rank, tile_qubits=args.tile_qubits,
-                             max_stages=args.max_stages, max_cost=args.max_cost)
+        opts = sv.SimOptions(precision=prec, shots=args.e2e_shots, rng_seed=args.seed, memory_budget=1 << 45,
+                             device=local_rank, tile_qubits=args.tile_qubits, max_stages=args.max_stages,
+                             max_cost=args.max_cost, sampler="tree")
         circ = generate_random_gate_list(RandomSpec(n, args.blocks, args.seed))
         del shard
         torch.cuda.empty_cache()
 
         def e2e_step():
+            # host gate records in -> plan (+ JIT, cubins from the process-wide cache after the
+            # warm-up call) -> passes (+ remaps) -> tree sampler -> counts on the host
             if world > 1:
                 res = pt.execute_distributed(circ, world, opts, gather=False)
-                res.shards[0].abs().max()  # force completion on this rank
-                return 8
-            state, _ = sv.run_circuit(circ, opts)
-            state.norm_sq()  # 8-byte device -> host read of the result
-            return 8
+            else:
+                _, counts = sv.run_circuit(circ, opts)
+                res = type("R", (), {"counts": counts})
+            c = res.counts
+            return 16 * (len(c.indices) if c is not None else 0) + 16  # (index, count) pairs + mass/nunique
 
         e2e_step()
         barrier()
@@ -372,7 +376,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e2e = {"value": gates / (e2e_ms / 1000.0), "unit": "gates/s",
                "h2d_bytes_per_step": int(plan.info["param_bytes"] + gt.nbytes + gp.nbytes),
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-               "note": "gate tensor planned on the host; the program reaches HBM as kernel parameters"}
+               "shots": args.e2e_shots,
+               "note": ("host gate records -> plan + JIT (cubin cache warm after one warm-up call) -> kernels "
+                        "-> tree sampler; (index, count) pairs of the shots read back to the host; the state "
+                        "stays in HBM")}
 
     if rank != 0:
         return
@@ -456,6 +463,7 @@ def main():
     ap.add_argument("--max-stages", type=int, default=0)
     ap.add_argument("--max-cost", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-shots", type=int, default=100_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-qubits", type=int, default=25)

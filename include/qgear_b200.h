@@ -216,6 +216,9 @@ int qg_sample(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, u
  *            (capacity >= min(shots, n_amps)); mode 1: dense counts
  *            out_count_dev[n_amps] (capacity >= n_amps), out_index_dev unused.
  *            tag (< 2^24) selects an independent stream (the rank of a shard).
+ *            n_out_dev (optional, mode 0): the count also written to device memory,
+ *            stream-ordered — with n_out_host NULL the call never synchronises
+ *            (CUDA-graph capturable, like prepare with mass_host NULL).
  * A sharded state: every rank prepares, the rank masses are all-gathered, and
  * qg_split_shots (same seed on every rank) splits the shots over the ranks by
  * the same binomial tree (tag 1); each rank then draws its count with tag 2+rank.
@@ -226,7 +229,7 @@ int qg_sample_tree_prepare(const void* state, int64_t n_amps, int32_t dtype, voi
 int qg_sample_tree_draw(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
                         int64_t shots, uint64_t seed, uint32_t tag, int32_t mode, int64_t index_base,
                         int64_t* out_index_dev, int64_t* out_count_dev, int64_t capacity, int64_t* n_out_host,
-                        void* stream);
+                        int64_t* n_out_dev, void* stream);
 /* counts_host[r] for r < n_parts (a power of two <= 64) from masses_host[r];
  * workspace: >= 1 KiB of device memory */
 int qg_split_shots(const double* masses_host, int32_t n_parts, int64_t shots, uint64_t seed, void* workspace,

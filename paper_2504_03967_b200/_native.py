@@ -81,7 +81,7 @@ _SIGS = {
     "qg_sample_tree_workspace_bytes": (C.c_int64, [C.c_int64]),
     "qg_sample_tree_prepare": (C.c_int, [_P, C.c_int64, C.c_int32, _P, C.c_int64, C.POINTER(C.c_double), _P]),
     "qg_sample_tree_draw": (C.c_int, [_P, C.c_int64, C.c_int32, _P, C.c_int64, C.c_int64, C.c_uint64, C.c_uint32,
-                                      C.c_int32, C.c_int64, _P, _P, C.c_int64, C.POINTER(C.c_int64), _P]),
+                                      C.c_int32, C.c_int64, _P, _P, C.c_int64, C.POINTER(C.c_int64), _P, _P]),
     "qg_split_shots": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_uint64, _P, C.c_int64, _P, _P]),
     "qg_binomial_test": (C.c_int, [C.c_double, C.c_double, C.c_uint64, C.c_int64, _P, _P]),
     "qg_qgir1_parse": (C.c_int, [_P, C.c_int64, C.POINTER(Qgir1Info)]),

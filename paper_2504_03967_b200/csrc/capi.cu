@@ -542,7 +542,7 @@ int qg_sample_tree_prepare(const void* state, int64_t n_amps, int32_t dtype, voi
 int qg_sample_tree_draw(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,
                         int64_t shots, uint64_t seed, uint32_t tag, int32_t mode, int64_t index_base,
                         int64_t* out_index_dev, int64_t* out_count_dev, int64_t capacity, int64_t* n_out_host,
-                        void* stream) {
+                        int64_t* n_out_dev, void* stream) {
     DeviceGuard dg_(state);
     if (int rc = check_dtype(dtype)) return rc;
     if (shots < 0 || shots >= (1ll << 53)) return fail(QG_E_INVALID_ARG, "shots must be in [0, 2^53)");
@@ -558,6 +558,8 @@ int qg_sample_tree_draw(const void* state, int64_t n_amps, int32_t dtype, void* 
     QG_CUDA(qg::tree_draw(state, n_amps, dtype, workspace, shots, seed, tag, mode, index_base, out_index_dev,
                           out_count_dev, mode == 0 ? nu : nullptr, st),
             "tree draw");
+    if (n_out_dev && mode == 0)
+        QG_CUDA(cudaMemcpyAsync(n_out_dev, nu, 8, cudaMemcpyDeviceToDevice, st), "nunique copy");
     if (n_out_host) {
         if (mode == 0) {
             QG_CUDA(cudaMemcpyAsync(n_out_host, nu, 8, cudaMemcpyDeviceToHost, st), "nunique copy");

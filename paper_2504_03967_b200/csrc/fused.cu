@@ -780,6 +780,7 @@ cudaError_t launch_fused(int dtype, int cfg_id, const void* desc, void* psi, uin
             case 5: return launch_fused_t<float, 5, 4, 1>(P, psi, rank_bits, st);
             case 6: return launch_fused_t<float, 5, 2, 1>(P, psi, rank_bits, st);
             case 7: return launch_fused_t<float, 6, 3, 1>(P, psi, rank_bits, st);
+            case 8: return launch_fused_t<float, 6, 2, 1>(P, psi, rank_bits, st);
             default: return launch_fused_t<float, 3, 0>(P, psi, rank_bits, st);
         }
     }

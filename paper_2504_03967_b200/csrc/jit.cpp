@@ -24,10 +24,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
+#include <unordered_map>
 #include <sstream>
 
 namespace qg {
+
+std::atomic<int64_t> g_cache_hits{0};
 
 namespace {
 
@@ -372,6 +376,11 @@ struct Gen {
     // ---------------------------------------------------------------- addressing
     // per-thread table entries (SMEM, written in the prologue)
     std::string gb_of(int m) {
+        if (variant & 524288) {  // per-thread mapping values held in registers (no SMEM table reads)
+            std::string v = q();
+            L("mov.b64 ", v, ", %gbm", m, ";");
+            return v;
+        }
         std::string a1 = q(), a2 = q(), v = q();
         L("ld.shared.u64 ", a1, ", [%tl8+", (size_t)m * kMapBytes, "];");
         L("ld.shared.u64 ", a2, ", [%tw8+", (size_t)m * kMapBytes + 256, "];");
@@ -379,6 +388,11 @@ struct Gen {
         return v;
     }
     std::string so_of(int m) {
+        if (variant & 524288) {
+            std::string v = r();
+            L("mov.b32 ", v, ", %som", m, ";");
+            return v;
+        }
         std::string a1 = r(), a2 = r(), v = r();
         L("ld.shared.u32 ", a1, ", [%tl4+", (size_t)m * kMapBytes + 384, "];");
         L("ld.shared.u32 ", a2, ", [%tw4+", (size_t)m * kMapBytes + 512, "];");
@@ -721,6 +735,13 @@ struct Gen {
         base_reg("%tw4", warp, 2);
         L("setp.eq.u32 %pw0, ", warp, ", 0;");
         L("setp.eq.u32 %pl0, ", lane, ", 0;");
+        if (variant & 524288)
+            for (int m = 0; m <= ns; ++m) {
+                std::string g, so;
+                thread_map(m, lane, warp, g, so, true, true);
+                L("mov.b64 %gbm", m, ", ", g, ";");
+                L("mov.b32 %som", m, ", ", so, ";");
+            }
         for (int m = 0; m <= ns; ++m) {
             std::string gl, sl, gw, sw;
             thread_map(m, lane, warp, gl, sl, true, false);
@@ -1060,10 +1081,17 @@ struct Gen {
                 }
             }
             std::map<uint64_t, std::pair<std::string, Bases>> bases;
+            std::vector<std::pair<uint64_t, int>> order;  // variant 2097152: stores in ascending address
             for (int i = 0; i < R; ++i) {
                 uint64_t og = 0;
                 for (int b = 0; b < RB; ++b)
                     if (i & (1 << b)) og ^= S.out_g[b];
+                order.push_back({og, i});
+            }
+            if (variant & 2097152) std::sort(order.begin(), order.end());
+            for (const auto& oi : order) {
+                const int i = oi.second;
+                const uint64_t og = oi.first;
                 const uint64_t lo = og & lm, hi = og & ~lm;
                 auto it = bases.find(lo);
                 if (it == bases.end()) {
@@ -1071,7 +1099,15 @@ struct Gen {
                     if (lo) L("xor.b64 ", x, ", ", idx, ", ", u64s(lo), ";");
                     else L("mov.b64 ", x, ", ", idx, ";");
                     L("shl.b64 ", x, ", ", x, ", 3;");
-                    L("add.s64 ", x, ", ", x, ", %pt;");
+                    if (variant & 1048576) {  // timing probe: stores into a 16 MiB L2-resident window
+                        std::string y = q();
+                        L("add.s64 ", y, ", ", x, ", %pt;");
+                        L("sub.s64 ", y, ", ", y, ", %psi;");
+                        L("and.b64 ", y, ", ", y, ", 0xffffff;");
+                        L("add.s64 ", x, ", ", y, ", %psi;");
+                    } else {
+                        L("add.s64 ", x, ", ", x, ", %pt;");
+                    }
                     it = bases.emplace(lo, std::make_pair(x, Bases{})).first;
                 }
                 L((variant & 65536) ? "st.global.b64 " : "st.global.cs.b64 ",
@@ -1101,6 +1137,7 @@ struct Gen {
         h << "\t.reg .pred %p<" << (np + 1) << ">;\n";
         h << "\t.reg .b32 %xtid, %xlane, %xwarp, %smb, %smb2, %tlin, %tl8, %tw8, %tl4, %tw4, %F, %ctile, %nctile;\n";
         h << "\t.reg .b64 %rdl;\n";
+        h << "\t.reg .b64 %gbm<" << (P.n_stages + 1) << ">;\n\t.reg .b32 %som<" << (P.n_stages + 1) << ">;\n";
         h << "\t.reg .b64 %tile, %tend, %ntile, %G, %base, %nbase, %dG, %psi, %rk, %pt;\n";
         h << "\t.reg .pred %pfl, %pend, %pnext, %pw0, %pl0;\n";
         return h.str() + o.str() + "}\n";
@@ -1111,8 +1148,10 @@ struct Gen {
 
 int jit_variant() {
     static const int v = [] {
+        // default: per-thread mapping values in registers (524288); the other bits are
+        // measurement probes (tools/jit_time.py, profiles/r02*_jit_variants*.jsonl)
         const char* e = std::getenv("QG_JIT_VARIANT");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : 524288;
     }();
     return v;
 }
@@ -1127,6 +1166,33 @@ std::string jit_ptx_c64(const PassDesc<float>& P, int rb, int wb, int nbuf, cons
 size_t jit_smem_bytes(const PassDesc<float>& P, int rb, int wb, int nbuf) {
     return Gen::smem_bytes(P, rb, wb, nbuf, jit_variant());
 }
+
+// Process-wide cache of compiled passes keyed by their PTX text: re-planning the
+// same circuit (run_circuit called again, batched rebinding with unchanged
+// parameters, bench steps) reuses the cubins instead of recompiling.
+namespace {
+std::mutex g_cache_mu;
+std::unordered_map<std::string, std::shared_ptr<const std::vector<char>>> g_cache;
+size_t g_cache_bytes = 0;
+constexpr size_t kCacheMaxBytes = (size_t)1 << 30;  // PTX + cubin bytes kept
+
+std::shared_ptr<const std::vector<char>> cache_get(const std::string& ptx) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(ptx);
+    return it == g_cache.end() ? nullptr : it->second;
+}
+void cache_put(const std::string& ptx, const std::vector<char>& cubin) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (g_cache_bytes + ptx.size() + cubin.size() > kCacheMaxBytes) {
+        g_cache.clear();
+        g_cache_bytes = 0;
+    }
+    if (g_cache.emplace(ptx, std::make_shared<const std::vector<char>>(cubin)).second)
+        g_cache_bytes += ptx.size() + cubin.size();
+}
+}  // namespace
+
+int64_t jit_cache_hits() { return g_cache_hits.load(); }
 
 bool jit_compile(const std::string& ptx, std::vector<char>& cubin, std::string& log) {
     nvPTXCompilerHandle h = nullptr;
@@ -1235,7 +1301,14 @@ std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int
             if (!ptx.empty()) {
                 jk->smem = jit_smem_bytes(P, rb, wb, nbuf);
                 if (const char* e = std::getenv("QG_JIT_SMEM_PAD")) jk->smem += (size_t)std::atol(e);  // occupancy probe
-                jk->ok = jit_compile(ptx, jk->cubin, jk->err);
+                if (auto hit = cache_get(ptx)) {
+                    jk->cubin = *hit;
+                    jk->ok = true;
+                    g_cache_hits.fetch_add(1);
+                } else {
+                    jk->ok = jit_compile(ptx, jk->cubin, jk->err);
+                    if (jk->ok) cache_put(ptx, jk->cubin);
+                }
             } else {
                 jk->err = "pass not covered by the emitter";
             }

@@ -78,5 +78,7 @@ struct JitState {
 };
 std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int rb, int wb, int nbuf, int threads);
 int jit_default_threads();
+// passes whose cubin came from the process-wide PTX -> cubin cache (jit.cpp)
+int64_t jit_cache_hits();
 
 }  // namespace qg

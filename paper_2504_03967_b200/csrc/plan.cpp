@@ -128,7 +128,7 @@ static int validate(const int32_t* gt, const double* gp, int64_t n_gates, int n,
 // forces one (tuning)
 // (ids must match launch_fused in fused.cu; array index = id)
 static const KernelCfg kCfgC64[] = {{0, 4, 4}, {1, 4, 3}, {2, 4, 2}, {3, 3, 0}, {4, 5, 3}, {5, 5, 4}, {6, 5, 2},
-                                    {7, 6, 3}};
+                                    {7, 6, 3}, {8, 6, 2}};
 static const KernelCfg kCfgC128[] = {{0, 4, 3}, {1, 3, 2}, {2, 3, 0}, {3, 5, 3}};
 // auto preference order (ids)
 static const int kAutoC64[] = {4, 1, 2, 3};
@@ -136,7 +136,7 @@ static const int kAutoC128[] = {3, 0, 1, 2};
 
 static bool pick_cfg(int dtype, int n_local, int force_k, int force_cfg, KernelCfg& out) {
     const KernelCfg* cfgs = dtype == QG_DTYPE_C64 ? kCfgC64 : kCfgC128;
-    const int n_all = dtype == QG_DTYPE_C64 ? 8 : 4;
+    const int n_all = dtype == QG_DTYPE_C64 ? 9 : 4;
     const int* order = dtype == QG_DTYPE_C64 ? kAutoC64 : kAutoC128;
     const int nc = 4;  // auto candidates per dtype
     if (force_cfg > 0) {
@@ -1072,6 +1072,7 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
     // small states live in L2: no coalescing constraint; large ones keep the lowest
     // c_low qubits in every tile, so each HBM access is a 2^c_low-amplitude run
     int c_low = n_local >= 20 ? kLaneBits : 0;
+    if (const char* e = std::getenv("QG_DEV_CLOW")) c_low = std::atoi(e);  // dev probe only
     if (opts.low_qubits > 0 && n_local >= 20) c_low = std::min(std::max(opts.low_qubits, kLaneBits), cfg.k() - 1);
 
     std::vector<int> phys(n), inv(n);  // logical -> physical, physical -> logical

@@ -432,6 +432,29 @@ def decode_counts(counts, plan: QCrankPlan, source: ImageGray | None = None):
     return _reconstruct(n0, n1, tot, plan, source)
 
 
+def sample_decode(state: sv.StateVector, plan: QCrankPlan, rng_seed: int = 0, source: ImageGray | None = None,
+                  shots: int | None = None):
+    """SPEC.md:473-480 at the paper's shot budget s * 2^m (~5e10 for
+    m = 24): the tree sampler draws the multinomial counts straight into a dense
+    per-outcome array in HBM (no per-shot records), the (address, data bit)
+    marginals are reduced on the device, and only the 2^m x n_data tallies reach
+    the host for the reconstruction."""
+    shots = plan.shots if shots is None else int(shots)
+    m, nd = plan.n_addr, plan.n_data
+    ts = sv.TreeSampler(state.amplitudes)
+    mass = ts.prepare()
+    if not abs(mass - 1.0) <= sv.NORM_TOL[state.precision]:
+        raise sv.UnnormalizedStateError(f"norm^2 = {mass!r} outside tolerance")
+    dense = ts.draw(shots, rng_seed, dense=True)
+    c = dense.view(1 << nd, 1 << m)          # index = address + 2^m * data bits
+    tot = c.sum(0)
+    n1 = torch.stack([c.view(1 << (nd - 1 - d), 2, 1 << d, 1 << m)[:, 1].sum((0, 1)) for d in range(nd)], dim=1)
+    del dense, c
+    tot_h = tot.double().cpu().numpy()
+    n1_h = n1.double().cpu().numpy()
+    return _reconstruct(tot_h[:, None] - n1_h, n1_h, tot_h, plan, source)
+
+
 def decode_exact(probabilities, plan: QCrankPlan, source: ImageGray | None = None):
     """the same estimator with exact marginals."""
     p = probabilities.cpu().numpy() if isinstance(probabilities, torch.Tensor) else np.asarray(probabilities)

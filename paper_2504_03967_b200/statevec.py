@@ -442,6 +442,24 @@ class TreeSampler:
         self.mass = m.value
         return self.mass
 
+    def prepare_async(self) -> None:
+        """prepare() without reading the mass back (stream-ordered; CUDA-graph safe)."""
+        N.call("qg_sample_tree_prepare", C.c_void_p(self.amps.data_ptr()), 1 << self.n, self.dtype,
+               C.c_void_p(self.ws.data_ptr()), self.ws.numel(), None, _stream(self.amps.device))
+
+    def mass_device(self) -> torch.Tensor:
+        """The mass computed by the last prepare, as a 1-element device view (heap root)."""
+        return self.ws[:8].view(torch.float64)
+
+    def draw_into(self, shots: int, rng_seed: int, tag: int, idx: torch.Tensor, cnt: torch.Tensor,
+                  n_out: torch.Tensor) -> None:
+        """(index, count) pairs into preallocated buffers and their number into the
+        1-element int64 device tensor n_out, with no host synchronisation."""
+        N.call("qg_sample_tree_draw", C.c_void_p(self.amps.data_ptr()), 1 << self.n, self.dtype,
+               C.c_void_p(self.ws.data_ptr()), self.ws.numel(), int(shots), C.c_uint64(rng_seed & (2**64 - 1)),
+               int(tag), 0, self.index_base, C.c_void_p(idx.data_ptr()), C.c_void_p(cnt.data_ptr()), idx.numel(),
+               None, C.c_void_p(n_out.data_ptr()), _stream(self.amps.device))
+
     def draw(self, shots: int, rng_seed: int = 0, tag: int = 2, dense: bool = False):
         if self.mass is None:
             self.prepare()
@@ -454,11 +472,67 @@ class TreeSampler:
         N.call("qg_sample_tree_draw", C.c_void_p(self.amps.data_ptr()), na, self.dtype, C.c_void_p(self.ws.data_ptr()),
                self.ws.numel(), int(shots), C.c_uint64(rng_seed & (2**64 - 1)), int(tag), 1 if dense else 0,
                self.index_base, C.c_void_p(0 if idx is None else idx.data_ptr()), C.c_void_p(cnt.data_ptr()), cap,
-               C.byref(nout), _stream(dev))
+               C.byref(nout), None, _stream(dev))
         if dense:
             return cnt
         k = nout.value
         return idx[:k], cnt[:k]
+
+
+class CircuitGraph:
+    """One planned circuit captured as a CUDA graph: |0..0> init, every fused pass
+    and (shots > 0) the tree sampler.  replay() is one graph launch with no host
+    synchronisation; result() reads the norm and the outcome count back (one
+    sync) and checks the norm like sample_counts (statevec.py:226-228).  For
+    small, launch-bound circuits run many times (BASELINE configs[0]: 16 q,
+    300 gates, complex128, 3000 shots)."""
+
+    def __init__(self, plan: "CompiledCircuit", shots: int = 0, rng_seed: int = 0, device=None):
+        if plan.log2_ranks:
+            raise ValueError("multi-rank plan: use paper_2504_03967_b200.partition")
+        n, prec = plan.n_qubits, plan.precision
+        self.plan, self.shots, self.seed = plan, int(shots), int(rng_seed)
+        self.state = init_zero_state(n, prec, 1 << 62, device)
+        amps = self.state.amplitudes
+        dev = amps.device
+        self.ts = TreeSampler(amps) if shots > 0 else None
+        cap = max(1, min(self.shots, 1 << n))
+        self.idx = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.cnt = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.nout = torch.zeros(1, dtype=torch.int64, device=dev)
+        side = torch.cuda.Stream(dev)  # warm-up off the capture: JIT libraries load, CUB settles
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            self._body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
+            self._body()
+
+    def _body(self):
+        amps = self.state.amplitudes
+        N.call("qg_state_init_zero", C.c_void_p(amps.data_ptr()), self.plan.n_qubits,
+               _QG_DTYPE[self.plan.precision], 0, _stream(amps.device))
+        self.plan.execute(self.state)
+        if self.ts is not None:
+            self.ts.prepare_async()
+            self.ts.draw_into(self.shots, self.seed, 2, self.idx, self.cnt, self.nout)
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def result(self):
+        """(StateVector, CountsTable | None) of the last replay."""
+        counts = None
+        if self.ts is not None:
+            m = float(self.ts.mass_device().item())
+            if not abs(m - 1.0) <= NORM_TOL[self.plan.precision]:
+                raise UnnormalizedStateError(f"norm^2 = {m!r} outside tolerance")
+            k = int(self.nout.item())
+            counts = counts_from_arrays(self.idx[:k].cpu().numpy(), self.cnt[:k].cpu().numpy(), self.shots,
+                                        self.plan.n_qubits)
+        return self.state, counts
 
 
 def split_shots(masses, shots: int, rng_seed: int, device=None) -> list[int]:

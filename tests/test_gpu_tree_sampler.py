@@ -149,3 +149,27 @@ def test_split_shots():
     assert sum(a) == 10**9 and a[2] == 0 and a == sv.split_shots(m, 10**9, 3)
     for i, mi in enumerate(m):
         assert abs(a[i] - mi * 1e9) <= 6 * math.sqrt(1e9 * mi * (1 - mi)) + 1e-9
+
+
+def test_circuit_graph_config1():
+    """BASELINE configs[0] (16 q x 100 blocks, complex128, 3000 shots) as one CUDA
+    graph replay: state vs the oracle at 1e-12, counts of 3000 shots, identical on
+    replay (same seed)."""
+    n = 16
+    gt, gp = random_arrays(RandomSpec(n, 100, 0))
+    plan = sv.CompiledCircuit(gt, gp, n, "fp64")
+    g = sv.CircuitGraph(plan, 3000, 0)
+    g.replay()
+    st, c1 = g.result()
+    ref = oracle.run_arrays(gt, gp, n, gt.shape[0], "fp64")
+    got = st.to_numpy()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
+    assert c1.total == 3000 and sum(c1.counts.values()) == 3000
+    g.replay()
+    _, c2 = g.result()
+    assert c1.counts == c2.counts
+    shots = 300_000
+    g = sv.CircuitGraph(plan, shots, 4)
+    g.replay()
+    _, c = g.result()
+    _check_counts(c.indices, c.values, oracle.exact_probabilities(ref), n, shots)
