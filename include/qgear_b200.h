@@ -184,6 +184,12 @@ int qg_apply_ucry(void* state, int32_t n_local, int32_t dtype, const int32_t* ad
                   const int32_t* targets, int32_t n_targets, const double* alpha_dev, void* workspace,
                   int64_t workspace_bytes, void* stream);
 
+/* QCrank decode tallies from dense per-outcome counts
+ * (qg_sample_tree_draw mode 1) of an m-address + n_data-data-qubit state
+ * (outcome = address + 2^m * data bits): tot_dev[a] = shots at address a,
+ * n1_dev[a * n_data + j] = those with data qubit j = 1; one HBM read. */
+int qg_qcrank_tally(const int64_t* dense_counts, int32_t m, int32_t n_data, int64_t* tot_dev, int64_t* n1_dev,
+                    void* stream);
 /* ---- reductions and sampling (statevec.py:47-50, 215-234) ----------------- */
 /* sum |a|^2 in float64; result written to *out_host (synchronises `stream`) */
 int qg_norm_sq(const void* state, int64_t n_amps, int32_t dtype, void* workspace, int64_t workspace_bytes,

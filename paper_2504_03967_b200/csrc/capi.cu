@@ -517,6 +517,15 @@ int qg_sample(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, u
     return QG_OK;
 }
 
+int qg_qcrank_tally(const int64_t* dense_counts, int32_t m, int32_t n_data, int64_t* tot_dev, int64_t* n1_dev,
+                    void* stream) {
+    DeviceGuard dg_(dense_counts);
+    if (!dense_counts || !tot_dev || !n1_dev || m < 0 || n_data < 1 || n_data > 16 || m + n_data > 62)
+        return fail(QG_E_INVALID_ARG, "bad qcrank tally arguments");
+    QG_CUDA(qg::launch_qcrank_tally(dense_counts, m, n_data, tot_dev, n1_dev, (cudaStream_t)stream), "qcrank tally");
+    return QG_OK;
+}
+
 // ---- tree (binomial-split) sampler --------------------------------------------
 int64_t qg_sample_tree_workspace_bytes(int64_t n_amps) {
     if (n_amps < 1 || (n_amps & (n_amps - 1))) return -1;

@@ -20,6 +20,7 @@ struct UcryOp {
 };
 int64_t ucry_workspace_bytes(int m, int n_t, int dtype);
 cudaError_t launch_ucry(int dtype, void* psi, const UcryOp& op, const double* alpha_dev, void* ws, cudaStream_t st);
+cudaError_t launch_qcrank_tally(const int64_t* dense, int m, int nd, int64_t* tot, int64_t* n1, cudaStream_t st);
 
 cudaError_t launch_init_zero(void* psi, int n_local, int dtype, int rank, cudaStream_t st);
 cudaError_t launch_init_uniform(void* psi, int n_local, int dtype, int rank, uint64_t mask, cudaStream_t st);

@@ -78,14 +78,12 @@ struct NodeRng {
 };
 
 // log(k!) - [(k + 1/2) log(k + 1) - (k + 1) + log(2 pi) / 2]  (Stirling series tail)
+__constant__ double kStirlingTail[10] = {0.08106146679532733, 0.04134069595540946, 0.027677925684997717,
+                                         0.02079067210376584, 0.01664469118982126, 0.013876128823072875,
+                                         0.011896709945893313, 0.010411265261973668, 0.00925546218270945,
+                                         0.008330563433359472};
 __device__ __forceinline__ double stirling_tail(double k) {
-    if (k <= 9) {
-        constexpr double t[10] = {0.08106146679532733, 0.04134069595540946, 0.027677925684997717,
-                                  0.02079067210376584, 0.01664469118982126, 0.013876128823072875,
-                                  0.011896709945893313, 0.010411265261973668, 0.00925546218270945,
-                                  0.008330563433359472};
-        return t[(int)k];
-    }
+    if (k <= 9) return kStirlingTail[(int)k];
     const double kp1sq = (k + 1) * (k + 1);
     return (1.0 / 12 - (1.0 / 360 - 1.0 / 1260 / kp1sq) / kp1sq) / (k + 1);
 }
@@ -297,6 +295,97 @@ __global__ void tree_leaf(const T2* __restrict__ psi, int64_t n_sub, int sb, int
         }
 }
 
+// ---------------------------------------------------------------- dense mode: level-synchronous
+// Below the stored leaves the dense count array itself holds the tree: node (d, i)
+// lives at position i << (nl - d), its left child at the same position, its right
+// child at + half.  One level per launch, one binomial per node (a warp per node for
+// ranges >= 64 amplitudes, a thread per node below): no dependency chains inside a
+// warp, so the binomials run at the generator's throughput.  Children masses are
+// balanced pairwise sums in index order — bitwise the sums tree_leaf forms with its
+// in-lane adds and xor-butterflies — so both modes draw the same counts.
+__global__ void scatter_leaves(const int64_t* __restrict__ leaf_cnt, int64_t n_sub, int sb_log,
+                               int64_t* __restrict__ dense) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_sub; j += (int64_t)gridDim.x * blockDim.x)
+        dense[j << sb_log] = leaf_cnt[j];
+}
+
+template <typename T2, int C>
+__device__ __forceinline__ double tree_sum(const T2* __restrict__ p) {  // balanced pairwise sum of C amplitudes
+    double v[C];
+#pragma unroll
+    for (int a = 0; a < C; ++a) v[a] = pr(p[a]);
+#pragma unroll
+    for (int w = 1; w < C; w <<= 1)
+#pragma unroll
+        for (int a = 0; a < C; a += 2 * w) v[a] += v[a + w];
+    return v[0];
+}
+
+template <typename T2, int H>  // thread per node, children of H amplitudes (H <= 16)
+__global__ void level_thread(const T2* __restrict__ psi, int64_t* __restrict__ dense, int nl, int d, uint64_t seed,
+                             uint32_t tag) {
+    const int64_t nn = 1ll << d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pos = i << (nl - d);
+        const int64_t n = dense[pos];
+        if (n == 0) {
+            dense[pos + H] = 0;
+            continue;
+        }
+        const double mL = tree_sum<T2, H>(psi + pos), mR = tree_sum<T2, H>(psi + pos + H);
+        const int64_t k = (int64_t)split((double)n, mL, mR, seed, tag, d, (uint64_t)i);
+        dense[pos] = k;
+        dense[pos + H] = n - k;
+    }
+}
+
+template <typename T2, int C>  // warp per node, each lane sums C consecutive amplitudes (node = 32 C amps)
+__global__ void level_warp(const T2* __restrict__ psi, int64_t* __restrict__ dense, int nl, int d, uint64_t seed,
+                           uint32_t tag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nn = 1ll << d;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int R = 32 * C;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nn; i += warps) {
+        const int64_t pos = i * R;
+        const int64_t n = dense[pos];
+        if (n == 0) {
+            if (lane == 0) dense[pos + R / 2] = 0;
+            continue;
+        }
+        double m = tree_sum<T2, C>(psi + pos + (int64_t)lane * C);
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);  // half-warp = one child
+        const double mR = __shfl_sync(0xffffffffu, m, 16);
+        if (lane == 0) {
+            const int64_t k = (int64_t)split((double)n, m, mR, seed, tag, d, (uint64_t)i);
+            dense[pos] = k;
+            dense[pos + R / 2] = n - k;
+        }
+    }
+}
+
+template <typename T2>
+cudaError_t dense_levels(const T2* psi, int64_t* dense, int nl, int D, uint64_t seed, uint32_t tag, cudaStream_t st) {
+    for (int d = D; d < nl; ++d) {
+        const int r = nl - d;  // node range 2^r amplitudes
+        const int64_t nn = 1ll << d;
+        const unsigned tb = (unsigned)std::min<int64_t>((nn + 255) / 256, 148 * 32);
+        const unsigned wb = (unsigned)std::min<int64_t>((nn * 32 + 255) / 256, 148 * 32);
+        switch (r) {
+            case 8: level_warp<T2, 8><<<wb, 256, 0, st>>>(psi, dense, nl, d, seed, tag); break;
+            case 7: level_warp<T2, 4><<<wb, 256, 0, st>>>(psi, dense, nl, d, seed, tag); break;
+            case 6: level_warp<T2, 2><<<wb, 256, 0, st>>>(psi, dense, nl, d, seed, tag); break;
+            case 5: level_thread<T2, 16><<<tb, 256, 0, st>>>(psi, dense, nl, d, seed, tag); break;
+            case 4: level_thread<T2, 8><<<tb, 256, 0, st>>>(psi, dense, nl, d, seed, tag); break;
+            case 3: level_thread<T2, 4><<<tb, 256, 0, st>>>(psi, dense, nl, d, seed, tag); break;
+            case 2: level_thread<T2, 2><<<tb, 256, 0, st>>>(psi, dense, nl, d, seed, tag); break;
+            default: level_thread<T2, 1><<<tb, 256, 0, st>>>(psi, dense, nl, d, seed, tag); break;
+        }
+    }
+    return cudaGetLastError();
+}
+
 __global__ void split_parts(const double* __restrict__ masses, int n_parts, int64_t shots, uint64_t seed,
                             int64_t* __restrict__ out) {
     // binary tree over the parts (n_parts a power of two), tag 1, one thread
@@ -390,6 +479,12 @@ cudaError_t tree_draw(const void* psi, int64_t n_amps, int dtype, void* ws, int6
     const int sb = (int)L.sb;
     auto leaf = [&](auto* p) {
         using T2 = std::remove_const_t<std::remove_pointer_t<decltype(p)>>;
+        if (mode == 1 && sb == kSubT) {  // level-synchronous below the stored leaves
+            const int nl = 63 - __builtin_clzll((unsigned long long)n_amps);
+            scatter_leaves<<<(unsigned)std::min<int64_t>((L.n_sub + 255) / 256, 148 * 32), 256, 0, st>>>(
+                leaf_cnt, L.n_sub, 8, out_cnt);
+            return dense_levels<T2>(p, out_cnt, nl, L.D, seed, tag, st);
+        }
         if (mode == 1) {
             tree_leaf<T2, 2><<<blocks, 256, 0, st>>>(p, L.n_sub, sb, L.D, leaf_cnt, seed, tag, idx_base, nullptr,
                                                      nullptr, nullptr, out_cnt);

@@ -17,6 +17,8 @@
 //
 // Traffic = read + write of the state once (+ the table, 2^m * T * 2 reals).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "kernels.h"
@@ -146,6 +148,33 @@ int64_t ucry_workspace_bytes(int m, int n_t, int dtype) {
 
 cudaError_t launch_ucry(int dtype, void* psi, const UcryOp& op, const double* alpha_dev, void* ws, cudaStream_t st) {
     return dtype == 0 ? launch_t<float>(psi, op, alpha_dev, ws, st) : launch_t<double>(psi, op, alpha_dev, ws, st);
+}
+
+// QCrank decode tallies from dense per-outcome counts: outcome
+// index = address (low m bits) + 2^m * data bits.  One thread per address walks its
+// 2^n_data outcomes (a warp reads 32 consecutive addresses per outcome: coalesced):
+// tot[a] = all shots at address a, n1[a * n_data + j] = those with data bit j = 1.
+__global__ void qcrank_tally(const int64_t* __restrict__ dense, int m, int nd, int64_t* __restrict__ tot,
+                             int64_t* __restrict__ n1) {
+    const int64_t na = 1ll << m;
+    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < na; a += (int64_t)gridDim.x * blockDim.x) {
+        int64_t t = 0, b[16] = {};
+        for (int64_t d = 0; d < (1ll << nd); ++d) {
+            const int64_t c = __ldcs(dense + a + (d << m));
+            t += c;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < nd && ((d >> j) & 1)) b[j] += c;
+        }
+        tot[a] = t;
+        for (int j = 0; j < nd; ++j) n1[a * nd + j] = b[j];
+    }
+}
+
+cudaError_t launch_qcrank_tally(const int64_t* dense, int m, int nd, int64_t* tot, int64_t* n1, cudaStream_t st) {
+    const int64_t na = 1ll << m;
+    qcrank_tally<<<(unsigned)std::min<int64_t>((na + 255) / 256, 148 * 16), 256, 0, st>>>(dense, m, nd, tot, n1);
+    return cudaGetLastError();
 }
 
 }  // namespace qg

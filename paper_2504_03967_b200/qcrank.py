@@ -445,11 +445,13 @@ def sample_decode(state: sv.StateVector, plan: QCrankPlan, rng_seed: int = 0, so
     mass = ts.prepare()
     if not abs(mass - 1.0) <= sv.NORM_TOL[state.precision]:
         raise sv.UnnormalizedStateError(f"norm^2 = {mass!r} outside tolerance")
-    dense = ts.draw(shots, rng_seed, dense=True)
-    c = dense.view(1 << nd, 1 << m)          # index = address + 2^m * data bits
-    tot = c.sum(0)
-    n1 = torch.stack([c.view(1 << (nd - 1 - d), 2, 1 << d, 1 << m)[:, 1].sum((0, 1)) for d in range(nd)], dim=1)
-    del dense, c
+    dense = ts.draw(shots, rng_seed, dense=True)  # index = address + 2^m * data bits
+    dev = dense.device
+    tot = torch.empty(1 << m, dtype=torch.int64, device=dev)
+    n1 = torch.empty((1 << m, nd), dtype=torch.int64, device=dev)
+    N.call("qg_qcrank_tally", C.c_void_p(dense.data_ptr()), m, nd, C.c_void_p(tot.data_ptr()),
+           C.c_void_p(n1.data_ptr()), sv._stream(dev))
+    del dense
     tot_h = tot.double().cpu().numpy()
     n1_h = n1.double().cpu().numpy()
     return _reconstruct(tot_h[:, None] - n1_h, n1_h, tot_h, plan, source)

@@ -156,7 +156,8 @@ def _basis_then_qft(n, k, reversed_=False):
     return gt2, gp2, len(pre)
 
 
-def test_qft28_complex64_on_basis_state_is_dft():
+@pytest.mark.parametrize("jit", [-1, 1])
+def test_qft28_complex64_on_basis_state_is_dft(jit):
     """C2 scale (QFT 28 q, complex64) with FIRING controlled phases: on |0...0> every
     CR1 acts as the identity, on |bitrev(k)> every row's phase list is non-trivial
     (long predicated PH lists, tile-uniform slots, register/thread-controlled factors).
@@ -164,7 +165,7 @@ def test_qft28_complex64_on_basis_state_is_dft():
     rel-L2 <= 1e-5 (north_star complex64 tolerance)."""
     n, k = 28, 0x5A5A5A7
     gt, gp, npre = _basis_then_qft(n, k)
-    st, _ = sv.run_circuit(circuit(gt, gp, n), sv.SimOptions(precision="fp32", memory_budget=1 << 40))
+    st, _ = sv.run_circuit(circuit(gt, gp, n), sv.SimOptions(precision="fp32", memory_budget=1 << 40, jit=jit))
     a = st.amplitudes
     phase = complex(1j ** npre)
     num = den = 0.0

@@ -198,3 +198,34 @@ def test_image_round_trip_with_shots():
     assert rep.max_abs_error < 6 / math.sqrt(plan.shots_per_address)
     rep_x, _ = qc.decode_exact(sv.exact_probabilities(st), plan, img)
     assert rep_x.max_abs_error < 1e-5
+
+
+@pytest.mark.gpu
+def test_sample_decode_dense_tally_matches_counts():
+    """sample_decode (tree sampler dense counts -> qg_qcrank_tally on the device) agrees
+    with the host marginals of the same counts, and reconstructs the image within the
+    shot-noise bound at the paper's budget s * 2^m."""
+    import torch
+
+    from paper_2504_03967_b200 import statevec as sv
+
+    rng = np.random.default_rng(5)
+    m, nd = 10, 3
+    img = qc.ImageGray(32, 96, rng.integers(0, 256, (1 << m) * nd, dtype=np.uint8))
+    plan = qc.make_plan(img, m, nd)
+    st, _ = qc.simulate(qc.prepare_angles(img, m, nd), sv.SimOptions("fp32"))
+    rep, _ = qc.sample_decode(st, plan, 7, img)
+    assert rep.correlation >= 0.99 and rep.max_abs_error < 6 / math.sqrt(plan.shots_per_address)
+    # the device tally equals the host marginals of the same dense counts
+    ts = sv.TreeSampler(st.amplitudes)
+    ts.prepare()
+    dense = ts.draw(plan.shots, 7, dense=True)
+    tot = torch.empty(1 << m, dtype=torch.int64, device=dense.device)
+    n1 = torch.empty((1 << m, nd), dtype=torch.int64, device=dense.device)
+    sv.N.call("qg_qcrank_tally", sv.C.c_void_p(dense.data_ptr()), m, nd, sv.C.c_void_p(tot.data_ptr()),
+              sv.C.c_void_p(n1.data_ptr()), sv._stream(dense.device))
+    d = dense.cpu().numpy()
+    idx = np.flatnonzero(d)
+    h0, h1, ht = qc._lane_marginals(idx, d[idx], plan)
+    assert np.array_equal(ht, tot.cpu().numpy()) and np.array_equal(h1, n1.cpu().numpy())
+    assert int(tot.sum()) == plan.shots

@@ -47,19 +47,31 @@ def c1():
         sv.N.call("qg_state_init_zero", sv.C.c_void_p(st.amplitudes.data_ptr()), 16, 1, 0, sv._stream(st.amplitudes.device))
         plan.execute(st)
         return sv.sample_indices(st.amplitudes, 3000, 0)
-    ms, _ = timed(step, 20)
+    ms_eager, _ = timed(step, 20)
+    g = sv.CircuitGraph(plan, 3000, 0)  # init + 7 passes + tree sampler as one CUDA graph
+    ms_graph, _ = timed(g.replay, 200)
+    t0 = time.perf_counter()
+    for _ in range(50):
+        g.replay()
+        _, counts = g.result()  # + norm check + counts to the host
+    ms_graph_host = (time.perf_counter() - t0) * 1e3 / 50
+    ms = ms_graph
     t0 = time.perf_counter()
     psi = oracle.run_arrays(gt, gp, 16, gt.shape[0], "fp64")
     oracle.sample_counts_arrays(psi, 3000, 0, "fp64")
     ref_ms = (time.perf_counter() - t0) * 1e3
     return {"config": "c1 random 16q x 100 blocks c128 + 3000 shots", "ms": ms, "gates_per_s": 300 / ms * 1e3,
+            "ms_eager_streams": ms_eager, "ms_graph_replay": ms_graph, "ms_graph_with_counts_to_host": ms_graph_host,
             "passes": plan.info["n_passes"], "cpu_ref_ms": ref_ms, "cpu_ref": "oracle port, full config, 1 core"}
 
 
 def c2():
     n = 28
     gt, gp = qft_arrays(n)
-    plan = sv.CompiledCircuit(gt, gp, n, "fp32")
+    t0 = time.perf_counter()
+    plan = sv.CompiledCircuit(gt, gp, n, "fp32", jit=1)
+    js = plan.jit_status(wait=True)
+    plan_ms = (time.perf_counter() - t0) * 1e3
     st = sv.init_zero_state(n, "fp32")
 
     def gates():
@@ -76,7 +88,9 @@ def c2():
     dt = time.perf_counter() - t0
     ref_gates_per_s = gs.shape[0] / dt / 2 ** (n - 22)
     S = (1 << n) * 8
+    ms_t, _ = timed(lambda: sv.sample_indices(st.amplitudes, 100000, 0, sampler="tree"), 5)
     return {"config": "c2 QFT 28q c64 + 1e5 shots", "gate_ms": ms, "sample_ms": ms_s, "gates": int(gt.shape[0]),
+            "sample_ms_tree": ms_t, "plan_plus_jit_ms": plan_ms, "jit": js,
             "gates_per_s": gt.shape[0] / ms * 1e3, "passes": plan.info["n_passes"],
             "hbm_gbs": 2 * S * plan.info["n_passes"] / ms / 1e6, "max_abs_err_vs_uniform": err,
             "cpu_ref_gates_per_s": ref_gates_per_s,
