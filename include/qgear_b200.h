@@ -184,6 +184,13 @@ int qg_apply_ucry(void* state, int32_t n_local, int32_t dtype, const int32_t* ad
                   const int32_t* targets, int32_t n_targets, const double* alpha_dev, void* workspace,
                   int64_t workspace_bytes, void* stream);
 
+/* qg_sample (Philox uniforms) without any host synchronisation (CUDA-graph
+ * capturable): the norm is written to norm_sq_dev instead of being checked, the
+ * number of unique outcomes to n_unique_dev; the caller checks the norm after the
+ * stream has run (statevec.CircuitGraph.result). */
+int qg_sample_async(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, uint64_t seed,
+                    void* workspace, int64_t workspace_bytes, int64_t* out_index_dev, int64_t* out_count_dev,
+                    int64_t* n_unique_dev, double* norm_sq_dev, void* stream);
 /* QCrank decode tallies from dense per-outcome counts
  * (qg_sample_tree_draw mode 1) of an m-address + n_data-data-qubit state
  * (outcome = address + 2^m * data bits): tot_dev[a] = shots at address a,

@@ -78,6 +78,8 @@ _SIGS = {
     "qg_sample_workspace_bytes": (C.c_int64, [C.c_int64, C.c_int64]),
     "qg_sample": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int64, C.c_uint64, _P, C.c_double, _P, C.c_int64,
                             _P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_double), _P]),
+    "qg_sample_async": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int64, C.c_uint64, _P, C.c_int64, _P, _P, _P, _P,
+                                  _P]),
     "qg_qcrank_tally": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P]),
     "qg_sample_tree_workspace_bytes": (C.c_int64, [C.c_int64]),
     "qg_sample_tree_prepare": (C.c_int, [_P, C.c_int64, C.c_int32, _P, C.c_int64, C.POINTER(C.c_double), _P]),

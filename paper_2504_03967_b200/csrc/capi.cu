@@ -526,6 +526,26 @@ int qg_qcrank_tally(const int64_t* dense_counts, int32_t m, int32_t n_data, int6
     return QG_OK;
 }
 
+int qg_sample_async(const void* state, int64_t n_amps, int32_t dtype, int64_t shots, uint64_t seed,
+                    void* workspace, int64_t workspace_bytes, int64_t* out_index_dev, int64_t* out_count_dev,
+                    int64_t* n_unique_dev, double* norm_sq_dev, void* stream) {
+    DeviceGuard dg_(state);
+    if (int rc = check_dtype(dtype)) return rc;
+    if (shots < 1 || shots > (int64_t)INT32_MAX) return fail(QG_E_INVALID_ARG, "shots must be in [1, 2^31)");
+    if (!state || !workspace || !out_index_dev || !out_count_dev || !n_unique_dev || !norm_sq_dev || n_amps < 1 ||
+        (n_amps & (n_amps - 1)))
+        return fail(QG_E_INVALID_ARG, "bad sampler arguments");
+    if (workspace_bytes < qg::sample_workspace_bytes(n_amps, shots)) return fail(QG_E_INVALID_ARG, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    QG_CUDA(qg::sample_prefix(state, n_amps, dtype, workspace, st, nullptr), "sample prefix");
+    QG_CUDA(cudaMemcpyAsync(norm_sq_dev, qg::sample_total_ptr(workspace, n_amps), sizeof(double),
+                            cudaMemcpyDeviceToDevice, st), "norm copy");
+    QG_CUDA(qg::sample_draw(state, n_amps, dtype, shots, seed, nullptr, workspace, out_index_dev, out_count_dev, st,
+                            n_unique_dev),
+            "sample draw");
+    return QG_OK;
+}
+
 // ---- tree (binomial-split) sampler --------------------------------------------
 int64_t qg_sample_tree_workspace_bytes(int64_t n_amps) {
     if (n_amps < 1 || (n_amps & (n_amps - 1))) return -1;

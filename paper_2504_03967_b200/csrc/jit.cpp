@@ -186,10 +186,13 @@ struct Gen {
 
     // ---------------------------------------------------------------- ops
     // rotation as three in-place shears on pairs {i, i ^ V}, x = parity(W & i) = 0 member
+    // slot filter (variant 4194304): emit only slots with (slot & fmask) == fval
+    uint32_t fmask = 0, fval = 0;
+    bool in_sub(int i) const { return ((uint32_t)i & fmask) == fval; }
     void p_rot(uint32_t V, uint32_t W, const std::string& sa2, const std::string& sb2) {
         for (int pass = 0; pass < 3; ++pass)
             for (int i = 0; i < R; ++i) {
-                if (par(W & (uint32_t)i)) continue;
+                if (par(W & (uint32_t)i) || !in_sub(i)) continue;
                 const int j = i ^ (int)V;
                 if (pass == 1) L("fma.rn.f32x2 ", a(j), ", ", a(i), ", ", sb2, ", ", a(j), ";");
                 else L("fma.rn.f32x2 ", a(i), ", ", a(j), ", ", sa2, ", ", a(i), ";");
@@ -226,7 +229,7 @@ struct Gen {
         std::string c00r = bc(c[0]), c00i = bc(c[1]), c01r = bc(c[2]), c01i = bc(c[3]);
         std::string c10r = bc(c[4]), c10i = bc(c[5]), c11r = bc(c[6]), c11i = bc(c[7]);
         for (int i = 0; i < R; ++i) {
-            if (par(W & (uint32_t)i)) continue;
+            if (par(W & (uint32_t)i) || !in_sub(i)) continue;
             const int j = i ^ (int)V;
             std::string ty = q(), tx = q();
             c_mul(ty, a(j), c01r, c01i);
@@ -238,7 +241,7 @@ struct Gen {
     // multiply slots with parity(W & i) == P by e (packed)
     void p_phase(uint32_t W, int Pp, const std::string& er2, const std::string& ei2) {
         for (int i = 0; i < R; ++i)
-            if (par(W & (uint32_t)i) == Pp) c_mul(a(i), a(i), er2, ei2);
+            if (par(W & (uint32_t)i) == Pp && in_sub(i)) c_mul(a(i), a(i), er2, ei2);
     }
     void op_ph(uint32_t W, const std::string& e) {
         auto [er2, ei2] = split_bc(e);
@@ -263,6 +266,7 @@ struct Gen {
             L("selp.f32 ", d1y, ", 0f00000000, ", ey, ", ", fp, ";");
             std::string d0r = bc(d0x), d0i = bc(d0y), d1r = bc(d1x), d1i = bc(d1y);
             for (int i = 0; i < R; ++i) {
+                if (!in_sub(i)) continue;
                 if (par(W & (uint32_t)i)) c_mul(a(i), a(i), d1r, d1i);
                 else c_mul(a(i), a(i), d0r, d0i);
             }
@@ -306,7 +310,7 @@ struct Gen {
         std::string er2 = bc(ex), ei2 = bc(ey);
         auto cphase = [&]() {
             for (int i = 0; i < R; ++i)
-                if (((i >> T) & 1) && ((i >> C) & 1)) c_mul(a(i), a(i), er2, ei2);
+                if (((i >> T) & 1) && ((i >> C) & 1) && in_sub(i)) c_mul(a(i), a(i), er2, ei2);
         };
         if (!(fposs & ((1u << T) | (1u << C)))) {
             cphase();
@@ -337,6 +341,7 @@ struct Gen {
                 vi[combo] = bc(y);
             }
             for (int i = 0; i < R; ++i) {
+                if (!in_sub(i)) continue;
                 const int combo = ((i >> T) & 1) | (((i >> C) & 1) << 1);
                 c_mul(a(i), a(i), vr[combo], vi[combo]);
             }
@@ -647,6 +652,118 @@ struct Gen {
     int load_map = 0;
     int stagger_ns = 4000;
     uint64_t cmask_ = 0;
+
+    // global stores of the tile through mapping si (register CX map and flips folded in)
+    void store_stg(int si) {
+        const StageDesc& S = P.stg[si];
+        std::string g = gb_of(si);
+        uint64_t lm = thread_gmask(si);
+        std::string idx = g;
+        if (fposs) {
+            idx = q();
+            L("mov.b64 ", idx, ", ", g, ";");
+            for (int b = 0; b < RB; ++b) {
+                if (!(fposs & (1u << b))) continue;
+                std::string t = r(), t64 = q();
+                L("bfe.u32 ", t, ", %F, ", b, ", 1;");
+                L("cvt.u64.u32 ", t64, ", ", t, ";");
+                L("neg.s64 ", t64, ", ", t64, ";");
+                L("and.b64 ", t64, ", ", t64, ", ", u64s(S.out_g[b]), ";");
+                L("xor.b64 ", idx, ", ", idx, ", ", t64, ";");
+                lm |= S.out_g[b];
+            }
+        }
+        std::map<uint64_t, std::pair<std::string, Bases>> bases;
+        std::vector<std::pair<uint64_t, int>> order;  // variant 2097152: stores in ascending address
+        for (int i = 0; i < R; ++i) {
+            uint64_t og = 0;
+            for (int b = 0; b < RB; ++b)
+                if (i & (1 << b)) og ^= S.out_g[b];
+            order.push_back({og, i});
+        }
+        if (variant & 2097152) std::sort(order.begin(), order.end());
+        for (const auto& oi : order) {
+            const int i = oi.second;
+            if (!in_sub(i)) continue;
+            const uint64_t og = oi.first;
+            const uint64_t lo = og & lm, hi = og & ~lm;
+            auto it = bases.find(lo);
+            if (it == bases.end()) {
+                std::string x = q();
+                if (lo) L("xor.b64 ", x, ", ", idx, ", ", u64s(lo), ";");
+                else L("mov.b64 ", x, ", ", idx, ";");
+                L("shl.b64 ", x, ", ", x, ", 3;");
+                if (variant & 1048576) {  // timing probe: stores into a 16 MiB L2-resident window
+                    std::string y = q();
+                    L("add.s64 ", y, ", ", x, ", %pt;");
+                    L("sub.s64 ", y, ", ", y, ", %psi;");
+                    L("and.b64 ", y, ", ", y, ", 0xffffff;");
+                    L("add.s64 ", x, ", ", y, ", %psi;");
+                } else {
+                    L("add.s64 ", x, ", ", x, ", %pt;");
+                }
+                it = bases.emplace(lo, std::make_pair(x, Bases{})).first;
+            }
+            L((variant & 65536) ? "st.global.b64 " : "st.global.cs.b64 ",
+              addr64(it->second.second, it->second.first, hi * 8), ", ", a(i), ";");
+        }
+    }
+    bool stored = false;
+
+    // the op list and thread phases of stage s (slot filter applies)
+    template <class TBF>
+    bool stage_body(int s, TBF& TB) {
+        const StageDesc& S = P.stg[s];
+        for (int oi = S.op_begin;; ++oi) {
+            const uint32_t w = P.ops[oi];
+            const uint32_t code = w & 0xffu;
+            if (code >= dec.size() || dec[code].fam < 0) return false;
+            if ((variant & 8) && dec[code].fam != 9) continue;  // timing probe: no ops (wrong results)
+            const Dec d = dec[code];
+            if (d.fam == 9) break;
+            const uint32_t T = d.t >= 0 ? 1u << d.t : 0u, Cb = d.c >= 0 ? 1u << d.c : 0u;
+            switch (d.fam) {
+                case F_RD: op_rd(T, T, w >> 16); break;
+                case F_CD: op_cd(T, T, w >> 16); break;
+                case F_PH: op_ph(T, ph_product(w, TB())); break;
+                case F_RDW: op_rd(T, T | Cb, w >> 16); break;
+                case F_RDV: op_rd(T | Cb, T, w >> 16); break;
+                case F_PHW: op_ph(T | Cb, ph_product(w, TB())); break;
+                case F_PH2: op_ph2(d.t, d.c, w >> 16); break;
+                case 7: op_cxm(d.t, d.c); break;
+                case 8: op_xf(w, TB()); break;
+                default: return false;
+            }
+        }
+        if (S.tph_end > S.tph_begin && !(variant & 8)) {
+            std::string one = f(), zero = f();
+            L("mov.f32 ", one, ", 0f3F800000;");
+            L("mov.f32 ", zero, ", 0f00000000;");
+            std::string ph = pack(one, zero);
+            const std::string& t = TB();
+            for (int e = S.tph_begin; e < S.tph_end; ++e) {
+                const Entry<float>& E = P.tph[e];
+                std::string pc = p(), ph_ = p(), m1 = q(), m2 = q();
+                L("and.b64 ", m1, ", ", t, ", ", u64s(E.cmask), ";");
+                L("setp.eq.u64 ", pc, ", ", m1, ", ", u64s(E.cmask), ";");
+                L("and.b64 ", m2, ", ", t, ", ", u64s(E.qmask), ";");
+                L("setp.ne.u64 ", ph_, ", ", m2, ", 0;");
+                const size_t vo = off_tph + 32 * (size_t)e + 16;
+                std::string v0 = ldp_f32(vo), v1 = ldp_f32(vo + 4), v2 = ldp_f32(vo + 8), v3 = ldp_f32(vo + 12);
+                std::string vx = f(), vy = f(), np_ = q();
+                L("selp.f32 ", vx, ", ", v2, ", ", v0, ", ", ph_, ";");
+                L("selp.f32 ", vy, ", ", v3, ", ", v1, ", ", ph_, ";");
+                c_mul(np_, ph, bc(vx), bc(vy));
+                std::string nph = q();
+                L("selp.b64 ", nph, ", ", np_, ", ", ph, ", ", pc, ";");
+                ph = nph;
+            }
+            auto [r2, i2] = split_bc(ph);
+            for (int i = 0; i < R; ++i)
+                if (in_sub(i)) c_mul(a(i), a(i), r2, i2);
+        }
+        return true;
+    }
 
     // ---------------------------------------------------------------- prologue pieces
     // deposit the low bits of u32 x into the positions comp_q[0..n) (u64 result)
@@ -1007,52 +1124,52 @@ struct Gen {
                 if (tb.empty()) tb = tb_of(s);
                 return tb;
             };
-            for (int oi = S.op_begin;; ++oi) {
-                const uint32_t w = P.ops[oi];
-                const uint32_t code = w & 0xffu;
-                if (code >= dec.size() || dec[code].fam < 0) return "";
-                if ((variant & 8) && dec[code].fam != 9) continue;  // timing probe: no ops (wrong results)
-                const Dec d = dec[code];
-                if (d.fam == 9) break;
-                const uint32_t T = d.t >= 0 ? 1u << d.t : 0u, Cb = d.c >= 0 ? 1u << d.c : 0u;
-                switch (d.fam) {
-                    case F_RD: op_rd(T, T, w >> 16); break;
-                    case F_CD: op_cd(T, T, w >> 16); break;
-                    case F_PH: op_ph(T, ph_product(w, TB())); break;
-                    case F_RDW: op_rd(T, T | Cb, w >> 16); break;
-                    case F_RDV: op_rd(T | Cb, T, w >> 16); break;
-                    case F_PHW: op_ph(T | Cb, ph_product(w, TB())); break;
-                    case F_PH2: op_ph2(d.t, d.c, w >> 16); break;
-                    case 7: op_cxm(d.t, d.c); break;
-                    case 8: op_xf(w, TB()); break;
-                    default: return "";
+            const bool split = (variant & 4194304) && s == ns && si == ns && !(variant & (8 | 16 | 32 | 16384 | 262144));
+            uint32_t spect = 0;  // register bits no pair op / register move of this stage couples
+            if (split) {
+                uint32_t touched = 0;
+                for (int oi = S.op_begin;; ++oi) {
+                    const uint32_t code = P.ops[oi] & 0xffu;
+                    if (code >= dec.size() || dec[code].fam < 0) return "";
+                    const Dec d = dec[code];
+                    if (d.fam == 9) break;
+                    const uint32_t T = d.t >= 0 ? 1u << d.t : 0u, Cb = d.c >= 0 ? 1u << d.c : 0u;
+                    if (d.fam == F_RD || d.fam == F_CD || d.fam == F_RDW) touched |= T;
+                    if (d.fam == F_RDV) touched |= T | Cb;
+                    if (d.fam == 7) touched |= T | Cb;
                 }
+                for (int b = RB - 1; b >= 0 && __builtin_popcount(spect) < 2; --b)
+                    if (!(touched & (1u << b))) spect |= 1u << b;
             }
-            if (S.tph_end > S.tph_begin && !(variant & 8)) {
-                std::string one = f(), zero = f();
-                L("mov.f32 ", one, ", 0f3F800000;");
-                L("mov.f32 ", zero, ", 0f00000000;");
-                std::string ph = pack(one, zero);
-                const std::string& t = TB();
-                for (int e = S.tph_begin; e < S.tph_end; ++e) {
-                    const Entry<float>& E = P.tph[e];
-                    std::string pc = p(), ph_ = p(), m1 = q(), m2 = q();
-                    L("and.b64 ", m1, ", ", t, ", ", u64s(E.cmask), ";");
-                    L("setp.eq.u64 ", pc, ", ", m1, ", ", u64s(E.cmask), ";");
-                    L("and.b64 ", m2, ", ", t, ", ", u64s(E.qmask), ";");
-                    L("setp.ne.u64 ", ph_, ", ", m2, ", 0;");
-                    const size_t vo = off_tph + 32 * (size_t)e + 16;
-                    std::string v0 = ldp_f32(vo), v1 = ldp_f32(vo + 4), v2 = ldp_f32(vo + 8), v3 = ldp_f32(vo + 12);
-                    std::string vx = f(), vy = f(), np_ = q();
-                    L("selp.f32 ", vx, ", ", v2, ", ", v0, ", ", ph_, ";");
-                    L("selp.f32 ", vy, ", ", v3, ", ", v1, ", ", ph_, ";");
-                    c_mul(np_, ph, bc(vx), bc(vy));
-                    std::string nph = q();
-                    L("selp.b64 ", nph, ", ", np_, ", ", ph, ", ", pc, ";");
-                    ph = nph;
+            if (!spect) {
+                if (!stage_body(s, TB)) return "";
+            } else {
+                // the last stage in independent slot subsets (fixed spectator bits), each
+                // stored as soon as it is final: the STG burst interleaves with the compute
+                // of the next subset.  Register renames, the flip vector and its static
+                // knowledge restart from the same state for every subset.
+                std::string F0 = r();
+                L("mov.u32 ", F0, ", %F;");
+                int amap0[64];
+                std::copy(amap, amap + R, amap0);
+                const uint32_t fposs0 = fposs;
+                const int nsub = 1 << __builtin_popcount(spect);
+                for (int k2 = 0; k2 < nsub; ++k2) {
+                    uint32_t v = 0;
+                    for (int b = 0, t = 0; b < RB; ++b)
+                        if (spect & (1u << b)) v |= (uint32_t)((k2 >> t++) & 1) << b;
+                    fmask = spect;
+                    fval = v;
+                    if (k2) {
+                        L("mov.u32 %F, ", F0, ";");
+                        std::copy(amap0, amap0 + R, amap);
+                        fposs = fposs0;
+                    }
+                    if (!stage_body(s, TB)) return "";
+                    store_stg(si);
                 }
-                auto [r2, i2] = split_bc(ph);
-                for (int i = 0; i < R; ++i) c_mul(a(i), a(i), r2, i2);
+                fmask = fval = 0;
+                stored = true;
             }
         }
         if (cur != si && !(variant & 16)) {
@@ -1061,59 +1178,10 @@ struct Gen {
         }
         if ((variant & 262144) && !(variant & (32 | 16384))) {
             tma_store(si);
-        } else if (!(variant & (32 | 16384))) {  // store through the output mapping (register CX map and flips folded in)
-            const StageDesc& S = P.stg[si];
-            std::string g = gb_of(si);
-            uint64_t lm = thread_gmask(si);
-            std::string idx = g;
-            if (fposs) {
-                idx = q();
-                L("mov.b64 ", idx, ", ", g, ";");
-                for (int b = 0; b < RB; ++b) {
-                    if (!(fposs & (1u << b))) continue;
-                    std::string t = r(), t64 = q();
-                    L("bfe.u32 ", t, ", %F, ", b, ", 1;");
-                    L("cvt.u64.u32 ", t64, ", ", t, ";");
-                    L("neg.s64 ", t64, ", ", t64, ";");
-                    L("and.b64 ", t64, ", ", t64, ", ", u64s(S.out_g[b]), ";");
-                    L("xor.b64 ", idx, ", ", idx, ", ", t64, ";");
-                    lm |= S.out_g[b];
-                }
-            }
-            std::map<uint64_t, std::pair<std::string, Bases>> bases;
-            std::vector<std::pair<uint64_t, int>> order;  // variant 2097152: stores in ascending address
-            for (int i = 0; i < R; ++i) {
-                uint64_t og = 0;
-                for (int b = 0; b < RB; ++b)
-                    if (i & (1 << b)) og ^= S.out_g[b];
-                order.push_back({og, i});
-            }
-            if (variant & 2097152) std::sort(order.begin(), order.end());
-            for (const auto& oi : order) {
-                const int i = oi.second;
-                const uint64_t og = oi.first;
-                const uint64_t lo = og & lm, hi = og & ~lm;
-                auto it = bases.find(lo);
-                if (it == bases.end()) {
-                    std::string x = q();
-                    if (lo) L("xor.b64 ", x, ", ", idx, ", ", u64s(lo), ";");
-                    else L("mov.b64 ", x, ", ", idx, ";");
-                    L("shl.b64 ", x, ", ", x, ", 3;");
-                    if (variant & 1048576) {  // timing probe: stores into a 16 MiB L2-resident window
-                        std::string y = q();
-                        L("add.s64 ", y, ", ", x, ", %pt;");
-                        L("sub.s64 ", y, ", ", y, ", %psi;");
-                        L("and.b64 ", y, ", ", y, ", 0xffffff;");
-                        L("add.s64 ", x, ", ", y, ", %psi;");
-                    } else {
-                        L("add.s64 ", x, ", ", x, ", %pt;");
-                    }
-                    it = bases.emplace(lo, std::make_pair(x, Bases{})).first;
-                }
-                L((variant & 65536) ? "st.global.b64 " : "st.global.cs.b64 ",
-                  addr64(it->second.second, it->second.first, hi * 8), ", ", a(i), ";");
-            }
+        } else if (!(variant & (32 | 16384)) && !stored) {
+            store_stg(si);
         }
+        stored = false;
         L("mov.u64 %tile, %ntile;");
         L("mov.u64 %base, %nbase;");
         L("bra.uni $LOOP;");

@@ -303,6 +303,10 @@ static int swz(int dtype, int j) {  // linear XOR swizzle of a tile index (ampli
 }
 
 // register/lane/warp tile bits of one stage
+// lanes pinned to the lowest tile bits in a coalesced (global load / store) mapping:
+// 4 = whole 128 B lines per warp access (QG_DEV_IOL: dev override; round 1 used 5)
+static const int kIoLanes = std::getenv("QG_DEV_IOL") ? std::atoi(std::getenv("QG_DEV_IOL")) : 4;
+
 static void assign_mapping(int dtype, const KernelCfg& cfg, const std::vector<int>& reg_bits_needed, bool io_lanes,
                            HostStage& hs) {
     const int k = cfg.k();
@@ -310,7 +314,11 @@ static void assign_mapping(int dtype, const KernelCfg& cfg, const std::vector<in
     hs.reg_tile.clear(); hs.lane_tile.clear(); hs.warp_tile.clear();
     for (int b : reg_bits_needed) { hs.reg_tile.push_back(b); used[b] = 1; }
     if (io_lanes) {
-        for (int l = 0; l < kLaneBits; ++l) { hs.lane_tile.push_back(l); used[l] = 1; }
+        // coalesced: lanes 0..3 on tile bits 0..3 (every warp access is whole 128 B
+        // lines of >= 256 B HBM runs), the fifth lane on the lowest free tile bit
+        for (int l = 0; l < kIoLanes; ++l) { hs.lane_tile.push_back(l); used[l] = 1; }
+        for (int b = kIoLanes; b < k && (int)hs.lane_tile.size() < kLaneBits; ++b)
+            if (!used[b]) { hs.lane_tile.push_back(b); used[b] = 1; }
         for (int b = kLaneBits; b < k && (int)hs.reg_tile.size() < cfg.rb; ++b)
             if (!used[b]) { hs.reg_tile.push_back(b); used[b] = 1; }
     } else {
@@ -339,7 +347,7 @@ static void assign_mapping(int dtype, const KernelCfg& cfg, const std::vector<in
 }
 
 static bool disjoint_low5(const std::vector<int>& bits) {
-    for (int b : bits) if (b < kLaneBits) return false;
+    for (int b : bits) if (b < kIoLanes) return false;
     return true;
 }
 
@@ -736,7 +744,7 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
     hp.gph_re = gphase.real();
     hp.gph_im = gphase.imag();
     auto is_io = [](const HostStage& h) {
-        for (int l = 0; l < kLaneBits; ++l) if (h.lane_tile[l] != l) return false;
+        for (int l = 0; l < kIoLanes; ++l) if (h.lane_tile[l] != l) return false;
         return true;
     };
     hp.load_direct = is_io(hp.stages[0]);

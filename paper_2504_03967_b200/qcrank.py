@@ -452,9 +452,36 @@ def sample_decode(state: sv.StateVector, plan: QCrankPlan, rng_seed: int = 0, so
     N.call("qg_qcrank_tally", C.c_void_p(dense.data_ptr()), m, nd, C.c_void_p(tot.data_ptr()),
            C.c_void_p(n1.data_ptr()), sv._stream(dev))
     del dense
-    tot_h = tot.double().cpu().numpy()
-    n1_h = n1.double().cpu().numpy()
-    return _reconstruct(tot_h[:, None] - n1_h, n1_h, tot_h, plan, source)
+    return _reconstruct_device(tot, n1, plan, source)
+
+
+def _reconstruct_device(tot: torch.Tensor, n1: torch.Tensor, plan: QCrankPlan, source: ImageGray | None):
+    """_reconstruct on the device (2^27 pixels at m = 24: the numpy version takes
+    ~20 s on the host); same estimator, same outputs."""
+    m, nd = plan.n_addr, plan.n_data
+    dev = tot.device
+    t = tot.to(torch.float64)[:, None]
+    v = torch.where(t > 0, (t - 2.0 * n1.to(torch.float64)) / torch.clamp(t, min=1.0), torch.zeros_like(t))
+    v = v.clamp(-1.0, 1.0)
+    empty = torch.nonzero(tot == 0).flatten().cpu().tolist()
+    n_px = plan.width * plan.height if plan.width else plan.padded_len
+    k = torch.arange(n_px, dtype=torch.int64, device=dev)
+    g = k // nd
+    a = torch.zeros_like(g)
+    for b in range(m):
+        a |= ((g >> b) & 1) << (m - 1 - b)
+    est = v[a, k % nd]
+    px = torch.clamp(torch.round(255.0 * (est + 1.0) / 2.0), 0, 255).to(torch.uint8)
+    rep = ReconstructionReport(estimates=est.cpu().numpy(), empty_addresses=empty)
+    if source is not None:
+        truth = 2.0 * torch.from_numpy(np.asarray(source.pixels)).to(dev, torch.float64) / 255.0 - 1.0
+        err = est - truth
+        rep.mse = float((err * err).mean())
+        rep.max_abs_error = float(err.abs().max())
+        if float(truth.std()) > 0 and float(est.std()) > 0:
+            rep.correlation = float(torch.corrcoef(torch.stack([est, truth]))[0, 1])
+    img = ImageGray(plan.width, plan.height, px.cpu().numpy()) if plan.width else None
+    return rep, img
 
 
 def decode_exact(probabilities, plan: QCrankPlan, source: ImageGray | None = None):

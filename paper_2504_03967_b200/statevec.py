@@ -481,8 +481,9 @@ class TreeSampler:
 
 class CircuitGraph:
     """One planned circuit captured as a CUDA graph: |0..0> init, every fused pass
-    and (shots > 0) the tree sampler.  replay() is one graph launch with no host
-    synchronisation; result() reads the norm and the outcome count back (one
+    and (shots > 0) the sampler (per-shot Philox up to 2^24 shots, else the tree).
+    replay() is one graph launch with no host synchronisation; result() reads the
+    norm and the outcome count back (one
     sync) and checks the norm like sample_counts (statevec.py:226-228).  For
     small, launch-bound circuits run many times (BASELINE configs[0]: 16 q,
     300 gates, complex128, 3000 shots)."""
@@ -495,11 +496,17 @@ class CircuitGraph:
         self.state = init_zero_state(n, prec, 1 << 62, device)
         amps = self.state.amplitudes
         dev = amps.device
-        self.ts = TreeSampler(amps) if shots > 0 else None
-        cap = max(1, min(self.shots, 1 << n))
+        # per-shot Philox sampler (fewest graph nodes) up to 2^24 shots, the tree sampler above
+        self.per_shot = 0 < self.shots <= (1 << 24)
+        self.ts = TreeSampler(amps) if shots > 0 and not self.per_shot else None
+        cap = max(1, self.shots if self.per_shot else min(self.shots, 1 << n))
         self.idx = torch.empty(cap, dtype=torch.int64, device=dev)
         self.cnt = torch.empty(cap, dtype=torch.int64, device=dev)
         self.nout = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.norm = torch.zeros(1, dtype=torch.float64, device=dev)
+        if self.per_shot:
+            self.ws = torch.empty(max(N.lib().qg_sample_workspace_bytes(1 << n, self.shots), 256), dtype=torch.uint8,
+                                  device=dev)
         side = torch.cuda.Stream(dev)  # warm-up off the capture: JIT libraries load, CUB settles
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
@@ -515,7 +522,13 @@ class CircuitGraph:
         N.call("qg_state_init_zero", C.c_void_p(amps.data_ptr()), self.plan.n_qubits,
                _QG_DTYPE[self.plan.precision], 0, _stream(amps.device))
         self.plan.execute(self.state)
-        if self.ts is not None:
+        if self.per_shot:
+            N.call("qg_sample_async", C.c_void_p(amps.data_ptr()), 1 << self.plan.n_qubits,
+                   _QG_DTYPE[self.plan.precision], self.shots, C.c_uint64(self.seed & (2**64 - 1)),
+                   C.c_void_p(self.ws.data_ptr()), self.ws.numel(), C.c_void_p(self.idx.data_ptr()),
+                   C.c_void_p(self.cnt.data_ptr()), C.c_void_p(self.nout.data_ptr()), C.c_void_p(self.norm.data_ptr()),
+                   _stream(amps.device))
+        elif self.ts is not None:
             self.ts.prepare_async()
             self.ts.draw_into(self.shots, self.seed, 2, self.idx, self.cnt, self.nout)
 
@@ -525,8 +538,8 @@ class CircuitGraph:
     def result(self):
         """(StateVector, CountsTable | None) of the last replay."""
         counts = None
-        if self.ts is not None:
-            m = float(self.ts.mass_device().item())
+        if self.shots > 0:
+            m = float((self.norm if self.per_shot else self.ts.mass_device()).item())
             if not abs(m - 1.0) <= NORM_TOL[self.plan.precision]:
                 raise UnnormalizedStateError(f"norm^2 = {m!r} outside tolerance")
             k = int(self.nout.item())

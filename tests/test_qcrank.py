@@ -229,3 +229,7 @@ def test_sample_decode_dense_tally_matches_counts():
     h0, h1, ht = qc._lane_marginals(idx, d[idx], plan)
     assert np.array_equal(ht, tot.cpu().numpy()) and np.array_equal(h1, n1.cpu().numpy())
     assert int(tot.sum()) == plan.shots
+    rep_h, img_h = qc._reconstruct(h0, h1, ht, plan, img)
+    rep_d, img_d = qc._reconstruct_device(tot, n1, plan, img)
+    assert np.array_equal(img_h.pixels, img_d.pixels) and np.allclose(rep_h.estimates, rep_d.estimates, atol=1e-15)
+    assert abs(rep_h.mse - rep_d.mse) <= 1e-12 and rep_h.empty_addresses == rep_d.empty_addresses
