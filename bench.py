@@ -346,7 +346,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if not args.no_e2e:
         opts = sv.SimOptions(precision=prec, shots=args.e2e_shots, rng_seed=args.seed, memory_budget=1 << 45,
                              device=local_rank, tile_qubits=args.tile_qubits, max_stages=args.max_stages,
-                             max_cost=args.max_cost, sampler="tree")
+                             max_cost=args.max_cost)
         circ = generate_random_gate_list(RandomSpec(n, args.blocks, args.seed))
         del shard
         torch.cuda.empty_cache()
@@ -378,7 +378,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                "shots": args.e2e_shots,
                "note": ("host gate records -> plan + JIT (cubin cache warm after one warm-up call) -> kernels "
-                        "-> tree sampler; (index, count) pairs of the shots read back to the host; the state "
+                        "-> sampler (Philox, per shot); (index, count) pairs of the shots read back to the host; the state "
                         "stays in HBM")}
 
     if rank != 0:

@@ -589,6 +589,7 @@ struct Gen {
         o << ls << ":\n";
     }
     uint32_t tlin_mask = 0;
+    bool gen_pf = false;  // generic L2 prefetch (thread t -> 256 B chunk t of the next tile)
 
     // tile load (mapping m) from the tile at byte pointer `ptr` into registers <bank>0..R-1
     void reg_load(int m, const std::string& ptr, const std::string& bank) {
@@ -892,6 +893,18 @@ struct Gen {
             L("@%pl0 st.shared.u64 [%tw8+", pf + 256, "], ", gw, ";");
         }
         L("setp.lt.u32 %pfl, ", lane, ", ", R, ";");
+        gen_pf = run_bits() >= 5 && (1 << (k - 5)) == NT;
+        if (gen_pf) {  // thread t prefetches 256 B chunk t of the next tile (whatever the mappings)
+            L("mov.u64 %pfg, 0;");
+            for (int i = 0; i < k - 5; ++i) {
+                std::string t = r(), t64 = q();
+                L("bfe.u32 ", t, ", %xtid, ", i, ", 1;");
+                L("cvt.u64.u32 ", t64, ", ", t, ";");
+                L("shl.b64 ", t64, ", ", t64, ", ", (int)P.tile_q[5 + i], ";");
+                L("or.b64 %pfg, %pfg, ", t64, ";");
+            }
+            L("setp.eq.u32 %pfl, 1, 1;");
+        }
         if (variant & 262144) {
             const StageDesc& S = P.stg[si];
             L("mov.u32 %tlin, 0;");
@@ -1035,7 +1048,9 @@ struct Gen {
             }
             std::string ls = lab();
             L("@!", pp, " bra.uni ", ls, ";");
-            {
+            if (gen_pf) {
+                L("mov.b64 ", pf, ", %pfg;");
+            } else {
                 const size_t pfo = tab_pf - tab_gb;
                 std::string a1 = q(), a2 = q();
                 L("ld.shared.u64 ", a1, ", [%tl8+", pfo, "];");
@@ -1204,7 +1219,7 @@ struct Gen {
         h << "\t.reg .f32 %f<" << (nf + 1) << ">;\n";
         h << "\t.reg .pred %p<" << (np + 1) << ">;\n";
         h << "\t.reg .b32 %xtid, %xlane, %xwarp, %smb, %smb2, %tlin, %tl8, %tw8, %tl4, %tw4, %F, %ctile, %nctile;\n";
-        h << "\t.reg .b64 %rdl;\n";
+        h << "\t.reg .b64 %rdl, %pfg;\n";
         h << "\t.reg .b64 %gbm<" << (P.n_stages + 1) << ">;\n\t.reg .b32 %som<" << (P.n_stages + 1) << ">;\n";
         h << "\t.reg .b64 %tile, %tend, %ntile, %G, %base, %nbase, %dG, %psi, %rk, %pt;\n";
         h << "\t.reg .pred %pfl, %pend, %pnext, %pw0, %pl0;\n";
@@ -1216,10 +1231,11 @@ struct Gen {
 
 int jit_variant() {
     static const int v = [] {
-        // default: per-thread mapping values in registers (524288); the other bits are
+        // default: per-thread mapping values in registers (524288) and the last stage in
+        // slot subsets with interleaved stores (4194304); the other bits are
         // measurement probes (tools/jit_time.py, profiles/r02*_jit_variants*.jsonl)
         const char* e = std::getenv("QG_JIT_VARIANT");
-        return e ? std::atoi(e) : 524288;
+        return e ? std::atoi(e) : (524288 | 4194304);
     }();
     return v;
 }

@@ -303,9 +303,10 @@ static int swz(int dtype, int j) {  // linear XOR swizzle of a tile index (ampli
 }
 
 // register/lane/warp tile bits of one stage
-// lanes pinned to the lowest tile bits in a coalesced (global load / store) mapping:
-// 4 = whole 128 B lines per warp access (QG_DEV_IOL: dev override; round 1 used 5)
-static const int kIoLanes = std::getenv("QG_DEV_IOL") ? std::atoi(std::getenv("QG_DEV_IOL")) : 4;
+// lanes pinned to the lowest tile bits in a coalesced (global load / store) mapping: 2 =
+// every 32 B sector written / read whole by one warp access (QG_DEV_IOL: dev override;
+// round 1 pinned all 5: 228 -> 202 transposes for the 32 q circuit, HBM time unchanged)
+static const int kIoLanes = std::getenv("QG_DEV_IOL") ? std::atoi(std::getenv("QG_DEV_IOL")) : 2;
 
 static void assign_mapping(int dtype, const KernelCfg& cfg, const std::vector<int>& reg_bits_needed, bool io_lanes,
                            HostStage& hs) {

@@ -596,8 +596,17 @@ def sample_indices(amps: torch.Tensor, shots: int, rng_seed: int = 0, sampler: s
     return idx[:k], cnt[:k]
 
 
+def bitstrings(idx: np.ndarray, n_qubits: int) -> list[str]:
+    """bitstring() of many indices at once (qubit 0 leftmost), vectorised."""
+    idx = np.asarray(idx, dtype=np.int64)
+    if idx.size == 0 or n_qubits == 0:
+        return [""] * idx.size
+    chars = (((idx[:, None] >> np.arange(n_qubits, dtype=np.int64)) & 1).astype(np.uint8) + ord("0"))
+    return np.ascontiguousarray(chars).view(f"S{n_qubits}").ravel().astype(f"U{n_qubits}").tolist()
+
+
 def counts_from_arrays(idx: np.ndarray, cnt: np.ndarray, shots: int, n_qubits: int) -> CountsTable:
-    counts = {bitstring(int(i), n_qubits): int(c) for i, c in zip(idx.tolist(), cnt.tolist())}
+    counts = dict(zip(bitstrings(idx, n_qubits), np.asarray(cnt).tolist()))
     return CountsTable(counts=counts, total=shots, n_qubits=n_qubits, indices=idx, values=cnt)
 
 
