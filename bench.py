@@ -13,7 +13,7 @@ launching stream, max over ranks.  The state (32 GiB) is far larger than L2
 
 e2e = the same circuit through the public API paper_2504_03967_b200.statevec.
 run_circuit (host gate records -> planning -> JIT pass kernels (process-wide
-cubin cache) -> execution -> tree sampler, --e2e-shots shots) with the (index,
+cubin cache) -> execution -> per-shot sampler, --e2e-shots shots) with the (index,
 count) pairs read back to the host.
 
 --impl reference: the reference's own CPU executor from baseline/_ref (its
@@ -353,7 +353,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
         def e2e_step():
             # host gate records in -> plan (+ JIT, cubins from the process-wide cache after the
-            # warm-up call) -> passes (+ remaps) -> tree sampler -> counts on the host
+            # warm-up call) -> passes (+ remaps) -> sampler -> counts on the host
             if world > 1:
                 res = pt.execute_distributed(circ, world, opts, gather=False)
             else:

@@ -1210,7 +1210,8 @@ struct Gen {
         h << ".extern .shared .align 16 .b8 smem[];\n\n";
         h << ".visible .entry " << name << "(\n\t.param .align 8 .b8 P[" << sizeof(PD)
           << "],\n\t.param .u64 psi,\n\t.param .u64 rk\n)\n";
-        const int min_ctas = (WB >= 4 || RB >= 6 || (variant & (2048 | 4096))) ? 1 : ((variant & 2) ? 3 : 2);
+        int min_ctas = (WB >= 4 || RB >= 6 || (variant & (2048 | 4096))) ? 1 : ((variant & 2) ? 3 : 2);
+        if (variant & 8388608) min_ctas = 3;  // probe: three CTAs per SM (register cap 65536 / (3 x threads))
         h << ".maxntid " << NT << ", 1, 1\n.minnctapersm " << min_ctas << "\n{\n";
         h << "\t.reg .b64 %a<" << R << ">;\n";
         if (variant & 4096) h << "\t.reg .b64 %b<" << R << ">;\n";

@@ -193,6 +193,11 @@ struct Blocks {
     }
 };
 
+// lanes pinned to the lowest tile bits in a coalesced (global load / store) mapping: 2 =
+// every 32 B sector written / read whole by one warp access (QG_DEV_IOL: dev override;
+// round 1 pinned all 5: 228 -> 202 transposes for the 32 q circuit, HBM time unchanged)
+static const int kIoLanes = std::getenv("QG_DEV_IOL") ? std::atoi(std::getenv("QG_DEV_IOL")) : 2;
+
 // per-amplitude instruction estimates; `in_reg` = register
 // qubits of the stage being scanned (thread-level phases cost ~nothing per amp)
 static double gate_cost(const Gate& g, const std::vector<char>& in_reg) {
@@ -241,7 +246,7 @@ static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int
                     if (t < n_local) {
                         if (in_reg[t]) ok = true;
                         else if ((int)st.regs.size() < rb && (in_tile[t] || (int)tile.size() < k) &&
-                                 !(restrict_low && t < kLaneBits)) {
+                                 !(restrict_low && t < kIoLanes)) {
                             in_reg[t] = 1;
                             st.regs.push_back(t);
                             if (!in_tile[t]) { in_tile[t] = 1; tile.push_back(t); tile_added.push_back(t); }
@@ -275,7 +280,7 @@ static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int
         StageSched st;
         std::vector<Gate> keep;
         double scost = 0;
-        // stage 0 keeps the 5 lowest (lane) qubits out of registers so the tile
+        // stage 0 keeps the pinned io-lane qubits out of registers so the tile
         // loads straight into the stage mapping; relax if that leaves it empty
         const bool restrict_low = s == 0 && c_low >= kLaneBits;
         scan(s, restrict_low, st, keep, scost);
@@ -303,11 +308,6 @@ static int swz(int dtype, int j) {  // linear XOR swizzle of a tile index (ampli
 }
 
 // register/lane/warp tile bits of one stage
-// lanes pinned to the lowest tile bits in a coalesced (global load / store) mapping: 2 =
-// every 32 B sector written / read whole by one warp access (QG_DEV_IOL: dev override;
-// round 1 pinned all 5: 228 -> 202 transposes for the 32 q circuit, HBM time unchanged)
-static const int kIoLanes = std::getenv("QG_DEV_IOL") ? std::atoi(std::getenv("QG_DEV_IOL")) : 2;
-
 static void assign_mapping(int dtype, const KernelCfg& cfg, const std::vector<int>& reg_bits_needed, bool io_lanes,
                            HostStage& hs) {
     const int k = cfg.k();
