@@ -1257,23 +1257,26 @@ size_t jit_smem_bytes(const PassDesc<float>& P, int rb, int wb, int nbuf) {
 // parameters, bench steps) reuses the cubins instead of recompiling.
 namespace {
 std::mutex g_cache_mu;
-std::unordered_map<std::string, std::shared_ptr<const std::vector<char>>> g_cache;
+// never destroyed: modules would otherwise unload their libraries after the CUDA
+// runtime has shut down at process exit
+auto& g_cache = *new std::unordered_map<std::string, std::shared_ptr<JitModule>>();
 size_t g_cache_bytes = 0;
 constexpr size_t kCacheMaxBytes = (size_t)1 << 30;  // PTX + cubin bytes kept
 
-std::shared_ptr<const std::vector<char>> cache_get(const std::string& ptx) {
+// (a module stays loaded while any plan or the cache holds it; loaded libraries are
+// reused by every later plan with the same pass: no per-plan cudaLibraryLoadData)
+std::shared_ptr<JitModule> cache_get(const std::string& ptx) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(ptx);
     return it == g_cache.end() ? nullptr : it->second;
 }
-void cache_put(const std::string& ptx, const std::vector<char>& cubin) {
+void cache_put(const std::string& ptx, const std::shared_ptr<JitModule>& m) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    if (g_cache_bytes + ptx.size() + cubin.size() > kCacheMaxBytes) {
+    if (g_cache_bytes + ptx.size() + m->cubin.size() > kCacheMaxBytes) {
         g_cache.clear();
         g_cache_bytes = 0;
     }
-    if (g_cache.emplace(ptx, std::make_shared<const std::vector<char>>(cubin)).second)
-        g_cache_bytes += ptx.size() + cubin.size();
+    if (g_cache.emplace(ptx, m).second) g_cache_bytes += ptx.size() + m->cubin.size();
 }
 }  // namespace
 
@@ -1303,7 +1306,7 @@ bool jit_compile(const std::string& ptx, std::vector<char>& cubin, std::string& 
     return true;
 }
 
-JitKernel::~JitKernel() {
+JitModule::~JitModule() {
     for (Dev& d : dev)
         if (d.lib) cudaLibraryUnload(d.lib);
 }
@@ -1312,10 +1315,12 @@ cudaError_t launch_jit(JitKernel& k, const PassDesc<float>& P, void* psi, uint64
     int dv = 0;
     cudaError_t e = cudaGetDevice(&dv);
     if (e != cudaSuccess) return e;
-    if ((int)k.dev.size() <= dv) k.dev.resize(dv + 1);
-    JitKernel::Dev& D = k.dev[dv];
+    JitModule& M = *k.mod;
+    std::unique_lock<std::mutex> lk(M.mu);
+    if ((int)M.dev.size() <= dv) M.dev.resize(dv + 1);
+    JitModule::Dev& D = M.dev[dv];
     if (!D.kern) {
-        e = cudaLibraryLoadData(&D.lib, k.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+        e = cudaLibraryLoadData(&D.lib, M.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
         if (e != cudaSuccess) return e;
         e = cudaLibraryGetKernel(&D.kern, D.lib, k.name.c_str());
         if (e != cudaSuccess) return e;
@@ -1329,8 +1334,10 @@ cudaError_t launch_jit(JitKernel& k, const PassDesc<float>& P, void* psi, uint64
         D.grid = sms * (occ > 0 ? occ : 1);
     }
     const uint64_t grid = P.n_tiles < (uint64_t)D.grid ? P.n_tiles : (uint64_t)D.grid;
+    const cudaKernel_t kern = D.kern;
+    lk.unlock();
     void* args[] = {const_cast<PassDesc<float>*>(&P), &psi, &rank_bits};
-    return cudaLaunchKernel(reinterpret_cast<const void*>(D.kern), dim3((unsigned)grid), dim3(k.threads), args, k.smem,
+    return cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)grid), dim3(k.threads), args, k.smem,
                             st);
 }
 
@@ -1387,12 +1394,16 @@ std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int
                 jk->smem = jit_smem_bytes(P, rb, wb, nbuf);
                 if (const char* e = std::getenv("QG_JIT_SMEM_PAD")) jk->smem += (size_t)std::atol(e);  // occupancy probe
                 if (auto hit = cache_get(ptx)) {
-                    jk->cubin = *hit;
+                    jk->mod = hit;
                     jk->ok = true;
                     g_cache_hits.fetch_add(1);
                 } else {
-                    jk->ok = jit_compile(ptx, jk->cubin, jk->err);
-                    if (jk->ok) cache_put(ptx, jk->cubin);
+                    auto m = std::make_shared<JitModule>();
+                    jk->ok = jit_compile(ptx, m->cubin, jk->err);
+                    if (jk->ok) {
+                        jk->mod = m;
+                        cache_put(ptx, m);
+                    }
                 }
             } else {
                 jk->err = "pass not covered by the emitter";

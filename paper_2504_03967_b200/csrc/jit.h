@@ -35,22 +35,28 @@ size_t jit_smem_bytes(const PassDesc<float>& P, int rb, int wb, int nbuf);
 // PTX -> sm_100a cubin (nvPTXCompiler); false + log on failure
 bool jit_compile(const std::string& ptx, std::vector<char>& cubin, std::string& log);
 
-// one compiled pass, loaded lazily per device
-struct JitKernel {
+// a compiled pass (cubin) and its per-device loaded library / kernel / grid;
+// shared process-wide through the PTX-keyed cache (jit.cpp)
+struct JitModule {
     std::vector<char> cubin;
-    std::string name;
-    size_t smem = 0;
-    int threads = 0;
-    bool ok = false;
-    std::string err;
-    // per device: loaded library / kernel / grid
     struct Dev {
         cudaLibrary_t lib = nullptr;
         cudaKernel_t kern = nullptr;
         int grid = 0;
     };
+    std::mutex mu;
     std::vector<Dev> dev;
-    ~JitKernel();
+    ~JitModule();
+};
+
+// one pass of a plan: the module, loaded lazily per device
+struct JitKernel {
+    std::shared_ptr<JitModule> mod;
+    std::string name;
+    size_t smem = 0;
+    int threads = 0;
+    bool ok = false;
+    std::string err;
 };
 
 cudaError_t launch_jit(JitKernel& k, const PassDesc<float>& P, void* psi, uint64_t rank_bits, cudaStream_t st);

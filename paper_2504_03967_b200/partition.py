@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import statevec as sv
-from .errors import BadWorkerCountError, SequenceMismatchError, UnnormalizedStateError
+from .errors import BadWorkerCountError, ProtocolViolationError, SequenceMismatchError, UnnormalizedStateError
 
 
 def _check_worker_count(n_qubits: int, workers: int) -> None:
@@ -263,6 +263,45 @@ def _permute_to_logical(full: torch.Tensor, n: int, phys_of_logical) -> torch.Te
     return x.permute(*dims).contiguous().reshape(-1)
 
 
+# --------------------------------------------------------------------------- rank agreement
+def plan_fingerprint(gate_type: np.ndarray, gate_param: np.ndarray, n_qubits: int, workers: int) -> int:
+    """63-bit digest of what every rank must agree on before exchanging blocks."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=8)
+    h.update(np.ascontiguousarray(gate_type, dtype=np.int32).tobytes())
+    h.update(np.ascontiguousarray(gate_param, dtype=np.float64).tobytes())
+    h.update(np.array([n_qubits, workers], dtype=np.int64).tobytes())
+    return int.from_bytes(h.digest(), "little") & ((1 << 63) - 1)
+
+
+def check_step(seq: int, fingerprint: int, group=None, final: bool = False, device=None) -> None:
+    """Every rank at the same exchange step of the same plan, or an error on every rank.
+
+    The reference checks each message's (sequence number, sender) and the workers'
+    final sequence numbers at the gather (partition.py:168-173, 112-141): here one
+    all-gather of (seq, plan fingerprint) per remap stands in for the per-message
+    check; a mismatch raises ProtocolViolationError (SequenceMismatchError for the
+    final step), and a failed or timed-out collective (the process group's timeout,
+    the reference's _JOIN_TIMEOUT, partition.py:50) is re-raised as
+    ProtocolViolationError."""
+    import torch.distributed as dist
+
+    try:
+        t = torch.tensor([seq, fingerprint], dtype=torch.int64,
+                         device=device if device is not None and not _host_wire(group) else "cpu")
+        allv = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(allv, t, group=group)
+    except Exception as e:  # NCCL / gloo failure or timeout
+        raise ProtocolViolationError(f"exchange step {seq}: collective failed: {e}") from e
+    vals = [tuple(int(x) for x in v.tolist()) for v in allv]
+    if len(set(v[1] for v in vals)) > 1:
+        raise ProtocolViolationError(f"ranks run different plans at step {seq}: {[v[1] for v in vals]}")
+    if len(set(v[0] for v in vals)) > 1:
+        err = SequenceMismatchError if final else ProtocolViolationError
+        raise err(f"ranks at different exchange steps: {[v[0] for v in vals]}")
+
+
 # --------------------------------------------------------------------------- sampling
 def logical_indices(phys: torch.Tensor, phys_of_logical) -> torch.Tensor:
     """Physical basis indices (rank bits on top) -> logical indices: logical qubit q
@@ -383,13 +422,19 @@ def execute_distributed(circuit, workers: int, options: sv.SimOptions | None = N
         sv.N.call("qg_state_init_zero", sv.C.c_void_p(shard.data_ptr()), n_local, sv._QG_DTYPE[options.precision],
                   rank, sv._stream(dev))
         staging = None
+        fp = plan_fingerprint(gt, gp, n, workers)
         for seg in range(plan.n_segments):
             plan.execute_segment(seg, shard, rank)
             if seg < plan.n_segments - 1:
                 gpos, lpos = plan.remaps[seg]
                 if delay_hook is not None:
                     delay_hook(rank, seg)
-                sent[rank] += remap_dist(shard, n_local, gpos, lpos, rank, group, staging)
+                check_step(seg, fp, group, device=dev)
+                try:
+                    sent[rank] += remap_dist(shard, n_local, gpos, lpos, rank, group, staging)
+                except Exception as e:
+                    raise ProtocolViolationError(f"remap {seg} failed: {e}") from e
+        check_step(plan.n_segments, fp, group, final=True, device=dev)
         counts_all = _comm(torch.tensor(sent, dtype=torch.int64, device=dev), group)
         dist.all_reduce(counts_all, group=group)
         sent = counts_all.cpu().tolist()

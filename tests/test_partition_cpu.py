@@ -118,3 +118,37 @@ def test_partner_masks_match_reference_plan(golden):
         pt.chunk_length(4, 3)
     with pytest.raises(BadWorkerCountError):
         pt.chunk_length(2, 8)
+
+
+def _step_worker(rank, world, port, seqs, fps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pt.check_step(seqs[rank], fps[rank], final=(seqs[0] == 99))
+        out[rank] = "ok"
+    except Exception as e:  # noqa: BLE001
+        out[rank] = type(e).__name__
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seqs,fps,want", [
+    ([3, 3], [7, 7], "ok"),
+    ([3, 4], [7, 7], "ProtocolViolationError"),       # a rank skipped / repeated an exchange
+    ([3, 3], [7, 8], "ProtocolViolationError"),       # ranks run different circuits
+    ([99, 98], [7, 7], "SequenceMismatchError"),      # final step: partition.py gather seq check
+])
+def test_check_step_agreement(seqs, fps, want):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_step_worker, args=(2, _free_port(), seqs, fps, out), nprocs=2, join=True)
+    assert out[0] == want and out[1] == want
+
+
+def test_plan_fingerprint():
+    gt = np.array([[0, -1, 1], [4, 0, 1]], dtype=np.int32)
+    gp = np.array([0.0, 0.0])
+    a = pt.plan_fingerprint(gt, gp, 3, 2)
+    assert a == pt.plan_fingerprint(gt.copy(), gp.copy(), 3, 2) and 0 <= a < 2**63
+    assert a != pt.plan_fingerprint(gt, gp + 1e-9, 3, 2) and a != pt.plan_fingerprint(gt, gp, 3, 4)
