@@ -63,8 +63,9 @@ typedef struct {
     int32_t max_stages;       /* 0 = auto; register stages per pass (SMEM transposes + 1) */
     int32_t max_cost;         /* 0 = auto; per-amplitude instruction budget of one pass */
     int32_t kernel_cfg;       /* 0 = auto; else 1 + id of the fused-kernel configuration (tuning) */
-    int32_t jit;              /* circuit-specialised pass kernels (complex64): 0 = auto (large shards),
-                                 1 = on, -1 = off (the op-stream interpreter runs every pass) */
+    int32_t jit;              /* circuit-specialised pass kernels (complex64): 0 = auto (shards >= 2^31
+                                 amplitudes: on; 2^22..2^30: tiered, compiled in the background while
+                                 the interpreter runs), 1 = on, -1 = off (the interpreter runs every pass) */
     int32_t low_qubits;       /* 0 = auto; else the lowest qubits every fused tile contains (>= 5 on
                                  large shards): contiguous runs of 2^low_qubits amplitudes per HBM access */
     int32_t reserved[3];
@@ -119,7 +120,8 @@ typedef struct {
     double compile_ms_sum;    /* emit + compile time summed over passes */
     double compile_ms_wall;   /* plan creation -> last pass compiled */
     int32_t threads;
-    int32_t enabled;
+    int32_t enabled;          /* 0 off, 1 JIT (execution waits per pass), 2 tiered: compiled in the
+                                 background, passes run on the interpreter until their kernel is ready */
 } qg_jit_status;
 int qg_plan_jit_status(const qg_plan* plan, int32_t wait, qg_jit_status* out);
 /* the PTX emitted for fused pass `pass_index` (running index over the plan's fused

@@ -57,18 +57,26 @@ struct DeviceGuard {
 // complex64 ids >= 4 are the single-buffered ones)
 int jit_nbuf(const qg_plan& p) { return p.cfg.id >= 4 ? 1 : 2; }
 
-bool jit_wanted(const qg_plan& p, int mode) {
-    if (mode < 0 || p.dtype != QG_DTYPE_C64 || p.d32.empty() || jit_nbuf(p) != 1) return false;
-    if (mode > 0) return true;
+// 0 = interpreter only, 1 = JIT (execution waits for each pass's kernel), 2 = tiered:
+// passes compile in the background and run on the interpreter until their kernel is
+// ready (the two produce bit-identical states, test_gpu_jit.py); the process-wide
+// cubin cache makes every later plan of the same circuit start fully compiled
+int jit_wanted(const qg_plan& p, int mode) {
+    if (mode < 0 || p.dtype != QG_DTYPE_C64 || p.d32.empty() || jit_nbuf(p) != 1) return 0;
+    if (mode > 0) return 1;
     // auto: shards large enough that a pass takes longer than its share of the
     // compilation (~0.2 s of one host core per pass, spread over the host's cores
-    // and overlapped with the execution of the earlier passes): >= 2^31 amplitudes
-    return p.n_local >= 31;
+    // and overlapped with the execution of the earlier passes): >= 2^31 amplitudes;
+    // mid-size shards tier up in the background
+    if (p.n_local >= 31) return 1;
+    return p.n_local >= 22 ? 2 : 0;
 }
 
 void jit_launch(qg_plan& p, int mode) {
-    if (!jit_wanted(p, mode)) return;
-    p.jit_threads = qg::jit_default_threads();
+    const int w = jit_wanted(p, mode);
+    if (!w) return;
+    p.jit_blocking = w == 1;
+    p.jit_threads = w == 1 ? qg::jit_default_threads() : std::min(4, qg::jit_default_threads());
     p.jit = qg::jit_start(p.d32, p.cfg.rb, p.cfg.wb, jit_nbuf(p), p.jit_threads);
 }
 
@@ -83,7 +91,8 @@ int run_segment(const qg_plan* plan, int64_t seg, void* state, int32_t rank, cud
     const int64_t shard_bytes = ((int64_t)1 << plan->n_local) * (plan->dtype == QG_DTYPE_C64 ? 8 : 16);
     for (size_t p = 0; p < passes.size(); ++p) {
         cudaError_t e;
-        qg::JitKernel* jk = (idx[p] >= 0 && plan->jit) ? plan->jit->wait(idx[p]) : nullptr;
+        qg::JitKernel* jk = nullptr;
+        if (idx[p] >= 0 && plan->jit) jk = plan->jit_blocking ? plan->jit->wait(idx[p]) : plan->jit->try_get(idx[p]);
         if (jk) {
             e = qg::launch_jit(*jk, plan->d32[idx[p]], state, rank_bits, st);
         } else if (idx[p] >= 0) {
@@ -160,7 +169,7 @@ int qg_plan_jit_status(const qg_plan* plan, int32_t wait, qg_jit_status* out) {
     if (!plan->jit) return QG_OK;
     qg::JitState& J = *plan->jit;
     if (wait) J.join();
-    out->enabled = 1;
+    out->enabled = plan->jit_blocking ? 1 : 2;
     out->threads = plan->jit_threads;
     out->n_jit = J.n_ok.load();
     out->n_fallback = J.n_fallback.load();

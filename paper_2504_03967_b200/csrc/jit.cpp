@@ -25,7 +25,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <functional>
 #include <map>
+#include <tuple>
 #include <unordered_map>
 #include <sstream>
 
@@ -61,7 +63,7 @@ struct Gen {
     int reads_left = 0;    // SMEM buffer reads left in the tile (async loads: the last one frees it)
     size_t off_coef, off_ph, off_tph;
     // smem layout
-    size_t buf_bytes, tab_gb, tab_pf, tab_uph;
+    size_t buf_bytes, tab_gb, tab_pf, tab_uph, tab_hp;
     static constexpr size_t kMapBytes = 576;  // 32 x u64 + 16 x u64 + 32 x u32 + 16 x u32
     // decode table: code -> (fam, T, C); fam 7 = CXM, 8 = XF, 9 = END
     struct Dec { int fam = -1, t = -1, c = -1; };
@@ -78,6 +80,7 @@ struct Gen {
         tab_gb = tbufs(var) * NBUF * buf_bytes;           // per mapping: [lane g | warp g | lane s | warp s]
         tab_pf = tab_gb + (size_t)(P.n_stages + 1) * kMapBytes;  // [lane part | warp part] of the prefetch offset
         tab_uph = tab_pf + 384;                                   // tile-uniform phase slots (float2 each)
+        tab_hp = tab_uph + 8 * (size_t)kMaxUph;                   // hoisted per-thread phase slots
         for (int i = 0; i < R; ++i) amap[i] = i;
         dec.resize(oc_end(RB) + 1);
         for (int t = 0; t < RB; ++t) {
@@ -98,6 +101,45 @@ struct Gen {
         dec[oc_xf(RB)] = {8, -1, -1};
         dec[oc_end(RB)] = {9, -1, -1};
     }
+    // variant 33554432: phase ops whose factor lists are predicated on thread-constant
+    // positions (the stage's lane / warp bits, rank bits) get those factors multiplied
+    // once per launch into a per-thread SMEM slot (QFT rows: lists of up to n entries
+    // otherwise re-evaluated every tile); the tile-id-predicated rest stays per tile
+    static constexpr int kMaxHoist = 12, kMinHoisted = 4;
+    std::map<int, int> hoist;  // op index -> slot
+    std::vector<std::pair<int, int>> hoist_ops;  // (stage, op index) per slot
+    bool thread_const(int s, uint32_t pos) const {
+        const StageDesc& S = P.stg[s];
+        for (int l = 0; l < kLaneBits; ++l) if (S.lane_q[l] == pos) return true;
+        for (int w = 0; w < WB; ++w) if (S.warp_q[w] == pos) return true;
+        for (int i = 0; i < k; ++i) if (P.tile_q[i] == pos) return false;
+        const int n_comp = 63 - __builtin_clzll(P.n_tiles);
+        for (int i = 0; i < n_comp; ++i) if (P.comp_q[i] == pos) return false;
+        return true;  // a rank bit
+    }
+    void plan_hoist() {
+        hoist.clear();
+        hoist_ops.clear();
+        if (!(variant & 33554432)) return;
+        std::vector<std::tuple<int, int, int>> cand;  // (-count, stage, op)
+        for (int s = 1; s <= P.n_stages; ++s)
+            for (int oi = P.stg[s].op_begin;; ++oi) {
+                const uint32_t w = P.ops[oi], code = w & 0xffu;
+                if (code >= dec.size() || dec[code].fam < 0 || dec[code].fam == 9) break;
+                if (dec[code].fam != F_PH && dec[code].fam != F_PHW) continue;
+                const int n = (w >> 8) & 0x7f, b = w >> 16;
+                int c = 0;
+                for (int kk = 1; kk < n; ++kk) c += thread_const(s, P.ph[b + kk].pos) ? 1 : 0;
+                if (c >= kMinHoisted) cand.emplace_back(-c, s, oi);
+            }
+        std::sort(cand.begin(), cand.end());
+        for (const auto& t : cand) {
+            if ((int)hoist_ops.size() == kMaxHoist) break;
+            hoist[std::get<2>(t)] = (int)hoist_ops.size();
+            hoist_ops.emplace_back(std::get<1>(t), std::get<2>(t));
+        }
+    }
+    size_t hoist_bytes() const { return hoist_ops.size() * (size_t)NT * 8; }
     // variant 8192: transposes alternate between two SMEM tile buffers (one barrier each)
     static int tbufs(int var) { return (var & 8192) ? 2 : 1; }
     static size_t smem_bytes(const PD& P, int rb, int wb, int nbuf, int var) {
@@ -280,8 +322,55 @@ struct Gen {
         o << le << ":\n";
     }
     // ph_product<false>: entry 0 unconditional, then predicated factors in list order
+    bool prologue_ = false;
+    // entry 0 times the thread-constant factors of op oi (stage s), tb = thread bits | rank bits
+    std::string hoisted_product(int s, uint32_t w, const std::string& tb) {
+        const int n = (w >> 8) & 0x7f, b = w >> 16;
+        std::string ex = ldp_f32(off_ph + 16 * b + 8), ey = ldp_f32(off_ph + 16 * b + 12);
+        std::string e = pack(ex, ey);
+        for (int kk = 1; kk < n; ++kk) {
+            const PhEnt<float>& E = P.ph[b + kk];
+            if (!thread_const(s, E.pos)) continue;
+            std::string on = pred_nz(bit(tb, (int)E.pos));
+            std::string vx = f(), vy = f();
+            std::string e0 = ldp_f32(off_ph + 16 * (b + kk) + 8), e1 = ldp_f32(off_ph + 16 * (b + kk) + 12);
+            L("selp.f32 ", vx, ", ", e0, ", 0f3F800000, ", on, ";");
+            L("selp.f32 ", vy, ", ", e1, ", 0f00000000, ", on, ";");
+            std::string ne = q();
+            c_mul(ne, e, bc(vx), bc(vy));
+            e = ne;
+        }
+        return e;
+    }
+    int cur_op = -1, cur_stage = -1;  // the op / stage being emitted (hoisted phase slots)
     std::string ph_product(uint32_t w, const std::string& tb) {
         const int n = (w >> 8) & 0x7f, b = w >> 16;
+        auto hz = hoist.find(cur_op);
+        if (hz != hoist.end() && !prologue_) {  // entry 0 and the thread-constant factors: one LDS
+            std::string e = q();
+            L("ld.shared.b64 ", e, ", [%hpb+", (size_t)hz->second * NT * 8, "];");
+            if ((w & 0x8000u) && P.n_uph > 0) {
+                std::string u = q(), ne = q(), ad = r();
+                L("add.u32 ", ad, ", %smb, ", tab_uph + 8 * (size_t)P.ph[b].pad, ";");
+                L("ld.shared.b64 ", u, ", [", ad, "];");
+                auto [ur2, ui2] = split_bc(u);
+                c_mul(ne, e, ur2, ui2);
+                e = ne;
+            }
+            for (int kk = 1; kk < n; ++kk) {
+                const PhEnt<float>& E = P.ph[b + kk];
+                if (thread_const(cur_stage, E.pos)) continue;
+                std::string on = pred_nz(bit(tb, (int)E.pos));
+                std::string vx = f(), vy = f();
+                std::string e0 = ldp_f32(off_ph + 16 * (b + kk) + 8), e1 = ldp_f32(off_ph + 16 * (b + kk) + 12);
+                L("selp.f32 ", vx, ", ", e0, ", 0f3F800000, ", on, ";");
+                L("selp.f32 ", vy, ", ", e1, ", 0f00000000, ", on, ";");
+                std::string ne = q();
+                c_mul(ne, e, bc(vx), bc(vy));
+                e = ne;
+            }
+            return e;
+        }
         std::string ex = ldp_f32(off_ph + 16 * b + 8), ey = ldp_f32(off_ph + 16 * b + 12);
         std::string e = pack(ex, ey);
         if ((w & 0x8000u) && P.n_uph > 0) {  // the tile-uniform factors (computed at the tile start)
@@ -711,18 +800,73 @@ struct Gen {
     }
     bool stored = false;
 
+    // a run of consecutive phase ops (slot vectors W_k, factors e_k, no flip-vector
+    // mixing) as ONE multiply per slot: slot p gets the product of the e_k with
+    // parity(W_k & p) = 1; the per-class products are formed once per tile
+    // (variant 16777216; same result up to the order of the complex products)
+    void flush_ph_run(std::vector<std::pair<uint32_t, std::string>>& run) {
+        if (run.empty()) return;
+        if (run.size() == 1) {
+            op_ph(run[0].first, run[0].second);
+            run.clear();
+            return;
+        }
+        const int m = (int)run.size();
+        std::map<uint32_t, std::string> f;  // class -> product (packed)
+        std::function<std::string(uint32_t)> prod = [&](uint32_t c) -> std::string {
+            auto it = f.find(c);
+            if (it != f.end()) return it->second;
+            const int k0 = __builtin_ctz(c);
+            std::string v;
+            if ((c & (c - 1)) == 0) {
+                v = run[k0].second;
+            } else {
+                const std::string rest = prod(c & (c - 1));
+                auto [er2, ei2] = split_bc(run[k0].second);
+                v = q();
+                c_mul(v, rest, er2, ei2);
+            }
+            f[c] = v;
+            return v;
+        };
+        std::map<uint32_t, std::pair<std::string, std::string>> fb;  // class -> broadcast pair
+        for (int i = 0; i < R; ++i) {
+            if (!in_sub(i)) continue;
+            uint32_t c = 0;
+            for (int k2 = 0; k2 < m; ++k2) c |= (uint32_t)par(run[k2].first & (uint32_t)i) << k2;
+            if (!c) continue;
+            auto it = fb.find(c);
+            if (it == fb.end()) it = fb.emplace(c, split_bc(prod(c))).first;
+            c_mul(a(i), a(i), it->second.first, it->second.second);
+        }
+        run.clear();
+    }
+
     // the op list and thread phases of stage s (slot filter applies)
     template <class TBF>
     bool stage_body(int s, TBF& TB) {
         const StageDesc& S = P.stg[s];
+        std::vector<std::pair<uint32_t, std::string>> run;  // pending phase ops (variant 16777216)
+        cur_stage = s;
         for (int oi = S.op_begin;; ++oi) {
+            cur_op = oi;
             const uint32_t w = P.ops[oi];
             const uint32_t code = w & 0xffu;
             if (code >= dec.size() || dec[code].fam < 0) return false;
             if ((variant & 8) && dec[code].fam != 9) continue;  // timing probe: no ops (wrong results)
             const Dec d = dec[code];
-            if (d.fam == 9) break;
             const uint32_t T = d.t >= 0 ? 1u << d.t : 0u, Cb = d.c >= 0 ? 1u << d.c : 0u;
+            if (variant & 16777216) {
+                if ((d.fam == F_PH || d.fam == F_PHW) && run.size() < 5) {
+                    const uint32_t W = d.fam == F_PH ? T : (T | Cb);
+                    if (!(W & fposs)) {
+                        run.emplace_back(W, ph_product(w, TB()));
+                        continue;
+                    }
+                }
+                flush_ph_run(run);
+            }
+            if (d.fam == 9) break;
             switch (d.fam) {
                 case F_RD: op_rd(T, T, w >> 16); break;
                 case F_CD: op_cd(T, T, w >> 16); break;
@@ -893,6 +1037,23 @@ struct Gen {
             L("@%pl0 st.shared.u64 [%tw8+", pf + 256, "], ", gw, ";");
         }
         L("setp.lt.u32 %pfl, ", lane, ", ", R, ";");
+        if (!hoist_ops.empty()) {  // per-thread products of the thread-constant phase factors
+            L("shl.b32 %hpb, %xtid, 3;");
+            L("add.u32 %hpb, %hpb, %smb;");
+            L("add.u32 %hpb, %hpb, ", tab_hp, ";");
+            std::string rk = q();
+            L("ld.param.u64 ", rk, ", [rk];");
+            prologue_ = true;
+            for (size_t h = 0; h < hoist_ops.size(); ++h) {
+                const int s2 = hoist_ops[h].first, oi = hoist_ops[h].second;
+                std::string g, so, tb = q();
+                thread_map(s2, lane, warp, g, so, true, true);
+                L("or.b64 ", tb, ", ", g, ", ", rk, ";");
+                std::string e = hoisted_product(s2, P.ops[oi], tb);
+                L("st.shared.b64 [%hpb+", h * (size_t)NT * 8, "], ", e, ";");
+            }
+            prologue_ = false;
+        }
         gen_pf = run_bits() >= 5 && (1 << (k - 5)) == NT;
         if (gen_pf) {  // thread t prefetches 256 B chunk t of the next tile (whatever the mappings)
             L("mov.u64 %pfg, 0;");
@@ -1220,7 +1381,7 @@ struct Gen {
         h << "\t.reg .f32 %f<" << (nf + 1) << ">;\n";
         h << "\t.reg .pred %p<" << (np + 1) << ">;\n";
         h << "\t.reg .b32 %xtid, %xlane, %xwarp, %smb, %smb2, %tlin, %tl8, %tw8, %tl4, %tw4, %F, %ctile, %nctile;\n";
-        h << "\t.reg .b64 %rdl, %pfg;\n";
+        h << "\t.reg .b64 %rdl, %pfg;\n\t.reg .b32 %hpb;\n";
         h << "\t.reg .b64 %gbm<" << (P.n_stages + 1) << ">;\n\t.reg .b32 %som<" << (P.n_stages + 1) << ">;\n";
         h << "\t.reg .b64 %tile, %tend, %ntile, %G, %base, %nbase, %dG, %psi, %rk, %pt;\n";
         h << "\t.reg .pred %pfl, %pend, %pnext, %pw0, %pl0;\n";
@@ -1245,11 +1406,14 @@ std::string jit_ptx_c64(const PassDesc<float>& P, int rb, int wb, int nbuf, cons
     Gen g(P, rb, wb, nbuf, jit_variant());
     if (const char* e = std::getenv("QG_JIT_STAGGER_NS")) g.stagger_ns = std::atoi(e);
     if (!g.supported()) return "";
+    g.plan_hoist();
     return g.run(name);
 }
 
 size_t jit_smem_bytes(const PassDesc<float>& P, int rb, int wb, int nbuf) {
-    return Gen::smem_bytes(P, rb, wb, nbuf, jit_variant());
+    Gen g(P, rb, wb, nbuf, jit_variant());
+    g.plan_hoist();
+    return Gen::smem_bytes(P, rb, wb, nbuf, jit_variant()) + g.hoist_bytes();
 }
 
 // Process-wide cache of compiled passes keyed by their PTX text: re-planning the
@@ -1361,6 +1525,14 @@ void JitState::join(bool cancel) {
     for (std::thread& t : workers)
         if (t.joinable()) t.join();
     workers.clear();
+}
+
+JitKernel* JitState::try_get(int64_t i) {
+    if (i < 0 || i >= (int64_t)k.size()) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ready[i]) return nullptr;
+    JitKernel* j = k[i].get();
+    return (j && j->ok) ? j : nullptr;
 }
 
 JitKernel* JitState::wait(int64_t i) {

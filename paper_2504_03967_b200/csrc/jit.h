@@ -78,6 +78,7 @@ struct JitState {
     std::string first_error;
     ~JitState();
     JitKernel* wait(int64_t i);           // nullptr: run the interpreter for this pass
+    JitKernel* try_get(int64_t i);        // non-blocking: nullptr until pass i is compiled
     // wait for the workers; cancel = stop handing out passes first (passes never
     // compiled stay not-ready: only for plan destruction / rebind)
     void join(bool cancel = false);

@@ -103,6 +103,7 @@ struct qg_plan {
     std::shared_ptr<qg::JitState> jit;
     int jit_threads = 0;
     int jit_mode = 0;  // qg_plan_opts.jit
+    bool jit_blocking = true;  // false: tiered (interpreter until a pass's kernel is ready)
 };
 
 namespace qg {

@@ -97,3 +97,28 @@ def test_jit_bitexact_at_32_qubits():
     assert same_bits(a, b)
     del a, b
     torch.cuda.empty_cache()
+
+
+def test_tiered_jit_is_bit_identical_across_tiers():
+    """jit=auto on a 2^24 shard compiles in the background: the first execution mixes
+    interpreter and compiled passes, a later plan of the same circuit starts fully
+    compiled from the process-wide cache; every tier gives the same bits."""
+    import torch
+
+    n = 24
+    gt, gp = random_arrays(RandomSpec(n, 300, 11))
+    first = sv.CompiledCircuit(gt, gp, n, "fp32")
+    assert first.jit_status()["enabled"] == 2
+    s1 = sv.init_zero_state(n, "fp32")
+    first.execute(s1)
+    st = first.jit_status(wait=True)
+    assert st["n_jit"] + st["n_fallback"] == st["n_passes"]
+    second = sv.CompiledCircuit(gt, gp, n, "fp32")
+    st2 = second.jit_status(wait=True)
+    s2 = sv.init_zero_state(n, "fp32")
+    second.execute(s2)
+    ref = sv.init_zero_state(n, "fp32")
+    sv.CompiledCircuit(gt, gp, n, "fp32", jit=-1).execute(ref)
+    a, b, c = (torch.view_as_real(x.amplitudes) for x in (s1, s2, ref))
+    assert torch.equal(a, c) and torch.equal(b, c)
+    assert st2["n_jit"] == st["n_jit"]
