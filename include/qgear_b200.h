@@ -64,7 +64,7 @@ typedef struct {
     int32_t max_cost;         /* 0 = auto; per-amplitude instruction budget of one pass */
     int32_t kernel_cfg;       /* 0 = auto; else 1 + id of the fused-kernel configuration (tuning) */
     int32_t jit;              /* circuit-specialised pass kernels (complex64): 0 = auto (shards >= 2^31
-                                 amplitudes: on; 2^22..2^30: tiered, compiled in the background while
+                                 amplitudes: on; 2^26..2^30: tiered, compiled in the background while
                                  the interpreter runs), 1 = on, -1 = off (the interpreter runs every pass) */
     int32_t low_qubits;       /* 0 = auto; else the lowest qubits every fused tile contains (>= 5 on
                                  large shards): contiguous runs of 2^low_qubits amplitudes per HBM access */

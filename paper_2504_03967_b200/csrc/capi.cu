@@ -69,7 +69,7 @@ int jit_wanted(const qg_plan& p, int mode) {
     // and overlapped with the execution of the earlier passes): >= 2^31 amplitudes;
     // mid-size shards tier up in the background
     if (p.n_local >= 31) return 1;
-    return p.n_local >= 22 ? 2 : 0;
+    return p.n_local >= 26 ? 2 : 0;
 }
 
 void jit_launch(qg_plan& p, int mode) {

@@ -1394,10 +1394,11 @@ struct Gen {
 int jit_variant() {
     static const int v = [] {
         // default: per-thread mapping values in registers (524288) and the last stage in
-        // slot subsets with interleaved stores (4194304); the other bits are
+        // slot subsets with interleaved stores (4194304) and thread-constant phase factors
+        // hoisted to the prologue (33554432); the other bits are
         // measurement probes (tools/jit_time.py, profiles/r02*_jit_variants*.jsonl)
         const char* e = std::getenv("QG_JIT_VARIANT");
-        return e ? std::atoi(e) : (524288 | 4194304);
+        return e ? std::atoi(e) : (524288 | 4194304 | 33554432);
     }();
     return v;
 }

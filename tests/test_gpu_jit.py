@@ -100,12 +100,12 @@ def test_jit_bitexact_at_32_qubits():
 
 
 def test_tiered_jit_is_bit_identical_across_tiers():
-    """jit=auto on a 2^24 shard compiles in the background: the first execution mixes
+    """jit=auto on a 2^26 shard compiles in the background: the first execution mixes
     interpreter and compiled passes, a later plan of the same circuit starts fully
     compiled from the process-wide cache; every tier gives the same bits."""
     import torch
 
-    n = 24
+    n = 26
     gt, gp = random_arrays(RandomSpec(n, 300, 11))
     first = sv.CompiledCircuit(gt, gp, n, "fp32")
     assert first.jit_status()["enabled"] == 2

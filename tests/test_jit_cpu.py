@@ -26,10 +26,10 @@ def test_every_pass_compiles_or_falls_back(make, n):
 
 
 def test_jit_policy():
+    g26, p26 = random_arrays(RandomSpec(26, 4, 0))
+    assert CompiledCircuit(g26, p26, 26, "fp32").jit_status(wait=True)["enabled"] == 2  # auto: tiered
     gt, gp = random_arrays(RandomSpec(22, 10, 0))
-    assert CompiledCircuit(gt, gp, 22, "fp32").jit_status(wait=True)["enabled"] == 2  # auto: tiered
-    g20, p20 = random_arrays(RandomSpec(20, 10, 0))
-    assert CompiledCircuit(g20, p20, 20, "fp32").jit_status()["enabled"] == 0         # auto: small shard
+    assert CompiledCircuit(gt, gp, 22, "fp32").jit_status()["enabled"] == 0          # auto: small shard
     assert CompiledCircuit(gt, gp, 22, "fp64", jit=1).jit_status()["enabled"] == 0   # complex64 only
     assert CompiledCircuit(gt, gp, 22, "fp32", jit=-1).jit_status()["enabled"] == 0
 
