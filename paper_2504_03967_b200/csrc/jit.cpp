@@ -794,7 +794,7 @@ struct Gen {
                 }
                 it = bases.emplace(lo, std::make_pair(x, Bases{})).first;
             }
-            L((variant & 65536) ? "st.global.b64 " : "st.global.cs.b64 ",
+            L((variant & 134217728) ? "st.global.wt.b64 " : (variant & 65536) ? "st.global.b64 " : "st.global.cs.b64 ",
               addr64(it->second.second, it->second.first, hi * 8), ", ", a(i), ";");
         }
     }

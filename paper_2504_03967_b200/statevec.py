@@ -465,6 +465,12 @@ class TreeSampler:
             self.prepare()
         na = 1 << self.n
         dev = self.amps.device
+        if not dense and na >= 1 << 16 and shots >= na // 8:
+            # many shots per outcome: the level-synchronous dense draw (the same counts
+            # bit for bit) and a device compaction beat the warp-per-leaf splits
+            d = self.draw(shots, rng_seed, tag, dense=True)
+            nz = torch.nonzero(d).flatten()
+            return nz + self.index_base, d[nz]
         cap = na if dense else max(1, min(int(shots), na))
         cnt = torch.empty(cap, dtype=torch.int64, device=dev)
         idx = None if dense else torch.empty(cap, dtype=torch.int64, device=dev)

@@ -80,9 +80,15 @@ def test_tree_sampler_statistics(precision, n):
     t2 = sv.sample_counts(st, shots, 11, sampler="tree")
     assert t.counts == t2.counts
     assert sv.sample_counts(st, shots, 12, sampler="tree").counts != t.counts
-    # dense mode: the same counts laid out per amplitude
+    # dense mode (level-synchronous kernels) and the warp-per-leaf compact mode draw the
+    # same counts bit for bit (few shots per outcome keeps the compact mode on its own path)
     ts = sv.TreeSampler(st.amplitudes)
     ts.prepare()
+    few = max(1, (1 << n) // 16)
+    dense = ts.draw(few, 11, dense=True).cpu().numpy()
+    ci, cc = ts.draw(few, 11)
+    nz = np.flatnonzero(dense)
+    assert np.array_equal(nz, ci.cpu().numpy()) and np.array_equal(dense[nz], cc.cpu().numpy())
     dense = ts.draw(shots, 11, dense=True).cpu().numpy()
     nz = np.flatnonzero(dense)
     assert np.array_equal(nz, t.indices) and np.array_equal(dense[nz], t.values)
