@@ -55,15 +55,19 @@ struct DeviceGuard {
 
 // fused-kernel configurations the JIT emitter covers (must match launch_fused:
 // complex64 ids >= 4 are the single-buffered ones)
-int jit_nbuf(const qg_plan& p) { return p.cfg.id >= 4 ? 1 : 2; }
+int jit_nbuf(const qg_plan& p) {
+    return p.dtype == QG_DTYPE_C64 ? (p.cfg.id >= 4 ? 1 : 2) : (p.cfg.id == 3 ? 1 : 2);
+}
 
 // 0 = interpreter only, 1 = JIT (execution waits for each pass's kernel), 2 = tiered:
 // passes compile in the background and run on the interpreter until their kernel is
 // ready (the two produce bit-identical states, test_gpu_jit.py); the process-wide
 // cubin cache makes every later plan of the same circuit start fully compiled
 int jit_wanted(const qg_plan& p, int mode) {
-    if (mode < 0 || p.dtype != QG_DTYPE_C64 || p.d32.empty() || jit_nbuf(p) != 1) return 0;
+    if (mode < 0 || jit_nbuf(p) != 1) return 0;
+    if (p.dtype == QG_DTYPE_C64 ? p.d32.empty() : p.d64.empty()) return 0;
     if (mode > 0) return 1;
+    if (p.dtype == QG_DTYPE_C128) return p.n_local >= 30 ? 1 : (p.n_local >= 26 ? 2 : 0);  // same bytes as c64 + 1
     // auto: shards large enough that a pass takes longer than its share of the
     // compilation (~0.2 s of one host core per pass, spread over the host's cores
     // and overlapped with the execution of the earlier passes): >= 2^31 amplitudes;
@@ -77,7 +81,8 @@ void jit_launch(qg_plan& p, int mode) {
     if (!w) return;
     p.jit_blocking = w == 1;
     p.jit_threads = w == 1 ? qg::jit_default_threads() : std::min(4, qg::jit_default_threads());
-    p.jit = qg::jit_start(p.d32, p.cfg.rb, p.cfg.wb, jit_nbuf(p), p.jit_threads);
+    p.jit = p.dtype == QG_DTYPE_C64 ? qg::jit_start(p.d32, p.cfg.rb, p.cfg.wb, jit_nbuf(p), p.jit_threads)
+                                    : qg::jit_start(p.d64, p.cfg.rb, p.cfg.wb, jit_nbuf(p), p.jit_threads);
 }
 
 int check_dtype(int32_t dtype) {
@@ -94,7 +99,9 @@ int run_segment(const qg_plan* plan, int64_t seg, void* state, int32_t rank, cud
         qg::JitKernel* jk = nullptr;
         if (idx[p] >= 0 && plan->jit) jk = plan->jit_blocking ? plan->jit->wait(idx[p]) : plan->jit->try_get(idx[p]);
         if (jk) {
-            e = qg::launch_jit(*jk, plan->d32[idx[p]], state, rank_bits, st);
+            const void* d = plan->dtype == QG_DTYPE_C64 ? (const void*)&plan->d32[idx[p]] : (const void*)&plan->d64[idx[p]];
+            const uint64_t nt = plan->dtype == QG_DTYPE_C64 ? plan->d32[idx[p]].n_tiles : plan->d64[idx[p]].n_tiles;
+            e = qg::launch_jit(*jk, d, nt, state, rank_bits, st);
         } else if (idx[p] >= 0) {
             const void* d = plan->dtype == QG_DTYPE_C64 ? (const void*)&plan->d32[idx[p]] : (const void*)&plan->d64[idx[p]];
             e = qg::launch_fused(plan->dtype, plan->cfg.id, d, state, rank_bits, st);
@@ -165,7 +172,7 @@ int qg_plan_rebind(qg_plan* plan, const double* gate_param, int64_t n_gates) {
 int qg_plan_jit_status(const qg_plan* plan, int32_t wait, qg_jit_status* out) {
     if (!plan || !out) return fail(QG_E_INVALID_ARG, "NULL argument");
     std::memset(out, 0, sizeof *out);
-    out->n_passes = (int64_t)plan->d32.size();
+    out->n_passes = plan->dtype == QG_DTYPE_C64 ? (int64_t)plan->d32.size() : (int64_t)plan->d64.size();
     if (!plan->jit) return QG_OK;
     qg::JitState& J = *plan->jit;
     if (wait) J.join();
@@ -184,9 +191,12 @@ int qg_plan_jit_status(const qg_plan* plan, int32_t wait, qg_jit_status* out) {
 
 int qg_plan_pass_ptx(const qg_plan* plan, int64_t pass_index, char* buf, int64_t cap, int64_t* len) {
     if (!plan || !len) return fail(QG_E_INVALID_ARG, "NULL argument");
-    if (plan->dtype != QG_DTYPE_C64) return fail(QG_E_INVALID_ARG, "the pass emitter covers complex64 plans");
-    if (pass_index < 0 || pass_index >= (int64_t)plan->d32.size()) return fail(QG_E_INVALID_ARG, "pass_index out of range");
-    const std::string ptx = qg::jit_ptx_c64(plan->d32[pass_index], plan->cfg.rb, plan->cfg.wb, jit_nbuf(*plan), "qg_jit_pass");
+    const int64_t nd = plan->dtype == QG_DTYPE_C64 ? (int64_t)plan->d32.size() : (int64_t)plan->d64.size();
+    if (pass_index < 0 || pass_index >= nd) return fail(QG_E_INVALID_ARG, "pass_index out of range");
+    const std::string ptx =
+        plan->dtype == QG_DTYPE_C64
+            ? qg::jit_ptx(plan->d32[pass_index], plan->cfg.rb, plan->cfg.wb, jit_nbuf(*plan), "qg_jit_pass")
+            : qg::jit_ptx(plan->d64[pass_index], plan->cfg.rb, plan->cfg.wb, jit_nbuf(*plan), "qg_jit_pass");
     *len = (int64_t)ptx.size();
     if (buf && cap > 0) {
         const int64_t n = std::min<int64_t>(cap - 1, (int64_t)ptx.size());

@@ -37,8 +37,6 @@ std::atomic<int64_t> g_cache_hits{0};
 
 namespace {
 
-using PD = PassDesc<float>;
-
 int par(uint64_t x) { return __builtin_parityll(x); }
 
 std::string u64s(uint64_t v) {
@@ -47,11 +45,17 @@ std::string u64s(uint64_t v) {
     return b;
 }
 
+template <typename Real>
 struct Gen {
+    using PD = PassDesc<Real>;
+    // complex64: amplitudes are packed f32x2 (.b64), math in FFMA2 / FMUL2;
+    // complex128: amplitudes are .b128 registers unpacked into f64 for DFMA math
+    static constexpr bool D = sizeof(Real) == 8;
+    static constexpr int ES = D ? 16 : 8, ESL = D ? 4 : 3;  // amplitude bytes / log2
     const PD& P;
     int RB, WB, NBUF, R, NT, k;
     std::ostringstream o;
-    int nq = 0, nr = 0, nf = 0, np = 0, nl = 0;
+    int nq = 0, nr = 0, nf = 0, np = 0, nl = 0, nx = 0, nd = 0;
     int amap[64];          // slot -> %a register index (register CX moves rename)
     uint32_t fposs = 0;    // slot bits of the flip vector F that may be 1
     // bit 0: tile loads as cp.async into the SMEM buffer, issued a tile ahead; 2048: one CTA per SM
@@ -70,17 +74,19 @@ struct Gen {
     std::vector<Dec> dec;
 
     Gen(const PD& p, int rb, int wb, int nbuf, int var) : P(p), RB(rb), WB(wb), NBUF(nbuf), variant(var) {
+        if (D) variant &= (8 | 16 | 32 | 128 | 16384 | 32768 | 524288 | 4194304 | 33554432);  // c128: no probes of
+                                                                                          // the c64 memory path
         R = 1 << RB;
         NT = 32 << WB;
         k = P.k;
         off_coef = offsetof(PD, coef);
         off_ph = offsetof(PD, ph);
         off_tph = offsetof(PD, tph);
-        buf_bytes = (size_t)8 << k;
+        buf_bytes = (size_t)ES << k;
         tab_gb = tbufs(var) * NBUF * buf_bytes;           // per mapping: [lane g | warp g | lane s | warp s]
         tab_pf = tab_gb + (size_t)(P.n_stages + 1) * kMapBytes;  // [lane part | warp part] of the prefetch offset
         tab_uph = tab_pf + 384;                                   // tile-uniform phase slots (float2 each)
-        tab_hp = tab_uph + 8 * (size_t)kMaxUph;                   // hoisted per-thread phase slots
+        tab_hp = tab_uph + ES * (size_t)kMaxUph;                  // hoisted per-thread phase slots
         for (int i = 0; i < R; ++i) amap[i] = i;
         dec.resize(oc_end(RB) + 1);
         for (int t = 0; t < RB; ++t) {
@@ -139,20 +145,36 @@ struct Gen {
             hoist_ops.emplace_back(std::get<1>(t), std::get<2>(t));
         }
     }
-    size_t hoist_bytes() const { return hoist_ops.size() * (size_t)NT * 8; }
+    size_t hoist_bytes() const { return hoist_ops.size() * (size_t)NT * ES; }
     // variant 8192: transposes alternate between two SMEM tile buffers (one barrier each)
     static int tbufs(int var) { return (var & 8192) ? 2 : 1; }
     static size_t smem_bytes(const PD& P, int rb, int wb, int nbuf, int var) {
         (void)rb;
         (void)wb;
-        return tbufs(var) * nbuf * ((size_t)8 << P.k) + (size_t)(P.n_stages + 1) * kMapBytes + 384 +
-               8 * (size_t)kMaxUph;
+        return tbufs(var) * nbuf * ((size_t)ES << P.k) + (size_t)(P.n_stages + 1) * kMapBytes + 384 +
+               ES * (size_t)kMaxUph;
     }
 
     std::string q() { return "%q" + std::to_string(nq++); }
     std::string r() { return "%r" + std::to_string(nr++); }
     std::string f() { return "%f" + std::to_string(nf++); }
     std::string p() { return "%p" + std::to_string(np++); }
+    std::string xq() { return "%x" + std::to_string(nx++); }  // .b128 (complex128 value)
+    std::string dq() { return "%d" + std::to_string(nd++); }  // .f64
+    std::string cv() { return D ? xq() : q(); }               // a complex value
+    std::string sv() { return D ? dq() : f(); }               // a real scalar
+    static constexpr const char* ST = D ? "f64" : "f32";
+    static constexpr const char* ONE = D ? "0d3FF0000000000000" : "0f3F800000";
+    static constexpr const char* ZERO = D ? "0d0000000000000000" : "0f00000000";
+    static constexpr const char* CB = D ? "b128" : "b64";     // bit type of a complex value
+    // parameter-space offsets of the Real-typed fields
+    static size_t phe(int idx, int part) {  // PhEnt<Real> idx, part 0 = re, 1 = im
+        return offsetof(PD, ph) + sizeof(PhEnt<Real>) * (size_t)idx + offsetof(PhEnt<Real>, e) + sizeof(Real) * part;
+    }
+    static size_t tphv(int idx, int kk) {   // Entry<Real> idx, v[kk]
+        return offsetof(PD, tph) + sizeof(Entry<Real>) * (size_t)idx + offsetof(Entry<Real>, v) + sizeof(Real) * kk;
+    }
+    size_t coefo(uint32_t c) const { return off_coef + sizeof(Real) * (size_t)c; }
     std::string lab() { return "$J" + std::to_string(nl++); }
     std::string a(int slot) const { return "%a" + std::to_string(amap[slot]); }
     template <class... A>
@@ -163,15 +185,65 @@ struct Gen {
     }
 
     // ---------------------------------------------------------------- values
-    std::string ldp_f32(size_t off) {
-        std::string v = f();
-        L("ld.param.f32 ", v, ", [P+", off, "];");
+    std::string ldp_f32(size_t off) {  // a Real scalar from the parameter space
+        std::string v = sv();
+        L("ld.param.", ST, " ", v, ", [P+", off, "];");
         return v;
     }
-    std::string bc(const std::string& fv) {  // {v, v}
+    std::string bc(const std::string& fv) {  // {v, v} (complex64); the scalar itself (complex128)
+        if (D) return fv;
         std::string v = q();
         L("mov.b64 ", v, ", {", fv, ", ", fv, "};");
         return v;
+    }
+    std::pair<std::string, std::string> unpack(const std::string& c) {
+        std::string xr = sv(), xi = sv();
+        L("mov.", CB, " {", xr, ", ", xi, "}, ", c, ";");
+        return {xr, xi};
+    }
+    std::string shfl_s(const std::string& v, int o2) {  // butterfly shuffle of a Real scalar
+        std::string out = sv();
+        if (!D) {
+            L("shfl.sync.bfly.b32 ", out, ", ", v, ", ", o2, ", 31, 0xffffffff;");
+            return out;
+        }
+        std::string lo = r(), hi = r(), slo = r(), shi = r();
+        L("mov.b64 {", lo, ", ", hi, "}, ", v, ";");
+        L("shfl.sync.bfly.b32 ", slo, ", ", lo, ", ", o2, ", 31, 0xffffffff;");
+        L("shfl.sync.bfly.b32 ", shi, ", ", hi, ", ", o2, ", 31, 0xffffffff;");
+        L("mov.b64 ", out, ", {", slo, ", ", shi, "};");
+        return out;
+    }
+    void pack_into(const std::string& d, const std::string& x, const std::string& y) {
+        L("mov.", CB, " ", d, ", {", x, ", ", y, "};");
+    }
+    // complex value: a if pred else b
+    std::string csel(const std::string& a_, const std::string& b_, const std::string& pred) {
+        std::string v = cv();
+        if (!D) {
+            L("selp.b64 ", v, ", ", a_, ", ", b_, ", ", pred, ";");
+            return v;
+        }
+        auto [ar, ai] = unpack(a_);
+        auto [br, bi] = unpack(b_);
+        std::string vr = dq(), vi = dq();
+        L("selp.f64 ", vr, ", ", ar, ", ", br, ", ", pred, ";");
+        L("selp.f64 ", vi, ", ", ai, ", ", bi, ", ", pred, ";");
+        pack_into(v, vr, vi);
+        return v;
+    }
+    // x += s * y (the shear of p_rot), in place
+    void rfma(const std::string& x, const std::string& y, const std::string& s2) {
+        if (!D) {
+            L("fma.rn.f32x2 ", x, ", ", y, ", ", s2, ", ", x, ";");
+            return;
+        }
+        auto [xr, xi] = unpack(x);
+        auto [yr, yi] = unpack(y);
+        std::string nr_ = dq(), ni_ = dq();
+        L("fma.rn.f64 ", nr_, ", ", yr, ", ", s2, ", ", xr, ";");
+        L("fma.rn.f64 ", ni_, ", ", yi, ", ", s2, ", ", xi, ";");
+        pack_into(x, nr_, ni_);
     }
     // complex multiply / multiply-add in fused.cu's exact operation order
     std::string swp(const std::string& x) {  // {-x.y, x.x}
@@ -182,25 +254,47 @@ struct Gen {
         return s;
     }
     void c_mul(const std::string& d, const std::string& x, const std::string& mr2, const std::string& mi2) {
+        if (D) {  // d = x * (mr + i mi): (xr mr - xi mi, xi mr + xr mi)
+            auto [xr, xi] = unpack(x);
+            std::string tr = dq(), ti = dq(), nm = dq(), dr = dq(), di = dq();
+            L("mul.rn.f64 ", tr, ", ", xr, ", ", mr2, ";");
+            L("mul.rn.f64 ", ti, ", ", xi, ", ", mr2, ";");
+            L("neg.f64 ", nm, ", ", mi2, ";");
+            L("fma.rn.f64 ", dr, ", ", xi, ", ", nm, ", ", tr, ";");
+            L("fma.rn.f64 ", di, ", ", xr, ", ", mi2, ", ", ti, ";");
+            pack_into(d, dr, di);
+            return;
+        }
         std::string s = swp(x), t = q();
         L("mul.rn.f32x2 ", t, ", ", x, ", ", mr2, ";");
         L("fma.rn.f32x2 ", d, ", ", s, ", ", mi2, ", ", t, ";");
     }
     void c_fma(const std::string& d, const std::string& acc, const std::string& x, const std::string& mr2,
                const std::string& mi2) {
+        if (D) {  // d = acc + x * (mr + i mi)
+            auto [xr, xi] = unpack(x);
+            auto [ar, ai] = unpack(acc);
+            std::string tr = dq(), ti = dq(), nm = dq(), dr = dq(), di = dq();
+            L("fma.rn.f64 ", tr, ", ", xr, ", ", mr2, ", ", ar, ";");
+            L("fma.rn.f64 ", ti, ", ", xi, ", ", mr2, ", ", ai, ";");
+            L("neg.f64 ", nm, ", ", mi2, ";");
+            L("fma.rn.f64 ", dr, ", ", xi, ", ", nm, ", ", tr, ";");
+            L("fma.rn.f64 ", di, ", ", xr, ", ", mi2, ", ", ti, ";");
+            pack_into(d, dr, di);
+            return;
+        }
         std::string s = swp(x), t = q();
         L("fma.rn.f32x2 ", t, ", ", x, ", ", mr2, ", ", acc, ";");
         L("fma.rn.f32x2 ", d, ", ", s, ", ", mi2, ", ", t, ";");
     }
     // packed complex e -> ({e.x, e.x}, {e.y, e.y})
     std::pair<std::string, std::string> split_bc(const std::string& e) {
-        std::string ex = f(), ey = f();
-        L("mov.b64 {", ex, ", ", ey, "}, ", e, ";");
+        auto [ex, ey] = unpack(e);
         return {bc(ex), bc(ey)};
     }
     std::string pack(const std::string& x, const std::string& y) {
-        std::string v = q();
-        L("mov.b64 ", v, ", {", x, ", ", y, "};");
+        std::string v = cv();
+        pack_into(v, x, y);
         return v;
     }
     // 1 if bit `pos` of the 64-bit value v is set (u32 0/1)
@@ -236,34 +330,34 @@ struct Gen {
             for (int i = 0; i < R; ++i) {
                 if (par(W & (uint32_t)i) || !in_sub(i)) continue;
                 const int j = i ^ (int)V;
-                if (pass == 1) L("fma.rn.f32x2 ", a(j), ", ", a(i), ", ", sb2, ", ", a(j), ";");
-                else L("fma.rn.f32x2 ", a(i), ", ", a(j), ", ", sa2, ", ", a(i), ";");
+                if (pass == 1) rfma(a(j), a(i), sb2);
+                else rfma(a(i), a(j), sa2);
             }
     }
     void op_rd(uint32_t V, uint32_t W, uint32_t coef) {
-        std::string m0 = ldp_f32(off_coef + 4 * coef), m1 = ldp_f32(off_coef + 4 * (coef + 1));
+        std::string m0 = ldp_f32(coefo(coef)), m1 = ldp_f32(coefo(coef + 1));
         std::string sa = m0, sb = m1;
         if (W & fposs) {
-            std::string fp = fpar(W), n0 = f(), n1 = f();
-            sa = f();
-            sb = f();
-            L("neg.f32 ", n0, ", ", m0, ";");
-            L("neg.f32 ", n1, ", ", m1, ";");
-            L("selp.f32 ", sa, ", ", n0, ", ", m0, ", ", fp, ";");
-            L("selp.f32 ", sb, ", ", n1, ", ", m1, ", ", fp, ";");
+            std::string fp = fpar(W), n0 = sv(), n1 = sv();
+            sa = sv();
+            sb = sv();
+            L("neg.", ST, " ", n0, ", ", m0, ";");
+            L("neg.", ST, " ", n1, ", ", m1, ";");
+            L("selp.", ST, " ", sa, ", ", n0, ", ", m0, ", ", fp, ";");
+            L("selp.", ST, " ", sb, ", ", n1, ", ", m1, ", ", fp, ";");
         }
         p_rot(V, W, bc(sa), bc(sb));
     }
     void op_cd(uint32_t V, uint32_t W, uint32_t coef) {
         std::string m[8];
-        for (int i = 0; i < 8; ++i) m[i] = ldp_f32(off_coef + 4 * (coef + i));
+        for (int i = 0; i < 8; ++i) m[i] = ldp_f32(coefo(coef + i));
         std::string c[8];
         if (W & fposs) {  // X U X: c = (m11, m10, m01, m00)
             std::string fp = fpar(W);
             static const int sw[8] = {6, 7, 4, 5, 2, 3, 0, 1};
             for (int i = 0; i < 8; ++i) {
-                c[i] = f();
-                L("selp.f32 ", c[i], ", ", m[sw[i]], ", ", m[i], ", ", fp, ";");
+                c[i] = sv();
+                L("selp.", ST, " ", c[i], ", ", m[sw[i]], ", ", m[i], ", ", fp, ";");
             }
         } else {
             for (int i = 0; i < 8; ++i) c[i] = m[i];
@@ -273,7 +367,7 @@ struct Gen {
         for (int i = 0; i < R; ++i) {
             if (par(W & (uint32_t)i) || !in_sub(i)) continue;
             const int j = i ^ (int)V;
-            std::string ty = q(), tx = q();
+            std::string ty = cv(), tx = cv();
             c_mul(ty, a(j), c01r, c01i);
             c_mul(tx, a(i), c10r, c10i);
             c_fma(a(i), ty, a(i), c00r, c00i);
@@ -299,13 +393,12 @@ struct Gen {
         L("@", p0, " bra.uni ", la, ";");
         L("@", p1, " bra.uni ", lb, ";");
         {  // mixed warp: per-thread diag(d0, d1)
-            std::string ex = f(), ey = f();
-            L("mov.b64 {", ex, ", ", ey, "}, ", e, ";");
-            std::string d0x = f(), d0y = f(), d1x = f(), d1y = f();
-            L("selp.f32 ", d0x, ", ", ex, ", 0f3F800000, ", fp, ";");
-            L("selp.f32 ", d0y, ", ", ey, ", 0f00000000, ", fp, ";");
-            L("selp.f32 ", d1x, ", 0f3F800000, ", ex, ", ", fp, ";");
-            L("selp.f32 ", d1y, ", 0f00000000, ", ey, ", ", fp, ";");
+            auto [ex, ey] = unpack(e);
+            std::string d0x = sv(), d0y = sv(), d1x = sv(), d1y = sv();
+            L("selp.", ST, " ", d0x, ", ", ex, ", ", ONE, ", ", fp, ";");
+            L("selp.", ST, " ", d0y, ", ", ey, ", ", ZERO, ", ", fp, ";");
+            L("selp.", ST, " ", d1x, ", ", ONE, ", ", ex, ", ", fp, ";");
+            L("selp.", ST, " ", d1y, ", ", ZERO, ", ", ey, ", ", fp, ";");
             std::string d0r = bc(d0x), d0i = bc(d0y), d1r = bc(d1x), d1i = bc(d1y);
             for (int i = 0; i < R; ++i) {
                 if (!in_sub(i)) continue;
@@ -326,17 +419,17 @@ struct Gen {
     // entry 0 times the thread-constant factors of op oi (stage s), tb = thread bits | rank bits
     std::string hoisted_product(int s, uint32_t w, const std::string& tb) {
         const int n = (w >> 8) & 0x7f, b = w >> 16;
-        std::string ex = ldp_f32(off_ph + 16 * b + 8), ey = ldp_f32(off_ph + 16 * b + 12);
+        std::string ex = ldp_f32(phe(b, 0)), ey = ldp_f32(phe(b, 1));
         std::string e = pack(ex, ey);
         for (int kk = 1; kk < n; ++kk) {
-            const PhEnt<float>& E = P.ph[b + kk];
+            const PhEnt<Real>& E = P.ph[b + kk];
             if (!thread_const(s, E.pos)) continue;
             std::string on = pred_nz(bit(tb, (int)E.pos));
-            std::string vx = f(), vy = f();
-            std::string e0 = ldp_f32(off_ph + 16 * (b + kk) + 8), e1 = ldp_f32(off_ph + 16 * (b + kk) + 12);
-            L("selp.f32 ", vx, ", ", e0, ", 0f3F800000, ", on, ";");
-            L("selp.f32 ", vy, ", ", e1, ", 0f00000000, ", on, ";");
-            std::string ne = q();
+            std::string vx = sv(), vy = sv();
+            std::string e0 = ldp_f32(phe(b + kk, 0)), e1 = ldp_f32(phe(b + kk, 1));
+            L("selp.", ST, " ", vx, ", ", e0, ", ", ONE, ", ", on, ";");
+            L("selp.", ST, " ", vy, ", ", e1, ", ", ZERO, ", ", on, ";");
+            std::string ne = cv();
             c_mul(ne, e, bc(vx), bc(vy));
             e = ne;
         }
@@ -347,55 +440,55 @@ struct Gen {
         const int n = (w >> 8) & 0x7f, b = w >> 16;
         auto hz = hoist.find(cur_op);
         if (hz != hoist.end() && !prologue_) {  // entry 0 and the thread-constant factors: one LDS
-            std::string e = q();
-            L("ld.shared.b64 ", e, ", [%hpb+", (size_t)hz->second * NT * 8, "];");
+            std::string e = cv();
+            L("ld.shared.", CB, " ", e, ", [%hpb+", (size_t)hz->second * NT * ES, "];");
             if ((w & 0x8000u) && P.n_uph > 0) {
-                std::string u = q(), ne = q(), ad = r();
-                L("add.u32 ", ad, ", %smb, ", tab_uph + 8 * (size_t)P.ph[b].pad, ";");
-                L("ld.shared.b64 ", u, ", [", ad, "];");
+                std::string u = cv(), ne = cv(), ad = r();
+                L("add.u32 ", ad, ", %smb, ", tab_uph + ES * (size_t)P.ph[b].pad, ";");
+                L("ld.shared.", CB, " ", u, ", [", ad, "];");
                 auto [ur2, ui2] = split_bc(u);
                 c_mul(ne, e, ur2, ui2);
                 e = ne;
             }
             for (int kk = 1; kk < n; ++kk) {
-                const PhEnt<float>& E = P.ph[b + kk];
+                const PhEnt<Real>& E = P.ph[b + kk];
                 if (thread_const(cur_stage, E.pos)) continue;
                 std::string on = pred_nz(bit(tb, (int)E.pos));
-                std::string vx = f(), vy = f();
-                std::string e0 = ldp_f32(off_ph + 16 * (b + kk) + 8), e1 = ldp_f32(off_ph + 16 * (b + kk) + 12);
-                L("selp.f32 ", vx, ", ", e0, ", 0f3F800000, ", on, ";");
-                L("selp.f32 ", vy, ", ", e1, ", 0f00000000, ", on, ";");
-                std::string ne = q();
+                std::string vx = sv(), vy = sv();
+                std::string e0 = ldp_f32(phe(b + kk, 0)), e1 = ldp_f32(phe(b + kk, 1));
+                L("selp.", ST, " ", vx, ", ", e0, ", ", ONE, ", ", on, ";");
+                L("selp.", ST, " ", vy, ", ", e1, ", ", ZERO, ", ", on, ";");
+                std::string ne = cv();
                 c_mul(ne, e, bc(vx), bc(vy));
                 e = ne;
             }
             return e;
         }
-        std::string ex = ldp_f32(off_ph + 16 * b + 8), ey = ldp_f32(off_ph + 16 * b + 12);
+        std::string ex = ldp_f32(phe(b, 0)), ey = ldp_f32(phe(b, 1));
         std::string e = pack(ex, ey);
         if ((w & 0x8000u) && P.n_uph > 0) {  // the tile-uniform factors (computed at the tile start)
-            std::string u = q(), ne = q(), ad = r();
-            L("add.u32 ", ad, ", %smb, ", tab_uph + 8 * (size_t)P.ph[b].pad, ";");
-            L("ld.shared.b64 ", u, ", [", ad, "];");
+            std::string u = cv(), ne = cv(), ad = r();
+            L("add.u32 ", ad, ", %smb, ", tab_uph + ES * (size_t)P.ph[b].pad, ";");
+            L("ld.shared.", CB, " ", u, ", [", ad, "];");
             auto [ur2, ui2] = split_bc(u);
             c_mul(ne, e, ur2, ui2);
             e = ne;
         }
         for (int kk = 1; kk < n; ++kk) {
-            const PhEnt<float>& E = P.ph[b + kk];
+            const PhEnt<Real>& E = P.ph[b + kk];
             std::string on = pred_nz(bit(tb, (int)E.pos));
-            std::string vx = f(), vy = f();
-            std::string e0 = ldp_f32(off_ph + 16 * (b + kk) + 8), e1 = ldp_f32(off_ph + 16 * (b + kk) + 12);
-            L("selp.f32 ", vx, ", ", e0, ", 0f3F800000, ", on, ";");
-            L("selp.f32 ", vy, ", ", e1, ", 0f00000000, ", on, ";");
-            std::string ne = q();
+            std::string vx = sv(), vy = sv();
+            std::string e0 = ldp_f32(phe(b + kk, 0)), e1 = ldp_f32(phe(b + kk, 1));
+            L("selp.", ST, " ", vx, ", ", e0, ", ", ONE, ", ", on, ";");
+            L("selp.", ST, " ", vy, ", ", e1, ", ", ZERO, ", ", on, ";");
+            std::string ne = cv();
             c_mul(ne, e, bc(vx), bc(vy));
             e = ne;
         }
         return e;
     }
     void op_ph2(int T, int C, uint32_t coef) {
-        std::string ex = ldp_f32(off_coef + 4 * coef), ey = ldp_f32(off_coef + 4 * (coef + 1));
+        std::string ex = ldp_f32(coefo(coef)), ey = ldp_f32(coefo(coef + 1));
         std::string er2 = bc(ex), ei2 = bc(ey);
         auto cphase = [&]() {
             for (int i = 0; i < R; ++i)
@@ -423,9 +516,9 @@ struct Gen {
                 L("xor.b32 ", bcv, ", ", fc, ", ", sc, ";");
                 L("and.b32 ", both, ", ", bt, ", ", bcv, ";");
                 pp = pred_nz(both);
-                std::string x = f(), y = f();
-                L("selp.f32 ", x, ", ", ex, ", 0f3F800000, ", pp, ";");
-                L("selp.f32 ", y, ", ", ey, ", 0f00000000, ", pp, ";");
+                std::string x = sv(), y = sv();
+                L("selp.", ST, " ", x, ", ", ex, ", ", ONE, ", ", pp, ";");
+                L("selp.", ST, " ", y, ", ", ey, ", ", ZERO, ", ", pp, ";");
                 vr[combo] = bc(x);
                 vi[combo] = bc(y);
             }
@@ -502,8 +595,8 @@ struct Gen {
     }
     uint32_t thread_smask(int m) const {
         uint32_t s = 0;
-        for (int l = 0; l < kLaneBits; ++l) s |= (uint32_t)P.stg[m].lane_s[l] << 3;
-        for (int w = 0; w < WB; ++w) s |= (uint32_t)P.stg[m].warp_s[w] << 3;
+        for (int l = 0; l < kLaneBits; ++l) s |= (uint32_t)P.stg[m].lane_s[l] << ESL;
+        for (int w = 0; w < WB; ++w) s |= (uint32_t)P.stg[m].warp_s[w] << ESL;
         return s;
     }
     // 64-bit value with large constant added, reusing bases per high part
@@ -543,7 +636,7 @@ struct Gen {
             } else {
                 br = it->second;
             }
-            L("st.shared.b64 [", br, "+", hi, "], ", a(i), ";");
+            L("st.shared.", CB, " [", br, "+", hi, "], ", a(i), ";");
         }
     }
     void smem_load(const std::string& T, uint32_t lm, const std::vector<uint32_t>& O,
@@ -561,7 +654,7 @@ struct Gen {
             } else {
                 br = it->second;
             }
-            L("ld.shared.b64 ", a(i), ", [", br, "+", hi, "];");
+            L("ld.shared.", CB, " ", a(i), ", [", br, "+", hi, "];");
         }
     }
 
@@ -683,14 +776,14 @@ struct Gen {
     // tile load (mapping m) from the tile at byte pointer `ptr` into registers <bank>0..R-1
     void reg_load(int m, const std::string& ptr, const std::string& bank) {
         std::string g = gb_of(m), ad = q();
-        L("shl.b64 ", ad, ", ", g, ", 3;");
+        L("shl.b64 ", ad, ", ", g, ", ", ESL, ";");
         L("add.s64 ", ad, ", ", ad, ", ", ptr, ";");
         Bases B;
         for (int i = 0; i < R; ++i) {
             uint64_t off = 0;
             for (int b = 0; b < RB; ++b)
                 if (i & (1 << b)) off |= 1ull << P.stg[m].reg_q[b];
-            L("ld.global.cs.b64 ", bank, i, ", ", addr64(B, ad, off * 8), ";");
+            L("ld.global.cs.", CB, " ", bank, i, ", ", addr64(B, ad, off * ES), ";");
         }
     }
 
@@ -782,7 +875,7 @@ struct Gen {
                 std::string x = q();
                 if (lo) L("xor.b64 ", x, ", ", idx, ", ", u64s(lo), ";");
                 else L("mov.b64 ", x, ", ", idx, ";");
-                L("shl.b64 ", x, ", ", x, ", 3;");
+                L("shl.b64 ", x, ", ", x, ", ", ESL, ";");
                 if (variant & 1048576) {  // timing probe: stores into a 16 MiB L2-resident window
                     std::string y = q();
                     L("add.s64 ", y, ", ", x, ", %pt;");
@@ -794,8 +887,8 @@ struct Gen {
                 }
                 it = bases.emplace(lo, std::make_pair(x, Bases{})).first;
             }
-            L((variant & 134217728) ? "st.global.wt.b64 " : (variant & 65536) ? "st.global.b64 " : "st.global.cs.b64 ",
-              addr64(it->second.second, it->second.first, hi * 8), ", ", a(i), ";");
+            L((variant & 134217728) ? "st.global.wt." : (variant & 65536) ? "st.global." : "st.global.cs.", CB, " ",
+              addr64(it->second.second, it->second.first, hi * ES), ", ", a(i), ";");
         }
     }
     bool stored = false;
@@ -823,7 +916,7 @@ struct Gen {
             } else {
                 const std::string rest = prod(c & (c - 1));
                 auto [er2, ei2] = split_bc(run[k0].second);
-                v = q();
+                v = cv();
                 c_mul(v, rest, er2, ei2);
             }
             f[c] = v;
@@ -881,27 +974,25 @@ struct Gen {
             }
         }
         if (S.tph_end > S.tph_begin && !(variant & 8)) {
-            std::string one = f(), zero = f();
-            L("mov.f32 ", one, ", 0f3F800000;");
-            L("mov.f32 ", zero, ", 0f00000000;");
+            std::string one = sv(), zero = sv();
+            L("mov.", ST, " ", one, ", ", ONE, ";");
+            L("mov.", ST, " ", zero, ", ", ZERO, ";");
             std::string ph = pack(one, zero);
             const std::string& t = TB();
             for (int e = S.tph_begin; e < S.tph_end; ++e) {
-                const Entry<float>& E = P.tph[e];
+                const Entry<Real>& E = P.tph[e];
                 std::string pc = p(), ph_ = p(), m1 = q(), m2 = q();
                 L("and.b64 ", m1, ", ", t, ", ", u64s(E.cmask), ";");
                 L("setp.eq.u64 ", pc, ", ", m1, ", ", u64s(E.cmask), ";");
                 L("and.b64 ", m2, ", ", t, ", ", u64s(E.qmask), ";");
                 L("setp.ne.u64 ", ph_, ", ", m2, ", 0;");
-                const size_t vo = off_tph + 32 * (size_t)e + 16;
-                std::string v0 = ldp_f32(vo), v1 = ldp_f32(vo + 4), v2 = ldp_f32(vo + 8), v3 = ldp_f32(vo + 12);
-                std::string vx = f(), vy = f(), np_ = q();
-                L("selp.f32 ", vx, ", ", v2, ", ", v0, ", ", ph_, ";");
-                L("selp.f32 ", vy, ", ", v3, ", ", v1, ", ", ph_, ";");
+                std::string v0 = ldp_f32(tphv(e, 0)), v1 = ldp_f32(tphv(e, 1)), v2 = ldp_f32(tphv(e, 2)),
+                            v3 = ldp_f32(tphv(e, 3));
+                std::string vx = sv(), vy = sv(), np_ = cv();
+                L("selp.", ST, " ", vx, ", ", v2, ", ", v0, ", ", ph_, ";");
+                L("selp.", ST, " ", vy, ", ", v3, ", ", v1, ", ", ph_, ";");
                 c_mul(np_, ph, bc(vx), bc(vy));
-                std::string nph = q();
-                L("selp.b64 ", nph, ", ", np_, ", ", ph, ", ", pc, ";");
-                ph = nph;
+                ph = csel(np_, ph, pc);
             }
             auto [r2, i2] = split_bc(ph);
             for (int i = 0; i < R; ++i)
@@ -947,9 +1038,9 @@ struct Gen {
             L("xor.b32 ", so, ", ", so, ", ", m2, ";");
         };
         if (lanes)
-            for (int l = 0; l < kLaneBits; ++l) add(lane, l, S.lane_q[l], (uint32_t)S.lane_s[l] << 3);
+            for (int l = 0; l < kLaneBits; ++l) add(lane, l, S.lane_q[l], (uint32_t)S.lane_s[l] << ESL);
         if (warps)
-            for (int w = 0; w < WB; ++w) add(warp, w, S.warp_q[w], (uint32_t)S.warp_s[w] << 3);
+            for (int w = 0; w < WB; ++w) add(warp, w, S.warp_q[w], (uint32_t)S.warp_s[w] << ESL);
     }
 
     std::string tb_of(int s) {  // base | rank_bits | thread bits of stage s
@@ -1038,7 +1129,7 @@ struct Gen {
         }
         L("setp.lt.u32 %pfl, ", lane, ", ", R, ";");
         if (!hoist_ops.empty()) {  // per-thread products of the thread-constant phase factors
-            L("shl.b32 %hpb, %xtid, 3;");
+            L("shl.b32 %hpb, %xtid, ", ESL, ";");
             L("add.u32 %hpb, %hpb, %smb;");
             L("add.u32 %hpb, %hpb, ", tab_hp, ";");
             std::string rk = q();
@@ -1050,7 +1141,7 @@ struct Gen {
                 thread_map(s2, lane, warp, g, so, true, true);
                 L("or.b64 ", tb, ", ", g, ", ", rk, ";");
                 std::string e = hoisted_product(s2, P.ops[oi], tb);
-                L("st.shared.b64 [%hpb+", h * (size_t)NT * 8, "], ", e, ";");
+                L("st.shared.", CB, " [%hpb+", h * (size_t)NT * ES, "], ", e, ";");
             }
             prologue_ = false;
         }
@@ -1137,7 +1228,7 @@ struct Gen {
             std::string ls = lab(), pt0 = q();
             L("setp.ge.u64 %pend, %tile, %tend;");
             L("@%pend bra.uni ", ls, ";");
-            L("shl.b64 ", pt0, ", %base, 3;");
+            L("shl.b64 ", pt0, ", %base, ", ESL, ";");
             L("add.s64 ", pt0, ", ", pt0, ", %psi;");
             reg_load(li, pt0, "%b");
             o << ls << ":\n";
@@ -1147,7 +1238,7 @@ struct Gen {
         o << "$LOOP:\n";
         L("setp.ge.u64 %pend, %tile, %tend;");
         L("@%pend bra.uni $END;");
-        L("shl.b64 %pt, %base, 3;");
+        L("shl.b64 %pt, %base, ", ESL, ";");
         L("add.s64 %pt, %pt, %psi;");
         L("add.s64 %ntile, %tile, %G;");
         L("or.b64 %nbase, %base, ", u64s(~cmask), ";");
@@ -1160,7 +1251,7 @@ struct Gen {
             for (int i = 0; i < R; ++i) L("mov.b64 ", a(i), ", %b", i, ";");
             std::string ls = lab(), pn = q();
             L("@!%pnext bra.uni ", ls, ";");
-            L("shl.b64 ", pn, ", %nbase, 3;");
+            L("shl.b64 ", pn, ", %nbase, ", ESL, ";");
             L("add.s64 ", pn, ", ", pn, ", %psi;");
             reg_load(li, pn, "%b");
             o << ls << ":\n";
@@ -1178,17 +1269,21 @@ struct Gen {
             smem_load(so_of(1), thread_smask(1), O);
             after_read();
         } else if (variant & (32 | 32768)) {  // timing probes: no global loads (wrong results)
-            for (int i = 0; i < R; ++i) L("mov.b64 ", a(i), ", 0;");
+            for (int i = 0; i < R; ++i) {
+                std::string z = sv();
+                L("mov.", ST, " ", z, ", ", ZERO, ";");
+                pack_into(a(i), z, z);
+            }
         } else {  // load (io or stage-1 mapping): thread bits and register bits are disjoint
             std::string g = gb_of(li), ad = q();
-            L("shl.b64 ", ad, ", ", g, ", 3;");
+            L("shl.b64 ", ad, ", ", g, ", ", ESL, ";");
             L("add.s64 ", ad, ", ", ad, ", %pt;");
             Bases B;
             for (int i = 0; i < R; ++i) {
                 uint64_t off = 0;
                 for (int b = 0; b < RB; ++b)
                     if (i & (1 << b)) off |= 1ull << P.stg[li].reg_q[b];
-                L((variant & 131072) ? "ld.global.b64 " : "ld.global.cs.b64 ", a(i), ", ", addr64(B, ad, off * 8), ";");
+                L((variant & 131072) ? "ld.global." : "ld.global.cs.", CB, " ", a(i), ", ", addr64(B, ad, off * ES), ";");
             }
         }
         if (!(variant & 128)) {  // warm L2 with this CTA's next tile (variant 512: the one after)
@@ -1219,15 +1314,14 @@ struct Gen {
                 L("or.b64 ", pf, ", ", a1, ", ", a2, ";");
             }
             L("or.b64 ", ad, ", ", pf, ", ", tgt, ";");
-            L("shl.b64 ", ad, ", ", ad, ", 3;");
+            L("shl.b64 ", ad, ", ", ad, ", ", ESL, ";");
             L("add.s64 ", ad, ", ", ad, ", %psi;");
             if (variant & 256) {
                 L("cp.async.bulk.prefetch.L2.global [", ad, "], 256;");
             } else if (variant & 1024) {  // 64 B granules
                 for (int o2 = 0; o2 < 256; o2 += 64) L("prefetch.global.L2 [", ad, "+", o2, "];");
-            } else {
-                L("prefetch.global.L2 [", ad, "];");
-                L("prefetch.global.L2 [", ad, "+128];");
+            } else {  // one 32-amplitude chunk: 2 (complex64) / 4 (complex128) lines
+                for (int o2 = 0; o2 < 32 * ES; o2 += 128) L("prefetch.global.L2 [", ad, "+", o2, "];");
             }
             o << ls << ":\n";
         }
@@ -1242,45 +1336,42 @@ struct Gen {
                 std::string ls = lab(), pp = p();
                 L("setp.ne.u32 ", pp, ", %xwarp, ", u % (NT / 32), ";");
                 L("@", pp, " bra.uni ", ls, ";");
-                std::string one = f(), zero = f();
-                L("mov.f32 ", one, ", 0f3F800000;");
-                L("mov.f32 ", zero, ", 0f00000000;");
+                std::string one = sv(), zero = sv();
+                L("mov.", ST, " ", one, ", ", ONE, ";");
+                L("mov.", ST, " ", zero, ", ", ZERO, ";");
                 std::string e = pack(one, zero);
                 for (int r0 = 0; r0 < cnt; r0 += 32) {
                     // entry first + r0 + lane (runtime index into the param space)
-                    std::string idx = r(), off = q(), ad = q(), pos = r(), ex = f(), ey = f();
+                    std::string idx = r(), off = q(), ad = q(), pos = r(), ex = sv(), ey = sv();
                     std::string inr = p(), on = p(), t = q(), tb = r();
                     L("setp.lt.u32 ", inr, ", %xlane, ", cnt - r0, ";");
                     L("add.u32 ", idx, ", %xlane, ", first + r0, ";");
-                    L("mul.wide.u32 ", off, ", ", idx, ", 16;");
+                    L("mul.wide.u32 ", off, ", ", idx, ", ", sizeof(PhEnt<Real>), ";");
                     L("add.s64 ", ad, ", ", pb, ", ", off, ";");
                     L("add.s64 ", ad, ", ", ad, ", ", off_ph, ";");
                     L("@", inr, " ld.param.u32 ", pos, ", [", ad, "];");
-                    L("@", inr, " ld.param.f32 ", ex, ", [", ad, "+8];");
-                    L("@", inr, " ld.param.f32 ", ey, ", [", ad, "+12];");
+                    L("@", inr, " ld.param.", ST, " ", ex, ", [", ad, "+", offsetof(PhEnt<Real>, e), "];");
+                    L("@", inr, " ld.param.", ST, " ", ey, ", [", ad, "+", offsetof(PhEnt<Real>, e) + sizeof(Real), "];");
                     L("@!", inr, " mov.u32 ", pos, ", 0;");
                     L("shr.b64 ", t, ", ", ub, ", ", pos, ";");
                     L("cvt.u32.u64 ", tb, ", ", t, ";");
                     L("and.b32 ", tb, ", ", tb, ", 1;");
                     L("setp.ne.u32 ", on, ", ", tb, ", 0;");
                     L("and.pred ", on, ", ", on, ", ", inr, ";");
-                    std::string ne = q(), ns2 = q();
+                    std::string ne = cv();
                     std::string vr = bc(ex), vi = bc(ey);
                     c_mul(ne, e, vr, vi);
-                    L("selp.b64 ", ns2, ", ", ne, ", ", e, ", ", on, ";");
-                    e = ns2;
+                    e = csel(ne, e, on);
                 }
                 for (int o2 = 16; o2; o2 >>= 1) {  // product tree over the lanes
-                    std::string ex = f(), ey = f(), sx = f(), sy = f(), ne = q();
-                    L("mov.b64 {", ex, ", ", ey, "}, ", e, ";");
-                    L("shfl.sync.bfly.b32 ", sx, ", ", ex, ", ", o2, ", 31, 0xffffffff;");
-                    L("shfl.sync.bfly.b32 ", sy, ", ", ey, ", ", o2, ", 31, 0xffffffff;");
+                    auto [ex, ey] = unpack(e);
+                    std::string sx = shfl_s(ex, o2), sy = shfl_s(ey, o2), ne = cv();
                     c_mul(ne, e, bc(sx), bc(sy));
                     e = ne;
                 }
                 std::string ad = r();
-                L("add.u32 ", ad, ", %smb, ", tab_uph + 8 * (size_t)u, ";");
-                L("@%pl0 st.shared.b64 [", ad, "], ", e, ";");
+                L("add.u32 ", ad, ", %smb, ", tab_uph + ES * (size_t)u, ";");
+                L("@%pl0 st.shared.", CB, " [", ad, "], ", e, ";");
                 o << ls << ":\n";
             }
             L("bar.sync 0;");
@@ -1371,10 +1462,11 @@ struct Gen {
         h << ".extern .shared .align 16 .b8 smem[];\n\n";
         h << ".visible .entry " << name << "(\n\t.param .align 8 .b8 P[" << sizeof(PD)
           << "],\n\t.param .u64 psi,\n\t.param .u64 rk\n)\n";
-        int min_ctas = (WB >= 4 || RB >= 6 || (variant & (2048 | 4096))) ? 1 : ((variant & 2) ? 3 : 2);
+        int min_ctas = (D || WB >= 4 || RB >= 6 || (variant & (2048 | 4096))) ? 1 : ((variant & 2) ? 3 : 2);
         if (variant & 8388608) min_ctas = 3;  // probe: three CTAs per SM (register cap 65536 / (3 x threads))
         h << ".maxntid " << NT << ", 1, 1\n.minnctapersm " << min_ctas << "\n{\n";
-        h << "\t.reg .b64 %a<" << R << ">;\n";
+        h << "\t.reg ." << CB << " %a<" << R << ">;\n";
+        h << "\t.reg .b128 %x<" << (nx + 1) << ">;\n\t.reg .f64 %d<" << (nd + 1) << ">;\n";
         if (variant & 4096) h << "\t.reg .b64 %b<" << R << ">;\n";
         h << "\t.reg .b64 %q<" << (nq + 1) << ">;\n";
         h << "\t.reg .b32 %r<" << (nr + 1) << ">;\n";
@@ -1403,18 +1495,22 @@ int jit_variant() {
     return v;
 }
 
-std::string jit_ptx_c64(const PassDesc<float>& P, int rb, int wb, int nbuf, const std::string& name) {
-    Gen g(P, rb, wb, nbuf, jit_variant());
+template <typename Real>
+std::string jit_ptx(const PassDesc<Real>& P, int rb, int wb, int nbuf, const std::string& name) {
+    Gen<Real> g(P, rb, wb, nbuf, jit_variant());
     if (const char* e = std::getenv("QG_JIT_STAGGER_NS")) g.stagger_ns = std::atoi(e);
     if (!g.supported()) return "";
     g.plan_hoist();
     return g.run(name);
 }
+template std::string jit_ptx<float>(const PassDesc<float>&, int, int, int, const std::string&);
+template std::string jit_ptx<double>(const PassDesc<double>&, int, int, int, const std::string&);
 
-size_t jit_smem_bytes(const PassDesc<float>& P, int rb, int wb, int nbuf) {
-    Gen g(P, rb, wb, nbuf, jit_variant());
+template <typename Real>
+size_t jit_smem_bytes(const PassDesc<Real>& P, int rb, int wb, int nbuf) {
+    Gen<Real> g(P, rb, wb, nbuf, jit_variant());
     g.plan_hoist();
-    return Gen::smem_bytes(P, rb, wb, nbuf, jit_variant()) + g.hoist_bytes();
+    return Gen<Real>::smem_bytes(P, rb, wb, nbuf, g.variant) + g.hoist_bytes();
 }
 
 // Process-wide cache of compiled passes keyed by their PTX text: re-planning the
@@ -1476,7 +1572,7 @@ JitModule::~JitModule() {
         if (d.lib) cudaLibraryUnload(d.lib);
 }
 
-cudaError_t launch_jit(JitKernel& k, const PassDesc<float>& P, void* psi, uint64_t rank_bits, cudaStream_t st) {
+cudaError_t launch_jit(JitKernel& k, const void* P, uint64_t n_tiles, void* psi, uint64_t rank_bits, cudaStream_t st) {
     int dv = 0;
     cudaError_t e = cudaGetDevice(&dv);
     if (e != cudaSuccess) return e;
@@ -1498,10 +1594,10 @@ cudaError_t launch_jit(JitKernel& k, const PassDesc<float>& P, void* psi, uint64
         if (e != cudaSuccess) return e;
         D.grid = sms * (occ > 0 ? occ : 1);
     }
-    const uint64_t grid = P.n_tiles < (uint64_t)D.grid ? P.n_tiles : (uint64_t)D.grid;
+    const uint64_t grid = n_tiles < (uint64_t)D.grid ? n_tiles : (uint64_t)D.grid;
     const cudaKernel_t kern = D.kern;
     lk.unlock();
-    void* args[] = {const_cast<PassDesc<float>*>(&P), &psi, &rank_bits};
+    void* args[] = {const_cast<void*>(P), &psi, &rank_bits};
     return cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)grid), dim3(k.threads), args, k.smem,
                             st);
 }
@@ -1544,14 +1640,15 @@ JitKernel* JitState::wait(int64_t i) {
     return (j && j->ok) ? j : nullptr;
 }
 
-std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int rb, int wb, int nbuf, int threads) {
+template <typename Real>
+std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<Real>>& d32, int rb, int wb, int nbuf, int threads) {
     auto S = std::make_shared<JitState>();
     const int64_t n = (int64_t)d32.size();
     S->k.resize(n);
     S->ready.assign(n, 0);
     S->t0 = std::chrono::steady_clock::now();
     if (n == 0) return S;
-    const PassDesc<float>* descs = d32.data();
+    const PassDesc<Real>* descs = d32.data();
     JitState* st = S.get();
     auto work = [st, descs, n, rb, wb, nbuf]() {
         for (;;) {
@@ -1561,8 +1658,8 @@ std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int
             auto jk = std::make_unique<JitKernel>();
             jk->name = "qg_jit_pass";
             jk->threads = 32 << wb;
-            const PassDesc<float>& P = descs[i];
-            const std::string ptx = jit_ptx_c64(P, rb, wb, nbuf, jk->name);
+            const PassDesc<Real>& P = descs[i];
+            const std::string ptx = jit_ptx(P, rb, wb, nbuf, jk->name);
             if (!ptx.empty()) {
                 jk->smem = jit_smem_bytes(P, rb, wb, nbuf);
                 if (const char* e = std::getenv("QG_JIT_SMEM_PAD")) jk->smem += (size_t)std::atol(e);  // occupancy probe
@@ -1598,5 +1695,7 @@ std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int
     for (int t = 0; t < nt; ++t) S->workers.emplace_back(work);
     return S;
 }
+template std::shared_ptr<JitState> jit_start<float>(const std::vector<PassDesc<float>>&, int, int, int, int);
+template std::shared_ptr<JitState> jit_start<double>(const std::vector<PassDesc<double>>&, int, int, int, int);
 
 }  // namespace qg

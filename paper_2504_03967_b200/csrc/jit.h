@@ -26,12 +26,14 @@
 
 namespace qg {
 
-// PTX for one complex64 pass on the (rb, wb, nbuf) fused-kernel configuration;
-// "" when the pass uses a feature the emitter does not cover (the interpreter
-// runs it).  `name` is the entry point.
-std::string jit_ptx_c64(const PassDesc<float>& P, int rb, int wb, int nbuf, const std::string& name);
+// PTX for one pass (complex64: PassDesc<float>, complex128: PassDesc<double>) on the
+// (rb, wb, nbuf) fused-kernel configuration; "" when the pass uses a feature the
+// emitter does not cover (the interpreter runs it).  `name` is the entry point.
+template <typename Real>
+std::string jit_ptx(const PassDesc<Real>& P, int rb, int wb, int nbuf, const std::string& name);
 // dynamic SMEM bytes the emitted kernel needs
-size_t jit_smem_bytes(const PassDesc<float>& P, int rb, int wb, int nbuf);
+template <typename Real>
+size_t jit_smem_bytes(const PassDesc<Real>& P, int rb, int wb, int nbuf);
 // PTX -> sm_100a cubin (nvPTXCompiler); false + log on failure
 bool jit_compile(const std::string& ptx, std::vector<char>& cubin, std::string& log);
 
@@ -59,7 +61,8 @@ struct JitKernel {
     std::string err;
 };
 
-cudaError_t launch_jit(JitKernel& k, const PassDesc<float>& P, void* psi, uint64_t rank_bits, cudaStream_t st);
+// P: the pass's PassDesc<float> / PassDesc<double> (the kernel parameter)
+cudaError_t launch_jit(JitKernel& k, const void* P, uint64_t n_tiles, void* psi, uint64_t rank_bits, cudaStream_t st);
 
 // Per-plan compilation: worker threads emit + compile the passes in program
 // order while the caller may already execute the first ones (wait(i) blocks
@@ -83,7 +86,8 @@ struct JitState {
     // compiled stay not-ready: only for plan destruction / rebind)
     void join(bool cancel = false);
 };
-std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<float>>& d32, int rb, int wb, int nbuf, int threads);
+template <typename Real>
+std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<Real>>& descs, int rb, int wb, int nbuf, int threads);
 int jit_default_threads();
 // passes whose cubin came from the process-wide PTX -> cubin cache (jit.cpp)
 int64_t jit_cache_hits();

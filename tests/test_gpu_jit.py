@@ -122,3 +122,30 @@ def test_tiered_jit_is_bit_identical_across_tiers():
     a, b, c = (torch.view_as_real(x.amplitudes) for x in (s1, s2, ref))
     assert torch.equal(a, c) and torch.equal(b, c)
     assert st2["n_jit"] == st["n_jit"]
+
+
+@pytest.mark.parametrize("kind", ["random", "qft", "mixed"])
+def test_jit_complex128_vs_oracle(kind):
+    """complex128 circuit-specialised kernels (f64 DFMA code, .b128 amplitudes): the
+    north_star fp64 tolerance 1e-12 against the oracle's fp64 run, and within a few
+    ulps of the interpreter kernel (a different FMA association)."""
+    n = 20
+    if kind == "random":
+        gt, gp = random_arrays(RandomSpec(n, 300, 4))
+    elif kind == "qft":
+        gt, gp = qft_arrays(n)
+    else:
+        g1, p1 = random_arrays(RandomSpec(n, 80, 5))
+        g2, p2 = qft_arrays(n)
+        gt, gp = np.concatenate([g1, g2]), np.concatenate([p1, p2])
+    ref = oracle.run_arrays(gt, gp, n, gt.shape[0], "fp64")
+    plan = sv.CompiledCircuit(gt, gp, n, "fp64", jit=1)
+    st = plan.jit_status(wait=True)
+    assert st["enabled"] == 1 and st["n_jit"] == st["n_passes"]
+    s1 = sv.init_zero_state(n, "fp64")
+    plan.execute(s1)
+    got = s1.to_numpy()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
+    s0 = sv.init_zero_state(n, "fp64")
+    sv.CompiledCircuit(gt, gp, n, "fp64", jit=-1).execute(s0)
+    assert np.linalg.norm(got - s0.to_numpy()) / np.linalg.norm(ref) <= 1e-14
