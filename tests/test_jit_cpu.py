@@ -30,7 +30,8 @@ def test_jit_policy():
     assert CompiledCircuit(g26, p26, 26, "fp32").jit_status(wait=True)["enabled"] == 2  # auto: tiered
     gt, gp = random_arrays(RandomSpec(22, 10, 0))
     assert CompiledCircuit(gt, gp, 22, "fp32").jit_status()["enabled"] == 0          # auto: small shard
-    assert CompiledCircuit(gt, gp, 22, "fp64", jit=1).jit_status()["enabled"] == 0   # complex64 only
+    assert CompiledCircuit(gt, gp, 22, "fp64", jit=1).jit_status(wait=True)["enabled"] == 1  # complex128 too
+    assert CompiledCircuit(gt, gp, 22, "fp64").jit_status()["enabled"] == 0          # auto: small shard
     assert CompiledCircuit(gt, gp, 22, "fp32", jit=-1).jit_status()["enabled"] == 0
 
 
