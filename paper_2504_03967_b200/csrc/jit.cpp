@@ -176,7 +176,15 @@ struct Gen {
     }
     size_t coefo(uint32_t c) const { return off_coef + sizeof(Real) * (size_t)c; }
     std::string lab() { return "$J" + std::to_string(nl++); }
-    std::string a(int slot) const { return "%a" + std::to_string(amap[slot]); }
+    // amplitude register of a slot: complex64 a packed .b64; complex128 a virtual name "%A<i>"
+    // standing for the f64 pair (%ar<i>, %ai<i>) — unpack / pack_into resolve it without moves
+    std::string a(int slot) const { return (D ? "%A" : "%a") + std::to_string(amap[slot]); }
+    static bool is_amp(const std::string& c) { return D && c.size() > 2 && c[0] == '%' && c[1] == 'A'; }
+    // memory-operand form of an amplitude register and the matching access type
+    std::string amem(const std::string& c) const {
+        return is_amp(c) ? "{%ar" + c.substr(2) + ", %ai" + c.substr(2) + "}" : c;
+    }
+    static constexpr const char* MT = D ? "v2.f64" : "b64";
     template <class... A>
     void L(const A&... x) {
         o << "\t";
@@ -197,6 +205,7 @@ struct Gen {
         return v;
     }
     std::pair<std::string, std::string> unpack(const std::string& c) {
+        if (is_amp(c)) return {"%ar" + c.substr(2), "%ai" + c.substr(2)};
         std::string xr = sv(), xi = sv();
         L("mov.", CB, " {", xr, ", ", xi, "}, ", c, ";");
         return {xr, xi};
@@ -215,6 +224,11 @@ struct Gen {
         return out;
     }
     void pack_into(const std::string& d, const std::string& x, const std::string& y) {
+        if (is_amp(d)) {
+            L("mov.f64 %ar", d.substr(2), ", ", x, ";");
+            L("mov.f64 %ai", d.substr(2), ", ", y, ";");
+            return;
+        }
         L("mov.", CB, " ", d, ", {", x, ", ", y, "};");
     }
     // complex value: a if pred else b
@@ -636,7 +650,7 @@ struct Gen {
             } else {
                 br = it->second;
             }
-            L("st.shared.", CB, " [", br, "+", hi, "], ", a(i), ";");
+            L("st.shared.", MT, " [", br, "+", hi, "], ", amem(a(i)), ";");
         }
     }
     void smem_load(const std::string& T, uint32_t lm, const std::vector<uint32_t>& O,
@@ -654,7 +668,7 @@ struct Gen {
             } else {
                 br = it->second;
             }
-            L("ld.shared.", CB, " ", a(i), ", [", br, "+", hi, "];");
+            L("ld.shared.", MT, " ", amem(a(i)), ", [", br, "+", hi, "];");
         }
     }
 
@@ -887,8 +901,8 @@ struct Gen {
                 }
                 it = bases.emplace(lo, std::make_pair(x, Bases{})).first;
             }
-            L((variant & 134217728) ? "st.global.wt." : (variant & 65536) ? "st.global." : "st.global.cs.", CB, " ",
-              addr64(it->second.second, it->second.first, hi * ES), ", ", a(i), ";");
+            L((variant & 134217728) ? "st.global.wt." : (variant & 65536) ? "st.global." : "st.global.cs.", MT, " ",
+              addr64(it->second.second, it->second.first, hi * ES), ", ", amem(a(i)), ";");
         }
     }
     bool stored = false;
@@ -1283,7 +1297,7 @@ struct Gen {
                 uint64_t off = 0;
                 for (int b = 0; b < RB; ++b)
                     if (i & (1 << b)) off |= 1ull << P.stg[li].reg_q[b];
-                L((variant & 131072) ? "ld.global." : "ld.global.cs.", CB, " ", a(i), ", ", addr64(B, ad, off * ES), ";");
+                L((variant & 131072) ? "ld.global." : "ld.global.cs.", MT, " ", amem(a(i)), ", ", addr64(B, ad, off * ES), ";");
             }
         }
         if (!(variant & 128)) {  // warm L2 with this CTA's next tile (variant 512: the one after)
@@ -1465,7 +1479,8 @@ struct Gen {
         int min_ctas = (D || WB >= 4 || RB >= 6 || (variant & (2048 | 4096))) ? 1 : ((variant & 2) ? 3 : 2);
         if (variant & 8388608) min_ctas = 3;  // probe: three CTAs per SM (register cap 65536 / (3 x threads))
         h << ".maxntid " << NT << ", 1, 1\n.minnctapersm " << min_ctas << "\n{\n";
-        h << "\t.reg ." << CB << " %a<" << R << ">;\n";
+        if (D) h << "\t.reg .f64 %ar<" << R << ">, %ai<" << R << ">;\n";
+        else h << "\t.reg .b64 %a<" << R << ">;\n";
         h << "\t.reg .b128 %x<" << (nx + 1) << ">;\n\t.reg .f64 %d<" << (nd + 1) << ">;\n";
         if (variant & 4096) h << "\t.reg .b64 %b<" << R << ">;\n";
         h << "\t.reg .b64 %q<" << (nq + 1) << ">;\n";
