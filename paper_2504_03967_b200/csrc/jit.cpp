@@ -1335,7 +1335,8 @@ struct Gen {
             } else if (variant & 1024) {  // 64 B granules
                 for (int o2 = 0; o2 < 256; o2 += 64) L("prefetch.global.L2 [", ad, "+", o2, "];");
             } else {  // one 32-amplitude chunk: 2 (complex64) / 4 (complex128) lines
-                for (int o2 = 0; o2 < 32 * ES; o2 += 128) L("prefetch.global.L2 [", ad, "+", o2, "];");
+                for (int o2 = 0; o2 < 32 * ES; o2 += 128)
+                    L((variant & 268435456) ? "prefetch.global.L2::evict_last [" : "prefetch.global.L2 [", ad, "+", o2, "];");
             }
             o << ls << ":\n";
         }

@@ -217,12 +217,17 @@ constexpr double kStageCost = 6.0;
 // Schedules one fused pass from `rem` (physical-qubit gates, valid order);
 // leaves the unscheduled gates in `rem` (still a valid order).
 static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int rb, int c_low, int max_stages,
-                          double max_cost, int max_gates, std::vector<int>& tile, std::vector<StageSched>& stages) {
+                          double max_cost, int max_gates, std::vector<int>& tile, std::vector<StageSched>& stages,
+                          const std::vector<int>* fixed_tile = nullptr) {
     int n_taken = 0;
     std::vector<char> in_tile(n, 0);
     tile.clear();
     stages.clear();
-    for (int q = 0; q < c_low && q < n_local; ++q) { in_tile[q] = 1; tile.push_back(q); }
+    if (fixed_tile) {  // the tile is given (lookahead choice): stages pick registers inside it
+        for (int q : *fixed_tile) { in_tile[q] = 1; tile.push_back(q); }
+    } else {
+        for (int q = 0; q < c_low && q < n_local; ++q) { in_tile[q] = 1; tile.push_back(q); }
+    }
     double cost = 0;
     // one register stage: scan `rem` in order, execute what fits, defer the rest
     auto scan = [&](int s, bool restrict_low, StageSched& st, std::vector<Gate>& keep, double& scost) {
@@ -272,7 +277,7 @@ static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int
                 keep.push_back(g);
             }
         }
-        if (st.gates.empty()) {  // undo tile growth of an empty stage
+        if (st.gates.empty() && !fixed_tile) {  // undo tile growth of an empty stage
             for (int q : tile_added) { in_tile[q] = 0; tile.erase(std::find(tile.begin(), tile.end(), q)); }
         }
     };
@@ -299,6 +304,75 @@ static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int
     for (int q = 0; q < n_local && (int)tile.size() < k; ++q)
         if (!in_tile[q]) { in_tile[q] = 1; tile.push_back(q); }
     std::sort(tile.begin(), tile.end());
+}
+
+// Gates of `rem` (valid order) one pass over tile T could run, ignoring the register /
+// stage / cost limits: a non-diagonal gate needs its target in T; blocked gates are
+// deferred with the scheduler's rules (Blocks).  The tile search's objective.
+static int tile_value(const std::vector<Gate>& rem, size_t window, const std::vector<char>& in_t, int n, int n_local) {
+    Blocks B(n);
+    int cnt = 0;
+    const size_t m = std::min(window, rem.size());
+    for (size_t i = 0; i < m; ++i) {
+        const Gate& g = rem[i];
+        if (!B.blocked(g) && (is_diag(g) || (g.t < n_local && in_t[g.t]))) {
+            ++cnt;
+            continue;
+        }
+        B.defer(g);
+    }
+    return cnt;
+}
+
+// Lookahead tile: start from the scheduler's first-come tile and swap free (non-low)
+// tile qubits for other targets of the upcoming window while the number of runnable
+// gates does not drop (deterministic pseudo-random local search).
+static std::vector<int> search_tile(const std::vector<Gate>& rem, const std::vector<int>& start, int n, int n_local,
+                                    int c_low, int iters, uint64_t seed) {
+    const size_t window = 1024;
+    std::vector<char> in_t(n, 0);
+    for (int q : start) in_t[q] = 1;
+    std::vector<int> cand;  // non-diagonal targets in the window, outside the fixed low qubits
+    {
+        std::vector<char> seen(n, 0);
+        for (size_t i = 0; i < std::min(window, rem.size()); ++i) {
+            const Gate& g = rem[i];
+            if (is_diag(g) || g.t >= n_local || g.t < c_low || seen[g.t]) continue;
+            seen[g.t] = 1;
+            cand.push_back(g.t);
+        }
+    }
+    std::vector<int> freeq;
+    for (int q : start)
+        if (q >= c_low) freeq.push_back(q);
+    if (freeq.empty() || cand.empty()) return start;
+    int best = tile_value(rem, window, in_t, n, n_local);
+    uint64_t x = seed * 0x9E3779B97F4A7C15ull + 1;
+    auto rnd = [&](uint64_t m) {
+        x ^= x << 13;
+        x ^= x >> 7;
+        x ^= x << 17;
+        return (size_t)(x % m);
+    };
+    for (int it = 0; it < iters; ++it) {
+        const size_t ia = rnd(freeq.size());
+        const int a = freeq[ia], b = cand[rnd(cand.size())];
+        if (in_t[b]) continue;
+        in_t[a] = 0;
+        in_t[b] = 1;
+        const int v = tile_value(rem, window, in_t, n, n_local);
+        if (v >= best) {
+            best = v;
+            freeq[ia] = b;
+        } else {
+            in_t[b] = 0;
+            in_t[a] = 1;
+        }
+    }
+    std::vector<int> out;
+    for (int q = 0; q < n; ++q)
+        if (in_t[q]) out.push_back(q);
+    return out;
 }
 
 // ------------------------------------------------------------------ mapping
@@ -1047,6 +1121,9 @@ int rebind_plan(qg_plan& plan, const double* gate_param, int64_t n_gates, std::s
 }
 
 // ------------------------------------------------------------------ driver
+// lookahead tile search iterations per fused pass (0 = first-come tiles; QG_DEV_TILE_SEARCH)
+static const int kTileSearch = std::getenv("QG_DEV_TILE_SEARCH") ? std::atoi(std::getenv("QG_DEV_TILE_SEARCH")) : 400;
+
 constexpr int kRemapMinPos = 10;  // 8 KiB runs (complex64) in a remap's strided blocks
 
 int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gates, int n_qubits,
@@ -1110,6 +1187,23 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
                     schedule_pass(trial, n, n_local, cfg.k(), cfg.rb, c_low, max_stages, max_cost, max_gates,
                                   tile, stages);
                     if (stages.empty()) break;
+                    if (kTileSearch > 0 && (int)tile.size() == cfg.k() && c_low > 0) {
+                        // lookahead tile: keep it when its pass schedules more gates
+                        const std::vector<int> t2 = search_tile(rem, tile, n, n_local, c_low, kTileSearch,
+                                                                plan.segs.back().size() + 7 * plan.segs.size());
+                        if (t2 != tile) {
+                            std::vector<Gate> trial2(rem);
+                            std::vector<int> tile2;
+                            std::vector<StageSched> stages2;
+                            schedule_pass(trial2, n, n_local, cfg.k(), cfg.rb, c_low, max_stages, max_cost, max_gates,
+                                          tile2, stages2, &t2);
+                            if (!stages2.empty() && trial2.size() < trial.size()) {
+                                trial.swap(trial2);
+                                tile.swap(tile2);
+                                stages.swap(stages2);
+                            }
+                        }
+                    }
                     hp = make_fused_pass(opts.dtype, cfg, n, tile, stages);
                     if (fits(opts.dtype, hp) || max_gates <= 1) { rem.swap(trial); break; }
                     max_gates = std::max(1, hp.n_gates * 3 / 4);
