@@ -329,7 +329,7 @@ static int tile_value(const std::vector<Gate>& rem, size_t window, const std::ve
 // gates does not drop (deterministic pseudo-random local search).
 static std::vector<int> search_tile(const std::vector<Gate>& rem, const std::vector<int>& start, int n, int n_local,
                                     int c_low, int iters, uint64_t seed) {
-    const size_t window = 1024;
+    static const size_t window = std::getenv("QG_DEV_TILE_WIN") ? (size_t)std::atoi(std::getenv("QG_DEV_TILE_WIN")) : 512;
     std::vector<char> in_t(n, 0);
     for (int q : start) in_t[q] = 1;
     std::vector<int> cand;  // non-diagonal targets in the window, outside the fixed low qubits
