@@ -37,6 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+DIST_BACKEND = os.environ.get("QG_DIST_BACKEND", "nccl")  # "gloo": multi-rank test mode on one GPU
 NVL_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction per GPU
 METRIC = "circuit wall-time, gates/s & HBM GB/s, 32q random-CX at 1/2/4/8 B200"
 
@@ -260,8 +261,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_2504_03967_b200 import statevec as sv
     from paper_2504_03967_b200.generators import RandomSpec, generate_random_gate_list, random_arrays
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # QG_DIST_BACKEND=gloo (a test mode): ranks may share a GPU, collectives go through host memory
+    dev_index = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    gloo = DIST_BACKEND == "gloo"
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if gloo else dev)
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
@@ -312,7 +322,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for _ in range(args.warmup):
         step(False)
     barrier()
-    clocks = ClockSampler(local_rank) if rank == 0 else None
+    clocks = ClockSampler(dev_index) if rank == 0 else None
     if clocks:
         clocks.start()
         time.sleep(0.3)
@@ -337,10 +347,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     barrier()
     clock_info = clocks.stop() if clocks else None
     remap_tot = float(np.sum(remap_ms)) / max(1, args.steps)  # per step, this rank
-    t = torch.tensor([total_ms, pass_ms, remap_tot], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, pass_ms, remap_tot = t.tolist()
+    total_ms, pass_ms, remap_tot = max_over_ranks([total_ms, pass_ms, remap_tot])
     ms_per_step = total_ms / args.steps
     gates = gt.shape[0]
     value = gates / (ms_per_step / 1000.0)
@@ -349,7 +356,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e = None
     if not args.no_e2e:
         opts = sv.SimOptions(precision=prec, shots=args.e2e_shots, rng_seed=args.seed, memory_budget=1 << 45,
-                             device=local_rank, tile_qubits=args.tile_qubits, max_stages=args.max_stages,
+                             device=dev_index, tile_qubits=args.tile_qubits, max_stages=args.max_stages,
                              max_cost=args.max_cost)
         circ = generate_random_gate_list(RandomSpec(n, args.blocks, args.seed))
         del shard
@@ -373,10 +380,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             d2h = e2e_step()
         barrier()
         e2e_ms = (time.perf_counter() - w0) * 1000.0 / max(1, args.e2e_steps)
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        if dist is not None:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = tt.item()
+        e2e_ms = max_over_ranks([e2e_ms])[0]
         e2e = {"value": gates / (e2e_ms / 1000.0), "unit": "gates/s",
                "h2d_bytes_per_step": int(plan.info["param_bytes"] + gt.nbytes + gp.nbytes),
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
@@ -407,7 +411,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "fused_passes": int(plan.info["n_passes"]), "remaps": int(plan.info["n_remaps"]),
                    "tile_qubits": int(plan.info["tile_qubits"]), "shard_bytes": shard_bytes,
                    "jit_passes": int(jit_info["n_jit"]), "jit_compile_ms_wall": jit_info["compile_ms_wall"],
-                   "l2": "no flush needed: state >> 126 MB L2"},
+                   "l2": "no flush needed: state >> 126 MB L2",
+                   "parallelism": f"sv-shard{world}" if world > 1 else "single",
+                   **({"dist_backend": DIST_BACKEND} if world > 1 else {})},
         "hbm_gbs_step": 2.0 * shard_bytes * plan.info["n_passes"] / (ms_per_step / 1000.0) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "fused_pass_kernel",
@@ -415,7 +421,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      else "fallback 6.65 TB/s (B200_PROFILING.md)",
                      "algorithmic_bytes_per_launch": 2 * shard_bytes, "avg_launch_ms": avg_launch_ms},
         "roofline_nvl": None if not plan.remaps else {
-            "bound": "nvlink", "achieved": sum(remap_egress) / (remap_tot / 1000.0) / 1e9,
+            "bound": "nvlink" if DIST_BACKEND == "nccl" else f"{DIST_BACKEND} host staging (test mode)",
+            "achieved": sum(remap_egress) / (remap_tot / 1000.0) / 1e9,
             "peak": NVL_PEAK_GBS, "unit": "GB/s",
             "frac": sum(remap_egress) / (remap_tot / 1000.0) / 1e9 / NVL_PEAK_GBS,
             "peak_source": "B200_PROFILING.md: measured peer copy 770 GB/s per direction (900 nominal)",
@@ -493,8 +500,11 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if DIST_BACKEND == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(DIST_BACKEND)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
