@@ -853,6 +853,9 @@ struct Gen {
     // global stores of the tile through mapping si (register CX map and flips folded in)
     void store_stg(int si) {
         const StageDesc& S = P.stg[si];
+        // slot bit b's global index vector: the stage's output mapping (its register CX
+        // relabels), or its input mapping when the registers were transposed into it
+        auto vec = [&](int b) { return st_in_ ? (1ull << S.reg_q[b]) : S.out_g[b]; };
         std::string g = gb_of(si);
         uint64_t lm = thread_gmask(si);
         std::string idx = g;
@@ -865,9 +868,9 @@ struct Gen {
                 L("bfe.u32 ", t, ", %F, ", b, ", 1;");
                 L("cvt.u64.u32 ", t64, ", ", t, ";");
                 L("neg.s64 ", t64, ", ", t64, ";");
-                L("and.b64 ", t64, ", ", t64, ", ", u64s(S.out_g[b]), ";");
+                L("and.b64 ", t64, ", ", t64, ", ", u64s(vec(b)), ";");
                 L("xor.b64 ", idx, ", ", idx, ", ", t64, ";");
-                lm |= S.out_g[b];
+                lm |= vec(b);
             }
         }
         std::map<uint64_t, std::pair<std::string, Bases>> bases;
@@ -875,7 +878,7 @@ struct Gen {
         for (int i = 0; i < R; ++i) {
             uint64_t og = 0;
             for (int b = 0; b < RB; ++b)
-                if (i & (1 << b)) og ^= S.out_g[b];
+                if (i & (1 << b)) og ^= vec(b);
             order.push_back({og, i});
         }
         if (variant & 2097152) std::sort(order.begin(), order.end());
@@ -903,9 +906,35 @@ struct Gen {
             }
             L((variant & 134217728) ? "st.global.wt." : (variant & 65536) ? "st.global." : "st.global.cs.", MT, " ",
               addr64(it->second.second, it->second.first, hi * ES), ", ", amem(a(i)), ";");
+            if (il_) next_load(amap[i]);
         }
     }
     bool stored = false;
+    bool st_in_ = false;  // store_stg: registers are in the stage's input mapping
+
+    // store/load interleave: the register just stored receives the next tile's amplitude of
+    // the load mapping's slot with the same register index, so the loads of tile t+1 stream
+    // while tile t's stores drain (HBM keeps reads and writes in flight together)
+    bool il_ = false;
+    std::string nld_;   // byte address of the next tile in the load mapping (this thread)
+    Bases nB_;
+    void next_load(int phys) {
+        if (nld_.empty()) {
+            std::string g = gb_of(load_map), t = q();
+            nld_ = q();
+            L("shl.b64 ", t, ", %nbase, ", ESL, ";");
+            L("add.s64 ", t, ", ", t, ", %psi;");
+            L("shl.b64 ", nld_, ", ", g, ", ", ESL, ";");
+            L("add.s64 ", nld_, ", ", nld_, ", ", t, ";");
+            nB_ = Bases{};
+        }
+        uint64_t off = 0;
+        for (int b = 0; b < RB; ++b)
+            if (phys & (1 << b)) off |= 1ull << P.stg[load_map].reg_q[b];
+        const std::string reg = (D ? "%A" : "%a") + std::to_string(phys);
+        L((variant & 131072) ? "@%pnext ld.global." : "@%pnext ld.global.cs.", MT, " ", amem(reg), ", ",
+          addr64(nB_, nld_, off * ES), ";");
+    }
 
     // a run of consecutive phase ops (slot vectors W_k, factors e_k, no flip-vector
     // mixing) as ONE multiply per slot: slot p gets the product of the e_k with
@@ -1073,11 +1102,21 @@ struct Gen {
     std::string run(const std::string& name) {
         const int ns = P.n_stages;
         const int li = P.load_direct ? 1 : 0;
-        const int si = P.store_direct ? ns : 0;
+        // variant 1073741824: stores go through the load mapping (one more transpose when the
+        // last stage's mapping differs; in-place reads and writes of a tile then share one
+        // HBM access order)
+        const int si = (variant & 1073741824) ? li : P.store_direct ? ns : 0;
         const int n_comp = 63 - __builtin_clzll(P.n_tiles);
         uint64_t cmask = 0;
         for (int i = 0; i < n_comp; ++i) cmask |= 1ull << P.comp_q[i];
         cmask_ = cmask;
+        if (std::getenv("QG_DEV_PLAN_DUMP")) {  // dev probe: io lanes of the load / store mappings
+            std::fprintf(stderr, "io ld %d st %d ns %d lanes_ld", P.load_direct, P.store_direct, ns);
+            for (int l = 0; l < kLaneBits; ++l) std::fprintf(stderr, " %d", (int)P.stg[li].lane_q[l]);
+            std::fprintf(stderr, " lanes_st");
+            for (int l = 0; l < kLaneBits; ++l) std::fprintf(stderr, " %d", (int)P.stg[si].lane_q[l]);
+            std::fprintf(stderr, "\n");
+        }
 
         // ---- prologue
         L("mov.u32 %xtid, %tid.x;");
@@ -1248,6 +1287,28 @@ struct Gen {
             o << ls << ":\n";
         }
 
+        il_ = (variant & 536870912) && !(variant & (1 | 4096 | 32 | 32768 | 16384 | 262144 | 1048576));
+        if (il_) {  // the CTA's first tile (later tiles are loaded by the previous tile's stores)
+            std::string ls = lab(), pt0 = q();
+            L("setp.ge.u64 %pend, %tile, %tend;");
+            L("@%pend bra.uni ", ls, ";");
+            L("shl.b64 ", pt0, ", %base, ", ESL, ";");
+            L("add.s64 ", pt0, ", ", pt0, ", %psi;");
+            for (int i = 0; i < R; ++i) amap[i] = i;
+            std::string g = gb_of(li), ad = q();
+            L("shl.b64 ", ad, ", ", g, ", ", ESL, ";");
+            L("add.s64 ", ad, ", ", ad, ", ", pt0, ";");
+            Bases B;
+            for (int i = 0; i < R; ++i) {
+                uint64_t off = 0;
+                for (int b = 0; b < RB; ++b)
+                    if (i & (1 << b)) off |= 1ull << P.stg[li].reg_q[b];
+                L((variant & 131072) ? "ld.global." : "ld.global.cs.", MT, " ", amem(a(i)), ", ", addr64(B, ad, off * ES),
+                  ";");
+            }
+            o << ls << ":\n";
+        }
+
         // ---- tile loop
         o << "$LOOP:\n";
         L("setp.ge.u64 %pend, %tile, %tend;");
@@ -1261,7 +1322,10 @@ struct Gen {
         L("setp.lt.u64 %pnext, %ntile, %tend;");
         first_tr = true;
         tbuf = 0;
-        if (variant & 4096) {  // this tile from the prefetch bank; the next tile's loads into it
+        nld_.clear();
+        if (il_) {
+            // this tile's registers were loaded by the previous tile's stores (or before the loop)
+        } else if (variant & 4096) {  // this tile from the prefetch bank; the next tile's loads into it
             for (int i = 0; i < R; ++i) L("mov.b64 ", a(i), ", %b", i, ";");
             std::string ls = lab(), pn = q();
             L("@!%pnext bra.uni ", ls, ";");
@@ -1457,6 +1521,7 @@ struct Gen {
         if (cur != si && !(variant & 16)) {
             transpose(cur, si);
             cur = si;
+            st_in_ = si != 0;
         }
         if ((variant & 262144) && !(variant & (32 | 16384))) {
             tma_store(si);
@@ -1464,6 +1529,7 @@ struct Gen {
             store_stg(si);
         }
         stored = false;
+        st_in_ = false;
         L("mov.u64 %tile, %ntile;");
         L("mov.u64 %base, %nbase;");
         L("bra.uni $LOOP;");
@@ -1608,6 +1674,8 @@ cudaError_t launch_jit(JitKernel& k, const void* P, uint64_t n_tiles, void* psi,
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(D.kern), k.threads,
                                                           k.smem);
         if (e != cudaSuccess) return e;
+        static const int occ_cap = std::getenv("QG_DEV_OCC") ? std::atoi(std::getenv("QG_DEV_OCC")) : 0;
+        if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;  // dev probe: CTAs per SM cap
         D.grid = sms * (occ > 0 ? occ : 1);
     }
     const uint64_t grid = n_tiles < (uint64_t)D.grid ? n_tiles : (uint64_t)D.grid;

@@ -26,6 +26,7 @@
 #include <cassert>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -1209,6 +1210,11 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
                     max_gates = std::max(1, hp.n_gates * 3 / 4);
                 }
                 if (stages.empty()) break;
+                if (std::getenv("QG_DEV_PLAN_DUMP")) {  // dev probe: tile qubits per pass
+                    std::fprintf(stderr, "tile");
+                    for (int q : tile) std::fprintf(stderr, " %d", q);
+                    std::fprintf(stderr, "\n");
+                }
                 hp.sched = stages;
                 plan.segs.back().push_back(std::move(hp));
             } else {

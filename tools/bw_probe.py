@@ -26,6 +26,14 @@ cases = {
     "r256_q16-19_28-31": [16, 17, 18, 19, 28, 29, 30, 31],
     "r256_q8-11_28-31": [8, 9, 10, 11, 28, 29, 30, 31],
     "r256_q12-17_30-31": [12, 13, 14, 15, 16, 17, 30, 31],
+    "r256_q19-26": list(range(19, 27)),
+    "r256_q21-28": list(range(21, 29)),
+    "r256_q20-23_28-31": [20, 21, 22, 23, 28, 29, 30, 31],
+    "r256_q12-15_24-27": [12, 13, 14, 15, 24, 25, 26, 27],
+    "r256_odd13-27": [13, 15, 17, 19, 21, 23, 25, 27],
+    "r256_q6_q25-31": [6] + list(range(25, 32)),
+    "r256_q7_q25-31": [7] + list(range(25, 32)),
+    "r256_q10_q25-31": [10] + list(range(25, 32)),
 }
 import os
 only = os.environ.get("QG_BW_CASES")
