@@ -323,25 +323,41 @@ __global__ void draw_kernel(const T2* __restrict__ psi, int64_t shots, const dou
     int64_t c = lo;
     while (c > 0 && bpre[c + 1] - bpre[c] <= 0.0) --c;  // rounding clamp onto a chunk with mass
     double r = target - bpre[c];
+    // two sequential scans (sub-block sums, then the sub-block's amplitudes), each
+    // reading kB values per batch with independent loads; the compare / accumulate
+    // order is the plain left-to-right loop's, so the outcome is bit-for-bit the same
+    constexpr int kB = 16;
     const int64_t nsb = ch / sb;
-    int64_t j = 0, last = -1;
+    int64_t j = nsb, last = -1;
     double acc = 0;
-    for (; j < nsb; ++j) {
-        const double v = sub[c * nsb + j];
-        if (v > 0) last = j;
-        if (acc + v > r) break;
-        acc += v;
+    for (int64_t j0 = 0; j0 < nsb && j == nsb; j0 += kB) {
+        double v[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) v[k] = j0 + k < nsb ? sub[c * nsb + j0 + k] : 0.0;
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+            if (j0 + k >= nsb) break;
+            if (v[k] > 0) last = j0 + k;
+            if (acc + v[k] > r) { j = j0 + k; break; }
+            acc += v[k];
+        }
     }
     if (j == nsb) { j = last < 0 ? nsb - 1 : last; acc -= sub[c * nsb + j]; }
     r -= acc;
     const T2* p = psi + c * ch + j * sb;
-    int64_t i = 0, lasti = -1;
+    int64_t i = sb, lasti = -1;
     double acc2 = 0;
-    for (; i < sb; ++i) {
-        const double v = prob(p[i]);
-        if (v > 0) lasti = i;
-        if (acc2 + v > r) break;
-        acc2 += v;
+    for (int64_t i0 = 0; i0 < sb && i == sb; i0 += kB) {
+        double v[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) v[k] = i0 + k < sb ? prob(p[i0 + k]) : 0.0;
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+            if (i0 + k >= sb) break;
+            if (v[k] > 0) lasti = i0 + k;
+            if (acc2 + v[k] > r) { i = i0 + k; break; }
+            acc2 += v[k];
+        }
     }
     if (i == sb) i = lasti < 0 ? sb - 1 : lasti;
     out[s] = (unsigned long long)(c * ch + j * sb + i);
@@ -371,7 +387,7 @@ cudaError_t sample_draw(const void* psi, int64_t n_amps, int dtype, int64_t shot
     const double* bpre = reinterpret_cast<const double*>(w + L.off_bpre);
     auto* draws = reinterpret_cast<unsigned long long*>(w + L.off_draw);
     auto* sorted = reinterpret_cast<unsigned long long*>(w + L.off_sorted);
-    const unsigned blocks = (unsigned)((shots + 255) / 256);
+    const unsigned blocks = (unsigned)((shots + 63) / 64);  // latency-bound threads: spread over SMs
     const double* uni = uniforms;
     const double* uni_total = nullptr;
     cudaError_t e;
@@ -388,10 +404,10 @@ cudaError_t sample_draw(const void* psi, int64_t n_amps, int dtype, int64_t shot
         uni_total = cum + shots;
     }
     if (dtype == 0)
-        draw_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(psi), shots, uni, uni_total, sub, bpre, L.n_ch,
+        draw_kernel<<<blocks, 64, 0, st>>>(static_cast<const float2*>(psi), shots, uni, uni_total, sub, bpre, L.n_ch,
                                             L.sb, L.ch, draws);
     else
-        draw_kernel<<<blocks, 256, 0, st>>>(static_cast<const double2*>(psi), shots, uni, uni_total, sub, bpre,
+        draw_kernel<<<blocks, 64, 0, st>>>(static_cast<const double2*>(psi), shots, uni, uni_total, sub, bpre,
                                             L.n_ch, L.sb, L.ch, draws);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
