@@ -65,6 +65,13 @@ struct Gen {
     int tbuf = 0;          // transpose buffer of the next transpose (variant 8192)
     bool first_tr = true;  // first transpose of the tile
     int reads_left = 0;    // SMEM buffer reads left in the tile (async loads: the last one frees it)
+    // producer/consumer mode (QG_JIT_PC): one CTA per SM = two consumer groups of NT threads
+    // (each runs alternate tiles in registers, like two CTAs) + one producer warp that fills a
+    // ring of kPcBufs SMEM tile buffers with cp.async (stage 1's input layout); per buffer a
+    // "full" mbarrier (producer -> consumers) and an "empty" one (the group's last SMEM read)
+    bool pc = false;
+    static constexpr int kPcBufs = 3;
+    size_t tab_mb = 0;     // mbarriers: full[kPcBufs], empty[kPcBufs]
     size_t off_coef, off_ph, off_tph;
     // smem layout
     size_t buf_bytes, tab_gb, tab_pf, tab_uph, tab_hp;
@@ -146,6 +153,31 @@ struct Gen {
         }
     }
     size_t hoist_bytes() const { return hoist_ops.size() * (size_t)NT * ES; }
+    static bool pc_wanted() {
+        static const bool v = std::getenv("QG_JIT_PC") && std::atoi(std::getenv("QG_JIT_PC")) > 0;
+        return v;
+    }
+    bool pc_ok() const {
+        return !D && NBUF == 1 && RB == 5 && WB == 3 && P.n_uph == 0 && P.n_stages >= 1 &&
+               !(variant & (1 | 2 | 4 | 16 | 64 | 2048 | 4096 | 8192 | 262144 | 536870912 | 1073741824 | 8388608));  // 16: the
+        // consumers' buffer release counts the transposes
+    }
+    void enable_pc() {
+        pc = true;
+        tab_mb = kPcBufs * buf_bytes;
+        tab_gb = tab_mb + 64;
+        tab_pf = tab_gb + (size_t)(P.n_stages + 1) * kMapBytes;
+        tab_uph = tab_pf + 384;
+        tab_hp = tab_uph + ES * (size_t)kMaxUph;
+    }
+    // after plan_hoist(): the producer/consumer form, when wanted, covered and within SMEM
+    bool pc_use() const {
+        return pc_wanted() && pc_ok() && pc_smem_bytes(P) + hoist_bytes() <= (size_t)225 * 1024;
+    }
+    static size_t pc_smem_bytes(const PD& P) {
+        return kPcBufs * ((size_t)ES << P.k) + 64 + (size_t)(P.n_stages + 1) * kMapBytes + 384 + ES * (size_t)kMaxUph;
+    }
+    std::string bsync() const { return pc ? "bar.sync %gbar, " + std::to_string(NT) + ";" : "bar.sync 0;"; }
     // variant 8192: transposes alternate between two SMEM tile buffers (one barrier each)
     static int tbufs(int var) { return (var & 8192) ? 2 : 1; }
     static size_t smem_bytes(const PD& P, int rb, int wb, int nbuf, int var) {
@@ -676,9 +708,9 @@ struct Gen {
     void transpose(int m1, int m2) {
         const bool two = (variant & 8192) != 0;
         if ((variant & 262144) && first_tr) L("cp.async.bulk.wait_group.read 0;");  // the last tile's stores
-        if (NBUF == 1 && (!two || first_tr)) L("bar.sync 0;");  // WAR on the buffer last read
+        if (NBUF == 1 && (!two || first_tr)) L(bsync());  // WAR on the buffer last read
         first_tr = false;
-        const std::string sb = (two && tbuf) ? std::string("%smb2") : std::string("%smb");
+        const std::string sb = pc ? std::string("%smc") : (two && tbuf) ? std::string("%smb2") : std::string("%smb");
         if (two) tbuf ^= 1;
         const StageDesc& S1 = P.stg[m1];
         std::string T = so_of(m1);
@@ -700,7 +732,7 @@ struct Gen {
             O[i] = v;
         }
         smem_store(T, lm, O, sb);
-        L("bar.sync 0;");
+        L(bsync());
         for (int i = 0; i < R; ++i) amap[i] = i;  // register renames end with the stage
         const StageDesc& S2 = P.stg[m2];
         std::string T2 = so_of(m2);
@@ -837,6 +869,15 @@ struct Gen {
     // called after each SMEM buffer read of a tile: after the last one, every
     // thread is done with the buffer and the next tile's loads may land in it
     void after_read() {
+        if (pc) {
+            if (--reads_left == 0) {
+                std::string e = r();
+                L("mad.lo.u32 ", e, ", %ib, 8, ", (unsigned)(tab_mb + 8 * kPcBufs), ";");
+                L("add.u32 ", e, ", ", e, ", %smb;");
+                L("mbarrier.arrive.shared::cta.b64 _, [", e, "];");
+            }
+            return;
+        }
         if (!(variant & 1) || --reads_left != 0) return;
         std::string ls = lab();
         L("bar.sync 0;");
@@ -1099,6 +1140,86 @@ struct Gen {
         return true;
     }
 
+    // the producer warp: fills buffer i % 3 with the CTA's tile i (mapping li's global
+    // addresses, the common swizzled SMEM layout) once the consumers released its previous
+    // contents; each lane's cp.async completions arrive on the buffer's full barrier
+    void producer(int li, const std::string& lane, int n_comp) {
+        o << "$PROD:\n";
+        const StageDesc& S = P.stg[li];
+        std::vector<std::string> gbv(1 << WB), sov(1 << WB);
+        for (int w = 0; w < (1 << WB); ++w) {
+            std::string wr = r();
+            L("mov.u32 ", wr, ", ", w, ";");
+            thread_map(li, lane, wr, gbv[w], sov[w], true, true);
+            std::string gs = q();
+            L("shl.b64 ", gs, ", ", gbv[w], ", ", ESL, ";");
+            gbv[w] = gs;
+        }
+        L("ld.param.u64 %psi, [psi];");
+        L("mov.u32 %pi, 0;");
+        o << "$PLOOP:\n";
+        std::string t = r(), t64 = q(), pp = p();
+        L("mad.lo.u32 ", t, ", %pi, %nctile, %ctile;");
+        L("cvt.u64.u32 ", t64, ", ", t, ";");
+        L("setp.ge.u64 ", pp, ", ", t64, ", ", u64s(P.n_tiles), ";");
+        L("@", pp, " bra.uni $PEND;");
+        L("rem.u32 %pb, %pi, ", kPcBufs, ";");
+        L("div.u32 %pj, %pi, ", kPcBufs, ";");
+        {  // buffer reuse: its previous tile's group is done reading it
+            std::string ls = lab(), lw = lab(), eb = r(), ph = r(), pz = p(), pw = p();
+            L("setp.eq.u32 ", pz, ", %pj, 0;");
+            L("@", pz, " bra.uni ", ls, ";");
+            L("add.u32 ", ph, ", %pj, 1;");  // (j - 1) & 1
+            L("and.b32 ", ph, ", ", ph, ", 1;");
+            L("mad.lo.u32 ", eb, ", %pb, 8, ", (unsigned)(tab_mb + 8 * kPcBufs), ";");
+            L("add.u32 ", eb, ", ", eb, ", %smb;");
+            o << lw << ":\n";
+            L("mbarrier.try_wait.parity.shared::cta.b64 ", pw, ", [", eb, "], ", ph, ";");
+            L("@!", pw, " bra.uni ", lw, ";");
+            o << ls << ":\n";
+        }
+        std::string base = deposit(t, n_comp), pt = q(), sbuf = r();
+        L("shl.b64 ", pt, ", ", base, ", ", ESL, ";");
+        L("add.s64 ", pt, ", ", pt, ", %psi;");
+        L("mad.lo.u32 ", sbuf, ", %pb, ", (unsigned)buf_bytes, ", %smb;");
+        const uint32_t lm = thread_smask(li);
+        for (int w = 0; w < (1 << WB); ++w) {
+            std::string ad = q();
+            L("add.s64 ", ad, ", ", pt, ", ", gbv[w], ";");
+            Bases B;
+            std::map<uint32_t, std::string> sb;
+            for (int i = 0; i < R; ++i) {
+                uint64_t off = 0;
+                uint32_t so = 0;
+                for (int b = 0; b < RB; ++b)
+                    if (i & (1 << b)) {
+                        off |= 1ull << S.reg_q[b];
+                        so ^= S.reg_s[b];
+                    }
+                const uint32_t lo = so & lm, hi = so & ~lm;
+                auto it = sb.find(lo);
+                if (it == sb.end()) {
+                    std::string br = r();
+                    L("xor.b32 ", br, ", ", sov[w], ", ", lo, ";");
+                    L("add.u32 ", br, ", ", br, ", ", sbuf, ";");
+                    it = sb.emplace(lo, br).first;
+                }
+                L("cp.async.ca.shared.global [", it->second, "+", hi, "], ", addr64(B, ad, off * ES), ", ", ES, ";");
+            }
+        }
+        {
+            std::string fb = r();
+            L("mad.lo.u32 ", fb, ", %pb, 8, ", (unsigned)tab_mb, ";");
+            L("add.u32 ", fb, ", ", fb, ", %smb;");
+            L("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [", fb, "];");
+        }
+        L("add.u32 %pi, %pi, 1;");
+        L("bra.uni $PLOOP;");
+        o << "$PEND:\n";
+        L("cp.async.wait_all;");
+        L("ret;");
+    }
+
     std::string run(const std::string& name) {
         const int ns = P.n_stages;
         const int li = P.load_direct ? 1 : 0;
@@ -1119,7 +1240,12 @@ struct Gen {
         }
 
         // ---- prologue
-        L("mov.u32 %xtid, %tid.x;");
+        if (pc) {  // consumers: thread index within the group (both groups share the per-thread tables)
+            L("mov.u32 %xtidf, %tid.x;");
+            L("and.b32 %xtid, %xtidf, ", NT - 1, ";");
+        } else {
+            L("mov.u32 %xtid, %tid.x;");
+        }
         std::string lane = r(), warp = r();
         L("and.b32 ", lane, ", %xtid, 31;");
         L("shr.u32 ", warp, ", %xtid, 5;");
@@ -1233,10 +1359,35 @@ struct Gen {
                 L("or.b64 %rdl, %rdl, ", t64, ";");
             }
         }
+        if (pc) {
+            std::string ls = lab(), pp = p();
+            L("setp.ne.u32 ", pp, ", %xtidf, 0;");
+            L("@", pp, " bra.uni ", ls, ";");
+            for (int b = 0; b < kPcBufs; ++b) {
+                L("mbarrier.init.shared::cta.b64 [smem+", tab_mb + 8 * b, "], 32;");             // full: producer lanes
+                L("mbarrier.init.shared::cta.b64 [smem+", tab_mb + 8 * (kPcBufs + b), "], ", NT, ";");  // empty
+            }
+            o << ls << ":\n";
+        }
         L("bar.sync 0;");
         L("mov.u32 %ctile, %ctaid.x;");
         L("mov.u32 %nctile, %nctaid.x;");
-        if (variant & 4) {  // contiguous tile ranges per CTA: consecutive tiles are adjacent runs
+        if (pc) {
+            L("setp.ge.u32 %ppr, %xtidf, ", 2 * NT, ";");
+            L("@%ppr bra.uni $PROD;");
+            std::string g = r(), t0 = r(), g2 = r();
+            L("shr.u32 ", g, ", %xtidf, ", 5 + WB, ";");
+            L("add.u32 %gbar, ", g, ", 1;");
+            L("mad.lo.u32 ", t0, ", ", g, ", %nctile, %ctile;");
+            L("shl.b32 ", g2, ", %nctile, 1;");
+            L("cvt.u64.u32 %tile, ", t0, ";");
+            L("cvt.u64.u32 %G, ", g2, ";");
+            L("mov.u64 %tend, ", u64s(P.n_tiles), ";");
+            std::string b0 = deposit(t0, n_comp), dg = deposit(g2, n_comp);
+            L("mov.u64 %base, ", b0, ";");
+            L("mov.u64 %dG, ", dg, ";");
+            L("mov.u32 %ii, ", g, ";");
+        } else if (variant & 4) {  // contiguous tile ranges per CTA: consecutive tiles are adjacent runs
             std::string c64 = q(), g64 = q(), t0 = q(), t1 = q(), t0s = r();
             L("cvt.u64.u32 ", c64, ", %ctile;");
             L("cvt.u64.u32 ", g64, ", %nctile;");
@@ -1323,7 +1474,30 @@ struct Gen {
         first_tr = true;
         tbuf = 0;
         nld_.clear();
-        if (il_) {
+        if (pc) {
+            // tile i of the CTA lives in buffer i % 3 (its (i / 3)-th fill): wait for the
+            // producer, then read stage 1's mapping straight out of the buffer
+            std::string j = r(), ph = r(), fb = r(), pp = p(), lw = lab();
+            L("rem.u32 %ib, %ii, ", kPcBufs, ";");
+            L("div.u32 ", j, ", %ii, ", kPcBufs, ";");
+            L("and.b32 ", ph, ", ", j, ", 1;");
+            L("mad.lo.u32 %smc, %ib, ", (unsigned)buf_bytes, ", %smb;");
+            L("mad.lo.u32 ", fb, ", %ib, 8, ", (unsigned)tab_mb, ";");
+            L("add.u32 ", fb, ", ", fb, ", %smb;");
+            o << lw << ":\n";
+            L("mbarrier.try_wait.parity.shared::cta.b64 ", pp, ", [", fb, "], ", ph, ";");
+            L("@!", pp, " bra.uni ", lw, ";");
+            reads_left = 1 + (ns - 1) + (P.store_direct ? 0 : 1);
+            std::vector<uint32_t> O(R);
+            for (int i = 0; i < R; ++i) {
+                uint32_t v = 0;
+                for (int b = 0; b < RB; ++b)
+                    if (i & (1 << b)) v ^= P.stg[1].reg_s[b];
+                O[i] = v;
+            }
+            smem_load(so_of(1), thread_smask(1), O, "%smc");
+            after_read();
+        } else if (il_) {
             // this tile's registers were loaded by the previous tile's stores (or before the loop)
         } else if (variant & 4096) {  // this tile from the prefetch bank; the next tile's loads into it
             for (int i = 0; i < R; ++i) L("mov.b64 ", a(i), ", %b", i, ";");
@@ -1364,7 +1538,7 @@ struct Gen {
                 L((variant & 131072) ? "ld.global." : "ld.global.cs.", MT, " ", amem(a(i)), ", ", addr64(B, ad, off * ES), ";");
             }
         }
-        if (!(variant & 128)) {  // warm L2 with this CTA's next tile (variant 512: the one after)
+        if (!(variant & 128) && !pc) {  // warm L2 with this CTA's next tile (variant 512: the one after)
             std::string pp = p(), pf = q(), ad = q();
             std::string tgt = "%nbase";
             if (variant & (512 | 4096)) {
@@ -1458,7 +1632,7 @@ struct Gen {
         L("mov.u32 %F, 0;");
         fposs = 0;
         for (int i = 0; i < R; ++i) amap[i] = i;
-        int cur = (variant & 1) ? 1 : li;
+        int cur = ((variant & 1) || pc) ? 1 : li;
         for (int s = 1; s <= ns; ++s) {
             const StageDesc& S = P.stg[s];
             if (cur != s && !(variant & 16)) {  // (variant 16: timing probe without transposes)
@@ -1532,10 +1706,12 @@ struct Gen {
         st_in_ = false;
         L("mov.u64 %tile, %ntile;");
         L("mov.u64 %base, %nbase;");
+        if (pc) L("add.u32 %ii, %ii, 2;");
         L("bra.uni $LOOP;");
         o << "$END:\n";
         if (variant & 262144) L("cp.async.bulk.wait_group 0;");
         L("ret;");
+        if (pc) producer(li, lane, n_comp);
 
         // ---- header
         std::ostringstream h;
@@ -1545,7 +1721,9 @@ struct Gen {
           << "],\n\t.param .u64 psi,\n\t.param .u64 rk\n)\n";
         int min_ctas = (D || WB >= 4 || RB >= 6 || (variant & (2048 | 4096))) ? 1 : ((variant & 2) ? 3 : 2);
         if (variant & 8388608) min_ctas = 3;  // probe: three CTAs per SM (register cap 65536 / (3 x threads))
-        h << ".maxntid " << NT << ", 1, 1\n.minnctapersm " << min_ctas << "\n{\n";
+        if (pc) min_ctas = 1;
+        h << ".maxntid " << (pc ? 2 * NT + 32 : NT) << ", 1, 1\n.minnctapersm " << min_ctas << "\n{\n";
+        if (pc) h << "\t.reg .b32 %xtidf, %gbar, %smc, %ii, %ib, %pi, %pb, %pj, %pt32;\n\t.reg .pred %ppr;\n";
         if (D) h << "\t.reg .f64 %ar<" << R << ">, %ai<" << R << ">;\n";
         else h << "\t.reg .b64 %a<" << R << ">;\n";
         h << "\t.reg .b128 %x<" << (nx + 1) << ">;\n\t.reg .f64 %d<" << (nd + 1) << ">;\n";
@@ -1583,6 +1761,7 @@ std::string jit_ptx(const PassDesc<Real>& P, int rb, int wb, int nbuf, const std
     if (const char* e = std::getenv("QG_JIT_STAGGER_NS")) g.stagger_ns = std::atoi(e);
     if (!g.supported()) return "";
     g.plan_hoist();
+    if (g.pc_use()) g.enable_pc();
     return g.run(name);
 }
 template std::string jit_ptx<float>(const PassDesc<float>&, int, int, int, const std::string&);
@@ -1592,7 +1771,15 @@ template <typename Real>
 size_t jit_smem_bytes(const PassDesc<Real>& P, int rb, int wb, int nbuf) {
     Gen<Real> g(P, rb, wb, nbuf, jit_variant());
     g.plan_hoist();
+    if (g.pc_use()) return Gen<Real>::pc_smem_bytes(P) + g.hoist_bytes();
     return Gen<Real>::smem_bytes(P, rb, wb, nbuf, g.variant) + g.hoist_bytes();
+}
+
+template <typename Real>
+int jit_block_threads(const PassDesc<Real>& P, int rb, int wb, int nbuf) {
+    Gen<Real> g(P, rb, wb, nbuf, jit_variant());
+    g.plan_hoist();
+    return g.pc_use() ? 2 * (32 << wb) + 32 : (32 << wb);
 }
 
 // Process-wide cache of compiled passes keyed by their PTX text: re-planning the
@@ -1741,8 +1928,8 @@ std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<Real>>& d32, int 
             const auto c0 = std::chrono::steady_clock::now();
             auto jk = std::make_unique<JitKernel>();
             jk->name = "qg_jit_pass";
-            jk->threads = 32 << wb;
             const PassDesc<Real>& P = descs[i];
+            jk->threads = jit_block_threads(P, rb, wb, nbuf);
             const std::string ptx = jit_ptx(P, rb, wb, nbuf, jk->name);
             if (!ptx.empty()) {
                 jk->smem = jit_smem_bytes(P, rb, wb, nbuf);

@@ -1190,8 +1190,11 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
                     if (stages.empty()) break;
                     if (kTileSearch > 0 && (int)tile.size() == cfg.k() && c_low > 0) {
                         // lookahead tile: keep it when its pass schedules more gates
+                        static const uint64_t seed0 =
+                            std::getenv("QG_DEV_TILE_SEED") ? std::strtoull(std::getenv("QG_DEV_TILE_SEED"), nullptr, 10) : 0;
                         const std::vector<int> t2 = search_tile(rem, tile, n, n_local, c_low, kTileSearch,
-                                                                plan.segs.back().size() + 7 * plan.segs.size());
+                                                                seed0 * 1000003 + plan.segs.back().size() +
+                                                                    7 * plan.segs.size());
                         if (t2 != tile) {
                             std::vector<Gate> trial2(rem);
                             std::vector<int> tile2;
