@@ -416,7 +416,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    **({"dist_backend": DIST_BACKEND} if world > 1 else {})},
         "hbm_gbs_step": 2.0 * shard_bytes * plan.info["n_passes"] / (ms_per_step / 1000.0) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "fused_pass_kernel",
+                     "traffic": traffic, "kernel": "qg_jit_pass (circuit-specialised fused pass)" if jit_info["n_jit"] else "fused_pass_kernel",
                      "peak_source": "MEASURED_PEAKS.json:hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                      else "fallback 6.65 TB/s (B200_PROFILING.md)",
                      "algorithmic_bytes_per_launch": 2 * shard_bytes, "avg_launch_ms": avg_launch_ms},

@@ -14,6 +14,11 @@ def g(name):
 print("dur_ms", g("gpu__time_duration.sum"), "dram_rd", g("dram__bytes_read.sum"), "dram_wr", g("dram__bytes_write.sum"),
       "inst", g("smsp__inst_executed.sum"), "regs", g("launch__registers_per_thread"),
       "ipc", g("sm__inst_executed.avg.per_cycle_active"))
+# amplitudes per launch: argv[2], else from the DRAM read bytes in GB (one read of a complex64 state)
+try:
+    amps = float(sys.argv[2]) if len(sys.argv) > 2 else float(g("dram__bytes_read.sum")) * 1e9 / 8
+except ValueError:
+    amps = 2**28
 st = []
 for i, h in enumerate(hdr):
     if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued"):
@@ -45,7 +50,6 @@ for r in rows:
         sw[m.group(2)] += s
 tot = sum(ex.values())
 tots = sum(sw.values()) or 1
-amps = float(sys.argv[2]) if len(sys.argv) > 2 else 2**28
 print(f"warp instr {tot}  per amp {tot*32/amps:.1f}")
 for op, e in ex.most_common(22):
     print(f"  {op:10s} {e/tot*100:5.1f}%  {e*32/amps:6.2f}/amp  stall {sw[op]/tots*100:5.1f}%")
