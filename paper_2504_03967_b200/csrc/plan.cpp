@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 namespace qg {
 
@@ -1124,6 +1125,18 @@ int rebind_plan(qg_plan& plan, const double* gate_param, int64_t n_gates, std::s
 // ------------------------------------------------------------------ driver
 // lookahead tile search iterations per fused pass (0 = first-come tiles; QG_DEV_TILE_SEARCH)
 static const int kTileSearch = std::getenv("QG_DEV_TILE_SEARCH") ? std::atoi(std::getenv("QG_DEV_TILE_SEARCH")) : 400;
+// independent searches per pass (different seeds, evaluated on host threads; QG_DEV_TILE_K):
+// 8 take the 32 q random circuit from 71 to 68 passes but not its time (1.232 -> 1.244 s: the
+// fewer passes carry the same gates, and a pass's time now grows with its gates), so 1
+static const int kTileStarts =
+    std::getenv("QG_DEV_TILE_K") ? std::max(1, std::atoi(std::getenv("QG_DEV_TILE_K"))) : 1;
+static int plan_threads() {
+    static const int t = [] {
+        const unsigned hw = std::thread::hardware_concurrency();
+        return hw == 0 ? 1 : (int)std::min(hw, 8u);
+    }();
+    return t;
+}
 
 constexpr int kRemapMinPos = 10;  // 8 KiB runs (complex64) in a remap's strided blocks
 
@@ -1192,21 +1205,39 @@ int build_plan(const int32_t* gate_type, const double* gate_param, int64_t n_gat
                         // lookahead tile: keep it when its pass schedules more gates
                         static const uint64_t seed0 =
                             std::getenv("QG_DEV_TILE_SEED") ? std::strtoull(std::getenv("QG_DEV_TILE_SEED"), nullptr, 10) : 0;
-                        const std::vector<int> t2 = search_tile(rem, tile, n, n_local, c_low, kTileSearch,
-                                                                seed0 * 1000003 + plan.segs.back().size() +
-                                                                    7 * plan.segs.size());
-                        if (t2 != tile) {
-                            std::vector<Gate> trial2(rem);
-                            std::vector<int> tile2;
-                            std::vector<StageSched> stages2;
-                            schedule_pass(trial2, n, n_local, cfg.k(), cfg.rb, c_low, max_stages, max_cost, max_gates,
-                                          tile2, stages2, &t2);
-                            if (!stages2.empty() && trial2.size() < trial.size()) {
-                                trial.swap(trial2);
-                                tile.swap(tile2);
-                                stages.swap(stages2);
+                        // kTileStarts independent searches (seeds j), each scheduled; the pass
+                        // keeps the one that schedules the most gates (ties: lowest j), so the
+                        // plan does not depend on how many host threads evaluate them
+                        struct Cand {
+                            std::vector<Gate> trial;
+                            std::vector<int> tile;
+                            std::vector<StageSched> stages;
+                            bool ok = false;
+                        };
+                        std::vector<Cand> cands(kTileStarts);
+                        const uint64_t sbase = seed0 * 1000003 + plan.segs.back().size() + 7 * plan.segs.size();
+                        auto eval = [&](int sj) {
+                            const std::vector<int> t2 =
+                                search_tile(rem, tile, n, n_local, c_low, kTileSearch, sbase + (uint64_t)sj * 7919);
+                            if (t2 == tile) return;
+                            Cand& c = cands[sj];
+                            c.trial = rem;
+                            schedule_pass(c.trial, n, n_local, cfg.k(), cfg.rb, c_low, max_stages, max_cost, max_gates,
+                                          c.tile, c.stages, &t2);
+                            c.ok = !c.stages.empty();
+                        };
+                        const int nth = std::min(kTileStarts, plan_threads());
+                        std::vector<std::thread> th;
+                        for (int w = 1; w < nth; ++w)
+                            th.emplace_back([&, w] { for (int sj = w; sj < kTileStarts; sj += nth) eval(sj); });
+                        for (int sj = 0; sj < kTileStarts; sj += nth) eval(sj);
+                        for (auto& t : th) t.join();
+                        for (Cand& c : cands)
+                            if (c.ok && c.trial.size() < trial.size()) {
+                                trial.swap(c.trial);
+                                tile.swap(c.tile);
+                                stages.swap(c.stages);
                             }
-                        }
                     }
                     hp = make_fused_pass(opts.dtype, cfg, n, tile, stages);
                     if (fits(opts.dtype, hp) || max_gates <= 1) { rem.swap(trial); break; }
