@@ -59,6 +59,7 @@ int jit_nbuf(const qg_plan& p) {
     // dev probe QG_DEV_JIT_CFG0: the JIT (single-buffered) also for the 16-warp complex64 tile (id 0)
     static const bool cfg0 = std::getenv("QG_DEV_JIT_CFG0") != nullptr;
     if (cfg0 && p.dtype == QG_DTYPE_C64 && p.cfg.id <= 1) return 1;
+    if (cfg0 && p.dtype == QG_DTYPE_C128 && p.cfg.id == 0) return 1;
     return p.dtype == QG_DTYPE_C64 ? (p.cfg.id >= 4 ? 1 : 2) : (p.cfg.id == 3 ? 1 : 2);
 }
 

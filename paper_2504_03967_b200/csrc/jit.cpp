@@ -1731,6 +1731,7 @@ struct Gen {
         if (pc) min_ctas = 1;
         if (!D && RB == 4 && WB == 4 && std::getenv("QG_DEV_JIT_CFG0")) min_ctas = 2;  // probe: 2 x 16 warps / SM
         if (!D && RB == 4 && WB == 3 && std::getenv("QG_DEV_JIT_CFG0")) min_ctas = 4;  // probe: 4 x 8 warps / SM
+        if (D && RB == 4 && WB == 3 && std::getenv("QG_DEV_JIT_CFG0")) min_ctas = 2;   // probe: c128, 2 x 8 warps / SM
         h << ".maxntid " << (pc ? 2 * NT + 32 : NT) << ", 1, 1\n.minnctapersm " << min_ctas << "\n{\n";
         if (pc) h << "\t.reg .b32 %xtidf, %gbar, %smc, %ii, %ib, %pi, %pb, %pj, %pt32;\n\t.reg .pred %ppr;\n";
         if (D) h << "\t.reg .f64 %ar<" << R << ">, %ai<" << R << ">;\n";
