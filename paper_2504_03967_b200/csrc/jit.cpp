@@ -1822,6 +1822,32 @@ void cache_put(const std::string& ptx, const std::shared_ptr<JitModule>& m) {
 
 int64_t jit_cache_hits() { return g_cache_hits.load(); }
 
+namespace {
+struct DescHit {
+    std::shared_ptr<JitModule> mod;
+    size_t smem = 0;
+    int threads = 0;
+};
+std::mutex g_dcache_mu;
+auto& g_dcache = *new std::unordered_map<std::string, DescHit>();
+size_t g_dcache_bytes = 0;
+bool dcache_get(const std::string& key, DescHit& out) {
+    std::lock_guard<std::mutex> lk(g_dcache_mu);
+    auto it = g_dcache.find(key);
+    if (it == g_dcache.end()) return false;
+    out = it->second;
+    return true;
+}
+void dcache_put(const std::string& key, const DescHit& h) {
+    std::lock_guard<std::mutex> lk(g_dcache_mu);
+    if (g_dcache_bytes + key.size() > ((size_t)256 << 20)) {
+        g_dcache.clear();
+        g_dcache_bytes = 0;
+    }
+    if (g_dcache.emplace(key, h).second) g_dcache_bytes += key.size();
+}
+}  // namespace
+
 bool jit_compile(const std::string& ptx, std::vector<char>& cubin, std::string& log) {
     nvPTXCompilerHandle h = nullptr;
     if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
@@ -1939,9 +1965,26 @@ std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<Real>>& d32, int 
             auto jk = std::make_unique<JitKernel>();
             jk->name = "qg_jit_pass";
             const PassDesc<Real>& P = descs[i];
-            jk->threads = jit_block_threads(P, rb, wb, nbuf);
-            const std::string ptx = jit_ptx(P, rb, wb, nbuf, jk->name);
-            if (!ptx.empty()) {
+            // descriptor-keyed level: a pass seen before (same bytes, same kernel shape and
+            // variant) reuses its module without re-emitting the PTX
+            std::string dkey(reinterpret_cast<const char*>(&P), sizeof(P));
+            {
+                const int hdr[5] = {(int)sizeof(Real), rb, wb, nbuf, jit_variant()};
+                dkey.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+            }
+            DescHit dh;
+            if (dcache_get(dkey, dh)) {
+                jk->mod = dh.mod;
+                jk->smem = dh.smem;
+                jk->threads = dh.threads;
+                jk->ok = true;
+                g_cache_hits.fetch_add(1);
+            }
+            jk->threads = jk->ok ? jk->threads : jit_block_threads(P, rb, wb, nbuf);
+            const std::string ptx = jk->ok ? std::string() : jit_ptx(P, rb, wb, nbuf, jk->name);
+            if (jk->ok) {
+                // (descriptor cache hit)
+            } else if (!ptx.empty()) {
                 jk->smem = jit_smem_bytes(P, rb, wb, nbuf);
                 if (const char* e = std::getenv("QG_JIT_SMEM_PAD")) jk->smem += (size_t)std::atol(e);  // occupancy probe
                 if (auto hit = cache_get(ptx)) {
@@ -1956,6 +1999,7 @@ std::shared_ptr<JitState> jit_start(const std::vector<PassDesc<Real>>& d32, int 
                         cache_put(ptx, m);
                     }
                 }
+                if (jk->ok) dcache_put(dkey, DescHit{jk->mod, jk->smem, jk->threads});
             } else {
                 jk->err = "pass not covered by the emitter";
             }
