@@ -259,7 +259,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     from paper_2504_03967_b200 import partition as pt
     from paper_2504_03967_b200 import statevec as sv
-    from paper_2504_03967_b200.generators import RandomSpec, generate_random_gate_list, random_arrays
+    from paper_2504_03967_b200.generators import (QftSpec, RandomSpec, build_qft, generate_random_gate_list,
+                                                   qft_arrays, random_arrays)
 
     # QG_DIST_BACKEND=gloo (a test mode): ranks may share a GPU, collectives go through host memory
     dev_index = local_rank % torch.cuda.device_count()
@@ -279,7 +280,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist = dist_mod
     n, prec = args.qubits, args.precision
     g = world.bit_length() - 1
-    gt, gp = random_arrays(RandomSpec(n, args.blocks, args.seed))
+    qft = args.circuit == "qft"  # BASELINE configs[1] (C2): QFT on n qubits, build_qft's gate order
+    gt, gp = qft_arrays(n) if qft else random_arrays(RandomSpec(n, args.blocks, args.seed))
     # circuit-specialised pass kernels for every shard size (complex64), compiled before the
     # warm-up so that every timed step runs them (at N > 1 the auto policy would tier up in the
     # background); later plans of the same circuit (the e2e leg) hit the process cubin cache
@@ -358,7 +360,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         opts = sv.SimOptions(precision=prec, shots=args.e2e_shots, rng_seed=args.seed, memory_budget=1 << 45,
                              device=dev_index, tile_qubits=args.tile_qubits, max_stages=args.max_stages,
                              max_cost=args.max_cost)
-        circ = generate_random_gate_list(RandomSpec(n, args.blocks, args.seed))
+        circ = build_qft(QftSpec(n)) if qft else generate_random_gate_list(RandomSpec(n, args.blocks, args.seed))
         del shard
         torch.cuda.empty_cache()
 
@@ -398,16 +400,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     prof = load_json(os.path.join(ROOT, "profiles", "fused_pass_traffic.json")) or {}
     traffic = prof.get(f"{n_local}q_{prec}", {}).get("dram_bytes_per_launch")
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and not qft:
         cpu = cpu_baseline_entry(n, args.cpu_sample_qubits, args.cpu_sample_blocks, args.ref_ladder)
     out = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c64" if prec == "fp32" else "c128",
-        "data": "synthetic: reference generator stream RandomSpec(32, 1000, seed 0) (PCG64), state |0..0>",
-        "config": {"workload": f"random CX-block circuit, {n} qubits, {args.blocks} blocks, "
-                               f"{'complex64' if prec == 'fp32' else 'complex128'}, {world} GPU(s)",
-                   "n_qubits": n, "blocks": args.blocks, "gates": int(gates), "seed": args.seed,
+        "data": (f"synthetic: build_qft(QftSpec({n})) gate order, state |0..0>" if qft else
+                 f"synthetic: reference generator stream RandomSpec({n}, {args.blocks}, seed {args.seed}) (PCG64), "
+                 "state |0..0>"),
+        "config": {"workload": (f"QFT, {n} qubits" if qft else
+                                f"random CX-block circuit, {n} qubits, {args.blocks} blocks") +
+                               f", {'complex64' if prec == 'fp32' else 'complex128'}, {world} GPU(s)",
+                   "n_qubits": n, "blocks": None if qft else args.blocks, "gates": int(gates), "seed": args.seed,
                    "fused_passes": int(plan.info["n_passes"]), "remaps": int(plan.info["n_remaps"]),
                    "tile_qubits": int(plan.info["tile_qubits"]), "shard_bytes": shard_bytes,
                    "jit_passes": int(jit_info["n_jit"]), "jit_compile_ms_wall": jit_info["compile_ms_wall"],
@@ -469,6 +474,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--qubits", type=int, default=32)
     ap.add_argument("--blocks", type=int, default=1000)
+    ap.add_argument("--circuit", choices=["random", "qft"], default="random")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--tile-qubits", type=int, default=0)
