@@ -178,6 +178,29 @@ struct Gen {
         return kPcBufs * ((size_t)ES << P.k) + 64 + (size_t)(P.n_stages + 1) * kMapBytes + 384 + ES * (size_t)kMaxUph;
     }
     std::string bsync() const { return pc ? "bar.sync %gbar, " + std::to_string(NT) + ";" : "bar.sync 0;"; }
+    // Scoped SMEM hand-over barriers.  Warp w of mapping m holds exactly the tile indices
+    // whose warp-position bits (StageDesc::warp_q, in order) spell w; register CX maps and
+    // flip vectors only permute register bits.  So a transpose from mapping ma to mb moves
+    // data only between warps that agree on the warp bits ma and mb share at the same
+    // index: none differ -> the warp exchanges with itself (bar.warp.sync), one differs
+    // (WB = 3) -> pairs {w, w ^ 2^j} (named barrier 1 + 4j + the pair index, 64 threads;
+    // one id per member set, so warps that drift apart never share an id across different
+    // groups), otherwise the whole CTA.  Write-after-read inside a tile needs no CTA
+    // barrier: a transpose's writers store the tile indices their own warp read in the
+    // previous transpose (same mapping).
+    bool wsync_ = false;
+    int last_dst_ = -1;  // mapping of a tile's last SMEM read (the final transpose's target)
+    std::string hand_sync(int ma, int mb) const {
+        if (!wsync_) return bsync();
+        const StageDesc &A = P.stg[ma], &B = P.stg[mb];
+        int diff = 0, dj = -1;
+        for (int j = 0; j < WB; ++j)
+            if (A.warp_q[j] != B.warp_q[j]) { ++diff; dj = j; }
+        if (std::getenv("QG_DEV_PLAN_DUMP")) std::fprintf(stderr, "handover %d -> %d: %d warp bits differ\n", ma, mb, diff);
+        if (diff == 0) return "bar.warp.sync -1;";
+        if (diff == 1 && WB == 3) return "bar.sync %gid" + std::to_string(dj) + ", 64;";
+        return bsync();
+    }
     // variant 8192: transposes alternate between two SMEM tile buffers (one barrier each)
     static int tbufs(int var) { return (var & 8192) ? 2 : 1; }
     static size_t smem_bytes(const PD& P, int rb, int wb, int nbuf, int var) {
@@ -708,7 +731,14 @@ struct Gen {
     void transpose(int m1, int m2) {
         const bool two = (variant & 8192) != 0;
         if ((variant & 262144) && first_tr) L("cp.async.bulk.wait_group.read 0;");  // the last tile's stores
-        if (NBUF == 1 && (!two || first_tr)) L(bsync());  // WAR on the buffer last read
+        // (variant 67108864: timing probe, warp-scoped barriers only — wrong results; bounds
+        // what decoupling the warps of a CTA at the transposes could gain)
+        const bool probe = (variant & 67108864) != 0;
+        if (NBUF == 1 && (!two || first_tr)) {  // WAR on the buffer last read
+            if (probe) L("bar.warp.sync -1;");
+            else if (!wsync_) L(bsync());
+            else L(first_tr ? hand_sync(last_dst_, m1) : std::string("bar.warp.sync -1;"));
+        }
         first_tr = false;
         const std::string sb = pc ? std::string("%smc") : (two && tbuf) ? std::string("%smb2") : std::string("%smb");
         if (two) tbuf ^= 1;
@@ -732,7 +762,7 @@ struct Gen {
             O[i] = v;
         }
         smem_store(T, lm, O, sb);
-        L(bsync());
+        L(probe ? std::string("bar.warp.sync -1;") : hand_sync(m1, m2));
         for (int i = 0; i < R; ++i) amap[i] = i;  // register renames end with the stage
         const StageDesc& S2 = P.stg[m2];
         std::string T2 = so_of(m2);
@@ -1253,6 +1283,28 @@ struct Gen {
         L("shr.u32 ", warp, ", %xtid, 5;");
         L("mov.u32 %xlane, ", lane, ";");
         L("mov.u32 %xwarp, ", warp, ";");
+        // scoped hand-over barriers (see hand_sync): off for the probe / alternative forms
+        // that share the buffer differently, and for tile-uniform phase slots (their
+        // per-tile table is written by one warp and read by all)
+        {
+            static const bool off = std::getenv("QG_DEV_CTA_SYNC") != nullptr;  // A/B probe
+            wsync_ = !off && !pc && NBUF == 1 && WB == 3 && P.n_uph == 0 &&
+                     !(variant & (1 | 4096 | 8192 | 262144 | 16 | 32 | 16384 | 67108864));
+            if (wsync_) {
+                int cur = li;
+                for (int s2 = 1; s2 <= ns; ++s2)
+                    if (cur != s2) { last_dst_ = s2; cur = s2; }
+                if (cur != si) last_dst_ = si;
+                for (int j = 0; j < 3; ++j) {  // 1 + 4j + (warp index without bit j)
+                    std::string lo = r(), hi = r();
+                    L("and.b32 ", lo, ", ", warp, ", ", (1 << j) - 1, ";");
+                    L("shr.u32 ", hi, ", ", warp, ", ", j + 1, ";");
+                    L("shl.b32 ", hi, ", ", hi, ", ", j, ";");
+                    L("or.b32 ", lo, ", ", lo, ", ", hi, ";");
+                    L("add.u32 %gid", j, ", ", lo, ", ", 1 + 4 * j, ";");
+                }
+            }
+        }
         L("mov.u32 %smb, smem;");
         L("add.u32 %smb2, %smb, ", buf_bytes, ";");
         // per-mapping tables of the lane and warp parts of a thread's global bits and
@@ -1742,7 +1794,7 @@ struct Gen {
         h << "\t.reg .b32 %r<" << (nr + 1) << ">;\n";
         h << "\t.reg .f32 %f<" << (nf + 1) << ">;\n";
         h << "\t.reg .pred %p<" << (np + 1) << ">;\n";
-        h << "\t.reg .b32 %xtid, %xlane, %xwarp, %smb, %smb2, %tlin, %tl8, %tw8, %tl4, %tw4, %F, %ctile, %nctile;\n";
+        h << "\t.reg .b32 %xtid, %xlane, %xwarp, %smb, %smb2, %tlin, %tl8, %tw8, %tl4, %tw4, %F, %ctile, %nctile, %gid0, %gid1, %gid2;\n";
         h << "\t.reg .b64 %rdl, %pfg;\n\t.reg .b32 %hpb;\n";
         h << "\t.reg .b64 %gbm<" << (P.n_stages + 1) << ">;\n\t.reg .b32 %som<" << (P.n_stages + 1) << ">;\n";
         h << "\t.reg .b64 %tile, %tend, %ntile, %G, %base, %nbase, %dG, %psi, %rk, %pt;\n";

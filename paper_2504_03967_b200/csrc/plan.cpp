@@ -423,6 +423,161 @@ static void assign_mapping(int dtype, const KernelCfg& cfg, const std::vector<in
         if (!used[b]) { hs.warp_tile.push_back(b); used[b] = 1; }
 }
 
+// Re-choose the warp bits of a stage (ordered) keeping its register bits: the lanes and
+// warps only decide which threads hold which thread-level tile bits, so ops, registers
+// and results do not change.  Lanes keep the stage's constraint (io: tile bits
+// 0..kIoLanes-1 pinned; otherwise conflict-free residue classes, as assign_mapping).
+static bool set_warps(int dtype, int k, HostStage& h, const std::vector<int>& W, bool io) {
+    std::vector<char> used(k, 0);
+    for (int b : h.reg_tile) used[b] = 1;
+    for (int b : W) {
+        if (b < 0 || b >= k || used[b]) return false;
+        used[b] = 1;
+    }
+    std::vector<int> lanes;
+    if (io) {
+        for (int l = 0; l < kIoLanes; ++l) {
+            if (used[l]) return false;
+            lanes.push_back(l);
+            used[l] = 1;
+        }
+    } else {
+        const int M = dtype == QG_DTYPE_C64 ? 4 : 3;
+        for (int r = 0; r < M; ++r) {
+            int pick = -1;
+            for (int b = 0; b < k && pick < 0; ++b)
+                if (!used[b] && b % M == r) pick = b;
+            if (pick < 0) return false;
+            lanes.push_back(pick);
+            used[pick] = 1;
+        }
+    }
+    for (int b = 0; b < k && (int)lanes.size() < kLaneBits; ++b)
+        if (!used[b]) { lanes.push_back(b); used[b] = 1; }
+    for (int b = 0; b < k; ++b)
+        if (!used[b]) return false;
+    h.lane_tile = lanes;
+    h.warp_tile = W;
+    return true;
+}
+
+// Sticky warp bits: consecutive mappings of a pass that place the same tile bits on the
+// same warp-index bits hand data over inside each warp at the transpose (the kernels
+// then synchronise the warp, or the warp pair when one warp bit changes, instead of
+// the CTA; jit.cpp hand_sync).  The SMEM hand-overs of a tile form a cycle over the
+// mappings (io load -> stage 0 -> ... -> last stage -> io store, the next tile's first
+// transpose waiting on the previous tile's last reads), so the warp-bit sets are chosen
+// by a DP around that cycle (cost 0 same set, 1 one bit differs, 4 otherwise), then
+// ordered so that shared bits keep their warp index.
+static void sticky_warps(int dtype, const KernelCfg& cfg, HostPass& hp, const std::vector<char>& io) {
+    const int k = cfg.k(), S = (int)hp.stages.size(), WB = cfg.wb;
+    if (WB <= 0 || S < 1) return;
+    const bool use_io = !io[0] || !io[S - 1];
+    std::vector<int> seq;  // node ids in hand-over order; S = the io mapping
+    if (use_io) seq.push_back(S);
+    for (int s = 0; s < S; ++s) seq.push_back(s);
+    const int nn = (int)seq.size();
+    if (nn < 2) return;
+    auto bits_of = [&](uint32_t m) {
+        std::vector<int> v;
+        for (int b = 0; b < k; ++b)
+            if (m >> b & 1u) v.push_back(b);
+        return v;
+    };
+    std::vector<std::vector<uint32_t>> cand(nn);
+    for (int i = 0; i < nn; ++i) {
+        const int node = seq[i];
+        for (uint32_t m = 0; m < (1u << k); ++m) {
+            if (__builtin_popcount(m) != WB) continue;
+            bool ok;
+            if (node == S) {
+                ok = (m & ((1u << kIoLanes) - 1)) == 0;
+            } else {
+                HostStage t = hp.stages[node];
+                ok = set_warps(dtype, k, t, bits_of(m), io[node]);
+            }
+            if (ok) cand[i].push_back(m);
+        }
+        if (cand[i].empty()) return;  // keep assign_mapping's choice
+    }
+    auto cost = [](uint32_t a, uint32_t b) {
+        const int d = __builtin_popcount(a ^ b) / 2;
+        return d == 0 ? 0 : d == 1 ? 1 : 4;
+    };
+    int best = 1 << 30;
+    std::vector<uint32_t> pick;
+    for (uint32_t f : cand[0]) {
+        std::vector<std::vector<int>> dp(nn), from(nn);
+        dp[0].assign(cand[0].size(), 1 << 30);
+        from[0].assign(cand[0].size(), -1);
+        for (size_t j = 0; j < cand[0].size(); ++j)
+            if (cand[0][j] == f) dp[0][j] = 0;
+        for (int i = 1; i < nn; ++i) {
+            dp[i].assign(cand[i].size(), 1 << 30);
+            from[i].assign(cand[i].size(), -1);
+            for (size_t j = 0; j < cand[i].size(); ++j)
+                for (size_t p = 0; p < cand[i - 1].size(); ++p) {
+                    if (dp[i - 1][p] >= (1 << 30)) continue;
+                    const int c = dp[i - 1][p] + cost(cand[i - 1][p], cand[i][j]);
+                    if (c < dp[i][j]) { dp[i][j] = c; from[i][j] = (int)p; }
+                }
+        }
+        for (size_t j = 0; j < cand[nn - 1].size(); ++j) {
+            if (dp[nn - 1][j] >= (1 << 30)) continue;
+            const int c = dp[nn - 1][j] + cost(cand[nn - 1][j], f);
+            if (c < best) {
+                best = c;
+                pick.assign(nn, 0);
+                int jj = (int)j;
+                for (int i = nn - 1; i >= 0; --i) {
+                    pick[i] = cand[i][jj];
+                    jj = from[i][jj];
+                }
+            }
+        }
+        if (best == 0) break;
+    }
+    if (pick.empty()) return;
+    // order: shared bits keep the previous node's warp index, new bits fill the rest
+    std::vector<int> prev;
+    for (int i = 0; i < nn; ++i) {
+        std::vector<int> W(WB, -1);
+        std::vector<int> nb;
+        for (int b : bits_of(pick[i])) {
+            int at = -1;
+            for (int j = 0; j < (int)prev.size(); ++j)
+                if (prev[j] == b) at = j;
+            if (at >= 0) W[at] = b; else nb.push_back(b);
+        }
+        for (int j = 0, t = 0; j < WB; ++j)
+            if (W[j] < 0) W[j] = nb[t++];
+        const int node = seq[i];
+        if (node == S) {
+            std::vector<char> used(k, 0);
+            for (int b : W) used[b] = 1;
+            std::vector<int> lanes, regs;
+            for (int l = 0; l < kIoLanes; ++l) { lanes.push_back(l); used[l] = 1; }
+            for (int b = kIoLanes; b < k && (int)lanes.size() < kLaneBits; ++b)
+                if (!used[b]) { lanes.push_back(b); used[b] = 1; }
+            for (int b = 0; b < k; ++b)
+                if (!used[b]) regs.push_back(b);
+            hp.io.lane_tile = lanes;
+            hp.io.warp_tile = W;
+            hp.io.reg_tile = regs;
+        } else {
+            HostStage& h = hp.stages[node];
+            if (!set_warps(dtype, k, h, W, io[node])) return;  // (cannot happen: feasibility is order-free)
+        }
+        prev = W;
+    }
+}
+
+// dev knob, off: measured on the 32 q circuit (profiles/r02i_sticky.jsonl) the sticky
+// mappings move warp bits onto low tile bits, the load / store lanes then span 32 B sectors
+// instead of 256 B runs, and the pass gets slower (22.8 vs 17.8 ms); with the scoped
+// barriers the decoupled warps are slower still (27.2 ms)
+static const bool kStickyWarps = std::getenv("QG_DEV_STICKY") ? std::atoi(std::getenv("QG_DEV_STICKY")) != 0 : false;
+
 static bool disjoint_low5(const std::vector<int>& bits) {
     for (int b : bits) if (b < kIoLanes) return false;
     return true;
@@ -806,11 +961,13 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
     const int S = (int)stages.size();
     hp.stages.resize(S);
     cd gphase(1, 0);
+    std::vector<char> io_s(S, 0);
     for (int s = 0; s < S; ++s) {
         std::vector<int> need;
         for (int q : stages[s].regs) need.push_back(tbit[q]);
         const bool compat = disjoint_low5(need);
         const bool io = compat && (s == 0 || s == S - 1);
+        io_s[s] = io;
         assign_mapping(dtype, cfg, need, io, hp.stages[s]);
         Emitter em(hp.stages[s], hp.tile_q, n, cfg.rb, gphase);
         for (const Gate& g : stages[s].gates) em.gate(g);
@@ -827,6 +984,7 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
     hp.load_direct = is_io(hp.stages[0]);
     hp.store_direct = is_io(hp.stages[S - 1]);
     assign_mapping(dtype, cfg, {}, true, hp.io);
+    if (kStickyWarps) sticky_warps(dtype, cfg, hp, io_s);
     hp.io.out_vec.assign(cfg.rb, 0);
     for (int b = 0; b < cfg.rb; ++b) hp.io.out_vec[b] = 1u << b;
     return hp;
