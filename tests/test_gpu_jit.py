@@ -149,3 +149,38 @@ def test_jit_complex128_vs_oracle(kind):
     s0 = sv.init_zero_state(n, "fp64")
     sv.CompiledCircuit(gt, gp, n, "fp64", jit=-1).execute(s0)
     assert np.linalg.norm(got - s0.to_numpy()) / np.linalg.norm(ref) <= 1e-14
+
+
+_STICKY_CHILD = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2504_03967_b200 import statevec as sv
+from paper_2504_03967_b200.generators import RandomSpec, random_arrays
+gt, gp = random_arrays(RandomSpec(24, 600, 5))
+out = []
+for jit in (-1, 1):
+    plan = sv.CompiledCircuit(gt, gp, 24, "fp32", jit=jit)
+    plan.jit_status(wait=True)
+    st = sv.init_zero_state(24, "fp32", 1 << 40)
+    plan.execute(st)
+    out.append(torch.view_as_real(st.amplitudes).clone())
+assert plan.jit_status(wait=True)["n_jit"] == plan.info["n_passes"]
+print("bitexact", torch.equal(out[0], out[1]))
+"""
+
+
+def test_scoped_barriers_bitexact_with_sticky_warps():
+    """The scoped SMEM hand-over barriers (jit.cpp hand_sync) are rarely scoped below the
+    CTA on the default plans; QG_DEV_STICKY=1 makes the planner share warp bits between
+    consecutive mappings, so most hand-overs sync a warp or a warp pair: the JIT state
+    must still equal the interpreter's bit for bit (a missing barrier shows up as a race)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QG_DEV_STICKY="1")
+    r = subprocess.run([sys.executable, "-c", _STICKY_CHILD, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "bitexact True" in r.stdout, r.stdout + r.stderr[-2000:]
