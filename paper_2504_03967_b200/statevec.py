@@ -389,9 +389,11 @@ def run_circuit(circuit, options: SimOptions | None = None):
         if any(it[0] == "ucry" for it in qcrank.collapse_ucry(gt[:nb], gp[:nb])):
             return qcrank.run_gates(gt, gp, n, options)
     _check_budget(n, options.precision, options.memory_budget)     # then TooManyQubitsError
+    # the state first, as the reference does (statevec.py:205-208): its |0..0> init runs on
+    # the device while the host plans
+    state = init_zero_state(n, options.precision, options.memory_budget, options.device)
     plan = CompiledCircuit(gt, gp, n, options.precision, 0, options.fuse, options.tile_qubits,
                            options.max_stages, options.max_cost, jit=options.jit)   # then gate errors
-    state = init_zero_state(n, options.precision, options.memory_budget, options.device)
     plan.execute(state)
     counts = None
     if options.shots > 0:
