@@ -89,7 +89,23 @@ def _compile(src: str, force: bool = True) -> str:
     return obj
 
 
+def build_counts_ext(force: bool = False) -> str:
+    """The host-side CPython helper `_counts` (csrc/counts_dict.c: the {bitstring: count} dict)."""
+    import sysconfig
+
+    src = os.path.join(CSRC, "counts_dict.c")
+    out = os.path.join(PKG, "_counts" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", "-Wall", f"-I{sysconfig.get_paths()['include']}", src, "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"gcc failed for counts_dict.c:\n{r.stdout}\n{r.stderr}")
+    return out
+
+
 def build(force: bool = False, verbose: bool = True) -> str:
+    build_counts_ext(force)
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _newest_input():
         return OUT
     os.makedirs(BUILD, exist_ok=True)

@@ -614,7 +614,16 @@ def bitstrings(idx: np.ndarray, n_qubits: int) -> list[str]:
 
 
 def counts_from_arrays(idx: np.ndarray, cnt: np.ndarray, shots: int, n_qubits: int) -> CountsTable:
-    counts = dict(zip(bitstrings(idx, n_qubits), np.asarray(cnt).tolist()))
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    cnt = np.ascontiguousarray(cnt, dtype=np.int64)
+    try:  # host-side formatting helper built with the library (csrc/counts_dict.c)
+        from ._counts import counts_dict
+    except ImportError:
+        counts_dict = None
+    if counts_dict is not None and n_qubits <= 64:
+        counts = counts_dict(idx, cnt, n_qubits)
+    else:
+        counts = dict(zip(bitstrings(idx, n_qubits), cnt.tolist()))
     return CountsTable(counts=counts, total=shots, n_qubits=n_qubits, indices=idx, values=cnt)
 
 
