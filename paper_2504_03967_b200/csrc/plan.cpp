@@ -313,14 +313,15 @@ static void schedule_pass(std::vector<Gate>& rem, int n, int n_local, int k, int
 // deferred with the scheduler's rules (Blocks).  The tile search's objective.
 static int tile_value(const std::vector<Gate>& rem, size_t window, const std::vector<char>& in_t, int n, int n_local) {
     Blocks B(n);
-    int cnt = 0;
+    int cnt = 0, n2 = 0;  // n2: qubits in state 2 (once all are, no later gate can run)
     const size_t m = std::min(window, rem.size());
-    for (size_t i = 0; i < m; ++i) {
+    for (size_t i = 0; i < m && n2 < n; ++i) {
         const Gate& g = rem[i];
         if (!B.blocked(g) && (is_diag(g) || (g.t < n_local && in_t[g.t]))) {
             ++cnt;
             continue;
         }
+        if (!is_diag(g) && B.s[g.t] != 2) ++n2;  // defer() sets a non-diagonal target to 2
         B.defer(g);
     }
     return cnt;
