@@ -280,7 +280,10 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
                     row((int64_t)s, 200, (int64_t)st.reg_tile.size(), packed, 0, 0, hdr);
                     for (const auto& o : st.ops) {
                         double m[8] = {0};
-                        if (o.kind == qg::A_RD) {  // the three shears as one real 2x2, complex layout
+                        if (o.kind == qg::A_RD && hp.scaled_rot) {  // scaled form: M = R / sigma
+                            const double k = o.m[1] == 0.0 ? 1.0 : o.m[0], t = o.m[1] == 0.0 ? o.m[0] : 1.0;
+                            m[0] = k; m[2] = -t; m[4] = t; m[6] = k;
+                        } else if (o.kind == qg::A_RD) {  // the three shears as one real 2x2, complex layout
                             const double a = o.m[0], b = o.m[1];
                             m[0] = 1 + a * b; m[2] = 2 * a + a * a * b; m[4] = b; m[6] = 1 + a * b;
                         } else {
@@ -306,6 +309,10 @@ int qg_plan_export(const qg_plan* plan, int64_t* rec, int64_t* n_rec, double* ma
                         row((int64_t)s, o.kind, t, c, o.cmask, o.qmask, m);
                     }
                     for (const auto& o : st.tph) row((int64_t)s, qg::A_TPH, -1, -1, o.cmask, o.qmask, o.m);
+                    if (s + 1 == hp.stages.size() && hp.rscale != 1.0) {  // the pass's rotation scale
+                        const double g[8] = {hp.rscale, 0.0, hp.rscale, 0.0};
+                        row((int64_t)s, qg::A_TPH, -1, -1, 0, 0, g);
+                    }
                     const bool last = si == last_seg && pi + 1 == seg.size() && s + 1 == hp.stages.size();
                     if (last && (plan->gphase_re != 1.0 || plan->gphase_im != 0.0)) {
                         const double g[8] = {plan->gphase_re, plan->gphase_im, plan->gphase_re, plan->gphase_im};

@@ -403,7 +403,64 @@ struct Gen {
                 else rfma(a(i), a(j), sa2);
             }
     }
+    // packed complex64 negation (ptxas folds it into the consuming FFMA2's operand)
+    std::string negc(const std::string& v) {
+        auto [xr, xi] = unpack(v);
+        std::string nr = sv(), ni = sv();
+        L("neg.f32 ", nr, ", ", xr, ";");
+        L("neg.f32 ", ni, ", ", xi, ";");
+        return pack(nr, ni);
+    }
+    // complex64 rotation in the planner's scaled form (plan.cpp Emitter::rotation), the same
+    // fmas as fused.cu p_rot_scaled: form 0 x' = x - k y, y' = y + k x; form 1 x' = k x - y,
+    // y' = x + k y; swapped roles (flip vector) see -k / the unit terms negated
+    void op_rd_scaled(uint32_t V, uint32_t W, uint32_t coef) {
+        const bool form1 = P.coef[coef + 1] != 0;
+        const std::string k = ldp_f32(coefo(coef));
+        const bool fl = (W & fposs) != 0;
+        const std::string fp = fl ? fpar(W) : std::string();
+        if (!form1) {
+            std::string kk = k;
+            if (fl) {
+                std::string nk0 = sv();
+                kk = sv();
+                L("neg.f32 ", nk0, ", ", k, ";");
+                L("selp.f32 ", kk, ", ", nk0, ", ", k, ", ", fp, ";");
+            }
+            std::string nkk = sv();
+            L("neg.f32 ", nkk, ", ", kk, ";");
+            const std::string kk2 = bc(kk), nkk2 = bc(nkk);
+            for (int i = 0; i < R; ++i) {
+                if (par(W & (uint32_t)i) || !in_sub(i)) continue;
+                const int j = i ^ (int)V;
+                std::string t = q();
+                L("fma.rn.f32x2 ", t, ", ", a(j), ", ", nkk2, ", ", a(i), ";");
+                L("fma.rn.f32x2 ", a(j), ", ", a(i), ", ", kk2, ", ", a(j), ";");
+                L("mov.b64 ", a(i), ", ", t, ";");
+            }
+            return;
+        }
+        const std::string k2 = bc(k);
+        for (int i = 0; i < R; ++i) {
+            if (par(W & (uint32_t)i) || !in_sub(i)) continue;
+            const int j = i ^ (int)V;
+            const std::string ny = negc(a(j));
+            std::string ax = ny, ay = a(i);
+            if (fl) {
+                ax = csel(a(j), ny, fp);           // flipped: + y
+                ay = csel(negc(a(i)), a(i), fp);   // flipped: - x
+            }
+            std::string t = q();
+            L("fma.rn.f32x2 ", t, ", ", a(i), ", ", k2, ", ", ax, ";");
+            L("fma.rn.f32x2 ", a(j), ", ", a(j), ", ", k2, ", ", ay, ";");
+            L("mov.b64 ", a(i), ", ", t, ";");
+        }
+    }
     void op_rd(uint32_t V, uint32_t W, uint32_t coef) {
+        if (!D) {
+            op_rd_scaled(V, W, coef);
+            return;
+        }
         std::string m0 = ldp_f32(coefo(coef)), m1 = ldp_f32(coefo(coef + 1));
         std::string sa = m0, sb = m1;
         if (W & fposs) {

@@ -577,6 +577,9 @@ static void sticky_warps(int dtype, const KernelCfg& cfg, HostPass& hp, const st
 // mappings move warp bits onto low tile bits, the load / store lanes then span 32 B sectors
 // instead of 256 B runs, and the pass gets slower (22.8 vs 17.8 ms); with the scoped
 // barriers the decoupled warps are slower still (27.2 ms)
+// complex64 rotations in the scaled two-FMA form (Emitter::rotation; the kernels read the RD
+// coefficients of complex64 passes in that form)
+static constexpr bool kScaledRot = true;
 static const bool kStickyWarps = std::getenv("QG_DEV_STICKY") ? std::atoi(std::getenv("QG_DEV_STICKY")) != 0 : false;
 
 static bool disjoint_low5(const std::vector<int>& bits) {
@@ -617,8 +620,10 @@ struct Emitter {
     // parity(W & v) = 1, or a CXM move) or at the stage end.
     std::vector<std::pair<uint32_t, std::vector<std::pair<uint64_t, cd>>>> sq;
     int n_cxm = 0;
-    Emitter(HostStage& h, const std::vector<int>& tq, int n, int rb_, cd& gp)
-        : hs(h), tile_q(tq), rb(rb_), gphase(gp), reg_of(n, -1), pend(h.reg_tile.size()) {
+    const bool scaled;   // complex64: rotations in the scaled two-FMA form (rotation())
+    double rscale = 1.0; // product of their factors in this stage
+    Emitter(HostStage& h, const std::vector<int>& tq, int n, int rb_, cd& gp, bool scaled_)
+        : hs(h), tile_q(tq), rb(rb_), gphase(gp), reg_of(n, -1), pend(h.reg_tile.size()), scaled(scaled_) {
         for (size_t b = 0; b < hs.reg_tile.size(); ++b) reg_of[tile_q[hs.reg_tile[b]]] = (int)b;
         for (int r = 0; r < kMaxRegBits; ++r) row[r] = 1u << r;
     }
@@ -794,12 +799,17 @@ struct Emitter {
     }
     // 2x2 on logical b: pairs along V = L e_b, roles by W = row b of L^-1; the kernel
     // has bodies for V = W = e_T, (V = e_T, W = e_T + e_C) and (V = e_T + e_C, W = e_T)
-    // Real orthogonal 2x2 (H, RY and their products) as a rotation R(psi) run as
-    // three in-place shears (Paeth: x += a y; y += b x; x += a y with a = -tan(psi/2),
-    // b = sin psi): 3 FMAs per pair instead of 4.  det -1: M = Z R(psi), the Z is
-    // queued as a phase (usually merging with later phases on the qubit); psi is
-    // folded into [-pi/2, pi/2] with R(psi + pi) = -R(psi) (sign -> global phase).
-    bool rotation(const M2& m, double& a, double& bb, bool& refl) {
+    // Real orthogonal 2x2 (H, RY and their products) as a rotation R(psi).  det -1:
+    // M = Z R(psi), the Z is queued as a phase (usually merging with later phases on the
+    // qubit); psi is folded into [-pi/2, pi/2] with R(psi + pi) = -R(psi) (sign -> global
+    // phase).  complex64 (scaled): R(psi) = sigma * M with M = [[1, -t], [t, 1]], t = tan psi,
+    // sigma = cos psi when |psi| <= pi/4 (form 0), else M = [[u, -1], [1, u]], u = cot psi,
+    // sigma = sin psi (form 1): two FMAs per pair (x' = x - t y, y' = y + t x; x' = u x - y,
+    // y' = x + u y); the factors sigma of a pass multiply into one real scale applied once at
+    // its end (HostPass::rscale; they cannot be deferred further: each is in [1/sqrt2, 1]).
+    // complex128: three in-place shears (Paeth: x += a y; y += b x; x += a y with
+    // a = -tan(psi/2), b = sin psi), 3 FMAs per pair, no scale.
+    bool rotation(const M2& m, double& a, double& bb, bool& refl, double& sigma) {
         const double m00 = m.a00.real(), m01 = m.a01.real(), m10 = m.a10.real(), m11 = m.a11.real();
         const double det = m00 * m11 - m01 * m10;
         refl = det < 0;
@@ -811,14 +821,21 @@ struct Emitter {
         if (e > 1e-12) return false;  // not orthogonal (never for products of H / RY)
         if (psi > M_PI / 2) { psi -= M_PI; gphase = -gphase; }
         else if (psi < -M_PI / 2) { psi += M_PI; gphase = -gphase; }
+        sigma = 1.0;
+        if (scaled) {
+            const double cp = std::cos(psi), sp = std::sin(psi);
+            if (std::fabs(sp) <= cp) { a = sp / cp; bb = 0.0; sigma = cp; }
+            else { a = cp / sp; bb = 1.0; sigma = sp; }
+            return true;
+        }
         a = -std::tan(psi / 2);
         bb = std::sin(psi);
         return true;
     }
     void emit_dense(int b, const M2& m) {
-        double ra = 0, rb_ = 0;
+        double ra = 0, rb_ = 0, sigma = 1.0;
         bool refl = false;
-        const bool rot = m_real(m) && rotation(m, ra, rb_, refl);
+        const bool rot = m_real(m) && rotation(m, ra, rb_, refl, sigma);
         uint32_t inv[kMaxRegBits] = {};
         inverse(inv);
         uint32_t v = col(b), w = inv[b];
@@ -847,6 +864,7 @@ struct Emitter {
         if (rot) {
             o.m[0] = ra;
             o.m[1] = rb_;
+            rscale *= sigma;
             if (refl) emit_phase(b, cd(-1, 0), 0);  // Z after the rotation
         } else {
             put(o.m, m);
@@ -962,6 +980,7 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
     const int S = (int)stages.size();
     hp.stages.resize(S);
     cd gphase(1, 0);
+    hp.scaled_rot = kScaledRot && dtype == QG_DTYPE_C64;
     std::vector<char> io_s(S, 0);
     for (int s = 0; s < S; ++s) {
         std::vector<int> need;
@@ -970,9 +989,10 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
         const bool io = compat && (s == 0 || s == S - 1);
         io_s[s] = io;
         assign_mapping(dtype, cfg, need, io, hp.stages[s]);
-        Emitter em(hp.stages[s], hp.tile_q, n, cfg.rb, gphase);
+        Emitter em(hp.stages[s], hp.tile_q, n, cfg.rb, gphase, hp.scaled_rot);
         for (const Gate& g : stages[s].gates) em.gate(g);
         em.finish();
+        hp.rscale *= em.rscale;
         hp.n_cxm += em.n_cxm;
         hp.n_gates += (int)stages[s].gates.size();
     }
@@ -1099,8 +1119,8 @@ static PassSize pass_size(const HostPass& hp) {
 template <typename Real>
 static bool fits_t(const HostPass& hp) {
     const PassSize z = pass_size(hp);
-    // one thread-phase slot is kept free for the plan's global phase
-    return z.ops + (int)hp.stages.size() <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 1 <= kMaxTph &&
+    // thread-phase slots kept free for the pass's rotation scale and the plan's global phase
+    return z.ops + (int)hp.stages.size() <= kMaxOps && z.coef <= CoefCap<Real>::value && z.tph + 2 <= kMaxTph &&
            z.phe <= kMaxPhe && z.xfe <= kMaxXfe && z.uph <= kMaxUph;
 }
 static bool fits(int dtype, const HostPass& hp) {
@@ -1221,6 +1241,7 @@ static int build_descriptors(qg_plan& plan, std::string& err) {
                 if (plan.dtype == QG_DTYPE_C64) {
                     plan.d32.emplace_back();
                     if (!build_desc<float>(hp, plan.n_local, plan.d32.back(), err)) return QG_E_INVALID_ARG;
+                    if (hp.rscale != 1.0) add_global_phase(plan.d32.back(), cd(hp.rscale, 0));
                     idx = (int64_t)plan.d32.size() - 1;
                 } else {
                     plan.d64.emplace_back();
