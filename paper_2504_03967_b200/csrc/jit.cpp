@@ -1173,7 +1173,25 @@ struct Gen {
                 default: return false;
             }
         }
-        if (S.tph_end > S.tph_begin && !(variant & 8)) {
+        if (S.tph_end == S.tph_begin + 1 && !(variant & 8) && P.tph[S.tph_begin].cmask == 0 &&
+            P.tph[S.tph_begin].qmask == 0 && P.tph[S.tph_begin].v[1] == 0 && P.tph[S.tph_begin].v[3] == 0 &&
+            P.tph[S.tph_begin].v[0] == P.tph[S.tph_begin].v[2]) {
+            // one unconditional real factor (a pass's rotation scale): a real multiply per
+            // slot, the same values as the complex multiply by (v, 0) of the general path
+            const std::string v = ldp_f32(tphv(S.tph_begin, 0));
+            for (int i = 0; i < R; ++i) {
+                if (!in_sub(i)) continue;
+                if (!D) {
+                    L("mul.rn.f32x2 ", a(i), ", ", a(i), ", ", bc(v), ";");
+                } else {
+                    auto [xr, xi] = unpack(a(i));
+                    std::string nr = dq(), ni = dq();
+                    L("mul.rn.f64 ", nr, ", ", xr, ", ", v, ";");
+                    L("mul.rn.f64 ", ni, ", ", xi, ", ", v, ";");
+                    pack_into(a(i), nr, ni);
+                }
+            }
+        } else if (S.tph_end > S.tph_begin && !(variant & 8)) {
             std::string one = sv(), zero = sv();
             L("mov.", ST, " ", one, ", ", ONE, ";");
             L("mov.", ST, " ", zero, ", ", ZERO, ";");
