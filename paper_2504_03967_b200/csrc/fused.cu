@@ -141,6 +141,30 @@ __device__ __forceinline__ void p_dense(T2 (&a)[1 << RB], const Real* __restrict
     }
 }
 
+// rotation by shears on pairs {i, i ^ V} (x = the parity(W & i) = 0 member):
+// x += a y; y += b x; x += a y — every FMA updates its own register in place
+template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
+__device__ __forceinline__ void p_rot(T2 (&a)[1 << RB], Real sa, Real sb) {
+#pragma unroll
+    for (int i = 0; i < (1 << RB); ++i) {
+        if (parity_c(W & (uint32_t)i)) continue;
+        const int j = i ^ (int)V;
+        a[i] = r_fma(a[i], a[j], sa);
+    }
+#pragma unroll
+    for (int i = 0; i < (1 << RB); ++i) {
+        if (parity_c(W & (uint32_t)i)) continue;
+        const int j = i ^ (int)V;
+        a[j] = r_fma(a[j], a[i], sb);
+    }
+#pragma unroll
+    for (int i = 0; i < (1 << RB); ++i) {
+        if (parity_c(W & (uint32_t)i)) continue;
+        const int j = i ^ (int)V;
+        a[i] = r_fma(a[i], a[j], sa);
+    }
+}
+
 // x e on the slots with parity(W & i) == P
 template <int RB, uint32_t W, int P, typename T2>
 __device__ __forceinline__ void p_phase(T2 (&a)[1 << RB], T2 e) {
@@ -216,40 +240,52 @@ __device__ __forceinline__ bool pred_ok(uint64_t tb, uint64_t m) { return (tb & 
 // are swapped), then run the compile-time body
 // rotation R(psi) as three in-place shears (planner: Emitter::rotation); a thread
 // whose roles are swapped sees X R X = R(-psi): both shear coefficients negate
-// the scaled two-FMA form (planner: Emitter::rotation), m = (k, form):
+// complex64: the scaled two-FMA form (planner: Emitter::rotation), m = (k, form):
 //   form 0: x' = x - k y, y' = y + k x        form 1: x' = k x - y, y' = x + k y
 // (R(psi) / sigma; the pass applies sigma's product once at its end).  Swapped roles see
-// R(-psi) / sigma: form 0 with -k, form 1 with the unit terms negated (g = +1 below).
+// R(-psi) / sigma: form 0 with -k, form 1 with the unit terms negated.
 // Every output is one fmaf of the inputs, as the JIT kernels compute it (bit-identical).
-__device__ __forceinline__ float fmx(float a, float b, float c) { return fmaf(a, b, c); }
-__device__ __forceinline__ double fmx(double a, double b, double c) { return fma(a, b, c); }
-template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
-__device__ __forceinline__ void p_rot_scaled(T2 (&a)[1 << RB], Real k, Real form, bool f) {
-    if (form == Real(0)) {
-        const Real kk = f ? -k : k, nk = -kk;
+template <int RB, uint32_t V, uint32_t W>
+__device__ __forceinline__ void p_rot_scaled(float2 (&a)[1 << RB], float k, float form, bool f) {
+    if (form == 0.0f) {
+        const float kk = f ? -k : k, nk = -kk;
 #pragma unroll
         for (int i = 0; i < (1 << RB); ++i) {
             if (parity_c(W & (uint32_t)i)) continue;
             const int j = i ^ (int)V;
-            const T2 x = a[i], y = a[j];
-            a[i] = T2{fmx(y.x, nk, x.x), fmx(y.y, nk, x.y)};
-            a[j] = T2{fmx(x.x, kk, y.x), fmx(x.y, kk, y.y)};
+            const float2 x = a[i], y = a[j];
+            a[i] = make_float2(fmaf(y.x, nk, x.x), fmaf(y.y, nk, x.y));
+            a[j] = make_float2(fmaf(x.x, kk, y.x), fmaf(x.y, kk, y.y));
         }
-    } else {
-        const Real g = f ? Real(1) : Real(-1);
+    } else if (!f) {
 #pragma unroll
         for (int i = 0; i < (1 << RB); ++i) {
             if (parity_c(W & (uint32_t)i)) continue;
             const int j = i ^ (int)V;
-            const T2 x = a[i], y = a[j];
-            a[i] = T2{fmx(x.x, k, g * y.x), fmx(x.y, k, g * y.y)};
-            a[j] = T2{fmx(y.x, k, -g * x.x), fmx(y.y, k, -g * x.y)};
+            const float2 x = a[i], y = a[j];
+            a[i] = make_float2(fmaf(x.x, k, -y.x), fmaf(x.y, k, -y.y));
+            a[j] = make_float2(fmaf(y.x, k, x.x), fmaf(y.y, k, x.y));
+        }
+    } else {  // swapped roles: the unit terms negate
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            if (parity_c(W & (uint32_t)i)) continue;
+            const int j = i ^ (int)V;
+            const float2 x = a[i], y = a[j];
+            a[i] = make_float2(fmaf(x.x, k, y.x), fmaf(x.y, k, y.y));
+            a[j] = make_float2(fmaf(y.x, k, -x.x), fmaf(y.y, k, -x.y));
         }
     }
 }
 template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
 __device__ __forceinline__ void op_rd(T2 (&a)[1 << RB], const Real* m, uint32_t F) {
-    p_rot_scaled<RB, V, W>(a, m[0], m[1], (bool)parity_c(W & F));
+    const bool f = parity_c(W & F);
+    if constexpr (sizeof(Real) == 4) {
+        p_rot_scaled<RB, V, W>(a, m[0], m[1], f);
+    } else {
+        const Real sa = sel(f, -m[0], m[0]), sb = sel(f, -m[1], m[1]);
+        p_rot<RB, V, W>(a, sa, sb);
+    }
 }
 template <int RB, uint32_t V, uint32_t W, typename T2, typename Real>
 __device__ __forceinline__ void op_cd(T2 (&a)[1 << RB], const Real* m, uint32_t F) {
@@ -654,8 +690,16 @@ __global__ void __launch_bounds__(32 << WB, (WB >= 4 || sizeof(Real) == 8 || RB 
                     v.y = hi ? E.v[3] : E.v[1];
                     ph = cmul(ph, v);
                 }
+                if (ph.y == Real(0)) {  // a real factor (a pass's rotation scale): the same values
 #pragma unroll
-                for (int i = 0; i < R; ++i) a[i] = cmul(a[i], ph);
+                    for (int i = 0; i < R; ++i) {
+                        a[i].x *= ph.x;
+                        a[i].y *= ph.x;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < R; ++i) a[i] = cmul(a[i], ph);
+                }
             }
         }
         if (cur != si) {

@@ -390,9 +390,19 @@ struct Gen {
     }
 
     // ---------------------------------------------------------------- ops
+    // rotation as three in-place shears on pairs {i, i ^ V}, x = parity(W & i) = 0 member
     // slot filter (variant 4194304): emit only slots with (slot & fmask) == fval
     uint32_t fmask = 0, fval = 0;
     bool in_sub(int i) const { return ((uint32_t)i & fmask) == fval; }
+    void p_rot(uint32_t V, uint32_t W, const std::string& sa2, const std::string& sb2) {
+        for (int pass = 0; pass < 3; ++pass)
+            for (int i = 0; i < R; ++i) {
+                if (par(W & (uint32_t)i) || !in_sub(i)) continue;
+                const int j = i ^ (int)V;
+                if (pass == 1) rfma(a(j), a(i), sb2);
+                else rfma(a(i), a(j), sa2);
+            }
+    }
     // packed complex64 negation (ptxas folds it into the consuming FFMA2's operand)
     std::string negc(const std::string& v) {
         auto [xr, xi] = unpack(v);
@@ -446,61 +456,23 @@ struct Gen {
             L("mov.b64 ", a(i), ", ", t, ";");
         }
     }
-    // complex128: the same fmas on the (re, im) f64 pairs
-    void op_rd_scaled_d(uint32_t V, uint32_t W, uint32_t coef) {
-        const bool form1 = P.coef[coef + 1] != 0;
-        const std::string k = ldp_f32(coefo(coef));
-        const bool fl = (W & fposs) != 0;
-        const std::string fp = fl ? fpar(W) : std::string();
-        auto neg = [&](const std::string& v) {
-            std::string t = dq();
-            L("neg.f64 ", t, ", ", v, ";");
-            return t;
-        };
-        auto fma = [&](const std::string& x, const std::string& y, const std::string& z) {
-            std::string t = dq();
-            L("fma.rn.f64 ", t, ", ", x, ", ", y, ", ", z, ";");
-            return t;
-        };
-        std::string kk = k;
-        if (!form1 && fl) {
-            kk = dq();
-            L("selp.f64 ", kk, ", ", neg(k), ", ", k, ", ", fp, ";");
-        }
-        const std::string nkk = form1 ? std::string() : neg(kk);
-        for (int i = 0; i < R; ++i) {
-            if (par(W & (uint32_t)i) || !in_sub(i)) continue;
-            const int j = i ^ (int)V;
-            auto [xr, xi] = unpack(a(i));
-            auto [yr, yi] = unpack(a(j));
-            std::string nxr, nxi, nyr, nyi;
-            if (!form1) {
-                nxr = fma(yr, nkk, xr);
-                nxi = fma(yi, nkk, xi);
-                nyr = fma(xr, kk, yr);
-                nyi = fma(xi, kk, yi);
-            } else {
-                std::string axr = neg(yr), axi = neg(yi), ayr = xr, ayi = xi;
-                if (fl) {  // flipped: x' = k x + y, y' = k y - x
-                    std::string s1 = dq(), s2 = dq(), s3 = dq(), s4 = dq();
-                    L("selp.f64 ", s1, ", ", yr, ", ", axr, ", ", fp, ";");
-                    L("selp.f64 ", s2, ", ", yi, ", ", axi, ", ", fp, ";");
-                    L("selp.f64 ", s3, ", ", neg(xr), ", ", xr, ", ", fp, ";");
-                    L("selp.f64 ", s4, ", ", neg(xi), ", ", xi, ", ", fp, ";");
-                    axr = s1; axi = s2; ayr = s3; ayi = s4;
-                }
-                nxr = fma(xr, k, axr);
-                nxi = fma(xi, k, axi);
-                nyr = fma(yr, k, ayr);
-                nyi = fma(yi, k, ayi);
-            }
-            pack_into(a(j), nyr, nyi);
-            pack_into(a(i), nxr, nxi);
-        }
-    }
     void op_rd(uint32_t V, uint32_t W, uint32_t coef) {
-        if (D) op_rd_scaled_d(V, W, coef);
-        else op_rd_scaled(V, W, coef);
+        if (!D) {
+            op_rd_scaled(V, W, coef);
+            return;
+        }
+        std::string m0 = ldp_f32(coefo(coef)), m1 = ldp_f32(coefo(coef + 1));
+        std::string sa = m0, sb = m1;
+        if (W & fposs) {
+            std::string fp = fpar(W), n0 = sv(), n1 = sv();
+            sa = sv();
+            sb = sv();
+            L("neg.", ST, " ", n0, ", ", m0, ";");
+            L("neg.", ST, " ", n1, ", ", m1, ";");
+            L("selp.", ST, " ", sa, ", ", n0, ", ", m0, ", ", fp, ";");
+            L("selp.", ST, " ", sb, ", ", n1, ", ", m1, ", ", fp, ";");
+        }
+        p_rot(V, W, bc(sa), bc(sb));
     }
     void op_cd(uint32_t V, uint32_t W, uint32_t coef) {
         std::string m[8];

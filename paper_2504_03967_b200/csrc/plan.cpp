@@ -577,8 +577,8 @@ static void sticky_warps(int dtype, const KernelCfg& cfg, HostPass& hp, const st
 // mappings move warp bits onto low tile bits, the load / store lanes then span 32 B sectors
 // instead of 256 B runs, and the pass gets slower (22.8 vs 17.8 ms); with the scoped
 // barriers the decoupled warps are slower still (27.2 ms)
-// rotations in the scaled two-FMA form (Emitter::rotation; the kernels read the RD
-// coefficients in that form)
+// complex64 rotations in the scaled two-FMA form (Emitter::rotation; the kernels read the RD
+// coefficients of complex64 passes in that form)
 static constexpr bool kScaledRot = true;
 static const bool kStickyWarps = std::getenv("QG_DEV_STICKY") ? std::atoi(std::getenv("QG_DEV_STICKY")) != 0 : false;
 
@@ -802,13 +802,13 @@ struct Emitter {
     // Real orthogonal 2x2 (H, RY and their products) as a rotation R(psi).  det -1:
     // M = Z R(psi), the Z is queued as a phase (usually merging with later phases on the
     // qubit); psi is folded into [-pi/2, pi/2] with R(psi + pi) = -R(psi) (sign -> global
-    // phase).  Scaled (both precisions): R(psi) = sigma * M with M = [[1, -t], [t, 1]], t = tan psi,
+    // phase).  complex64 (scaled): R(psi) = sigma * M with M = [[1, -t], [t, 1]], t = tan psi,
     // sigma = cos psi when |psi| <= pi/4 (form 0), else M = [[u, -1], [1, u]], u = cot psi,
     // sigma = sin psi (form 1): two FMAs per pair (x' = x - t y, y' = y + t x; x' = u x - y,
     // y' = x + u y); the factors sigma of a pass multiply into one real scale applied once at
     // its end (HostPass::rscale; they cannot be deferred further: each is in [1/sqrt2, 1]).
-    // (scaled = false: three in-place shears, Paeth: x += a y; y += b x; x += a y with
-    // a = -tan(psi/2), b = sin psi, 3 FMAs per pair, no scale; export / tools only.)
+    // complex128: three in-place shears (Paeth: x += a y; y += b x; x += a y with
+    // a = -tan(psi/2), b = sin psi), 3 FMAs per pair, no scale.
     bool rotation(const M2& m, double& a, double& bb, bool& refl, double& sigma) {
         const double m00 = m.a00.real(), m01 = m.a01.real(), m10 = m.a10.real(), m11 = m.a11.real();
         const double det = m00 * m11 - m01 * m10;
@@ -980,7 +980,7 @@ static HostPass make_fused_pass(int dtype, const KernelCfg& cfg, int n, const st
     const int S = (int)stages.size();
     hp.stages.resize(S);
     cd gphase(1, 0);
-    hp.scaled_rot = kScaledRot;
+    hp.scaled_rot = kScaledRot && dtype == QG_DTYPE_C64;
     std::vector<char> io_s(S, 0);
     for (int s = 0; s < S; ++s) {
         std::vector<int> need;
@@ -1246,7 +1246,6 @@ static int build_descriptors(qg_plan& plan, std::string& err) {
                 } else {
                     plan.d64.emplace_back();
                     if (!build_desc<double>(hp, plan.n_local, plan.d64.back(), err)) return QG_E_INVALID_ARG;
-                    if (hp.rscale != 1.0) add_global_phase(plan.d64.back(), cd(hp.rscale, 0));
                     idx = (int64_t)plan.d64.size() - 1;
                 }
                 last_desc = idx;

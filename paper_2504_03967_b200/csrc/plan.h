@@ -74,7 +74,7 @@ struct HostPass {
     Gate gate{};                      // unfused: the gate
     double gph_re = 1.0, gph_im = 0.0; // global phase factored out of this pass's diagonal ops
     bool scaled_rot = false;          // RD coefficients in the scaled form (Emitter::rotation)
-    double rscale = 1.0;              // product of the scaled rotations' factors (applied
+    double rscale = 1.0;              // complex64: product of the scaled rotations' factors (applied
                                       // once, as an unconditional thread-phase entry at the pass end)
 };
 
